@@ -1,0 +1,98 @@
+/*
+ * symqoc_b200.h -- C ABI of the B200 GRAPE fidelity+gradient engine.
+ *
+ * Drop-in boundary for the reference's hot path
+ *   symqoc.qoc.gradient(psi0, psi_f, bx, by, backend, tau) -> (gx, gy, P)
+ *   (/root/reference/pkg/src/symqoc/qoc.py:137-168)
+ * generalised to many symmetry blocks, K controls, the gate-fidelity
+ * objective and a batch of control vectors.
+ *
+ * Plain pointers and sizes only.  Complex numbers are interleaved
+ * (re, im) float64 pairs, matrices row-major.  Controls are laid out
+ * u[b][k][j] (batch, control, slice), exactly like the gradient.
+ *
+ * Error convention (reference: ValueError / DimensionError for bad shapes,
+ * FloatingPointError for non-finite P, qoc.py:191-192, pauli.py:24-25):
+ * every entry point returns an SQOC_* status; sqoc_last_error() gives the
+ * message of the last failure on the calling thread.
+ */
+#ifndef SYMQOC_B200_H
+#define SYMQOC_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SQOC_ABI_VERSION 1
+
+enum sqoc_status {
+  SQOC_OK = 0,
+  SQOC_ERR_ARG = 1,         /* bad argument / shape  (-> ValueError)          */
+  SQOC_ERR_NONFINITE = 2,   /* non-finite F or grad  (-> FloatingPointError)  */
+  SQOC_ERR_CUDA = 3,        /* CUDA runtime failure  (-> RuntimeError)        */
+  SQOC_ERR_UNSUPPORTED = 4, /* block size / feature not built (-> RuntimeError) */
+  SQOC_ERR_NCCL = 5         /* collective failure    (-> RuntimeError)        */
+};
+
+enum sqoc_objective {
+  SQOC_OBJ_STATE = 0, /* tau_b = <psi_f|X_N|psi_0>, F = sum_b w_b |tau_b|^2          */
+  SQOC_OBJ_GATE = 1   /* tau_b = Tr(V_b^dag X_N),   F = sum_b w_b |tau_b|^2, w_b default 1/(N_B d_b^2) */
+};
+
+enum sqoc_memory {
+  SQOC_MEM_HOST = 0,  /* u / F / grad / tau are host pointers (copies inside the call) */
+  SQOC_MEM_DEVICE = 1 /* u / F / grad / tau are device pointers on the problem's GPU   */
+};
+
+typedef struct sqoc_problem sqoc_problem;
+
+/* Upload one problem (setup, once): per-block generators and targets.
+ *   dims[b]            block dimension d_b
+ *   h0[b]              d_b x d_b complex (2 d_b^2 doubles), Hermitian
+ *   hk[b]              n_controls consecutive d_b x d_b complex matrices
+ *   initial[b]         state objective: psi_0 (2 d_b doubles); gate: NULL
+ *   target[b]          state: psi_f (2 d_b doubles); gate: V_b (2 d_b^2 doubles)
+ *   weights            n_blocks doubles, or NULL for the objective's default
+ *   n_slices, dt       piecewise-constant grid (TimeGrid, propagate.py:25-41)
+ *   max_batch          largest batch passed to sqoc_eval
+ * Replaces: propagate.Backend.__init__ (propagate.py:59-86) as the owner of
+ * the dense per-block matrices. */
+int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, int n_controls,
+                const double* const* h0, const double* const* hk, int objective,
+                const double* const* initial, const double* const* target, const double* weights,
+                int n_slices, double dt, int max_batch);
+
+/* One fidelity+gradient evaluation for `batch` control vectors.
+ *   u      [batch][n_controls][n_slices]
+ *   F      [batch]                          (may be NULL)
+ *   grad   [batch][n_controls][n_slices]    (may be NULL)
+ *   tau    [batch][n_blocks][2]             (may be NULL) per-block complex overlaps
+ *   stream cudaStream_t (NULL = legacy default stream)
+ * Blocking: returns after the results are complete (and copied for SQOC_MEM_HOST).
+ * Replaces: qoc.gradient (qoc.py:137-168) and qoc.objective (qoc.py:93-95). */
+int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* grad, double* tau,
+              int memory, void* stream);
+
+/* Free all device memory of the problem. */
+int sqoc_destroy(sqoc_problem* p);
+
+/* Single-block state-transfer gradient with the reference's exact signature
+ * semantics: qoc.gradient(psi0, psi_f, bx, by, backend, tau) with
+ * backend.h0/hx/hy dense d x d.  Host buffers; gx, gy [n_steps], P scalar. */
+int sqoc_state_gradient(int device, int d, const double* h0, const double* hx, const double* hy,
+                        const double* psi0, const double* psi_f, const double* bx, const double* by,
+                        int n_steps, double tau, double* gx, double* gy, double* P);
+
+/* Device kernel launches issued by the last sqoc_eval on this problem. */
+int sqoc_last_launch_count(const sqoc_problem* p);
+
+/* Largest block dimension the fused on-chip (tiny) path handles. */
+int sqoc_tiny_max_dim(void);
+
+const char* sqoc_last_error(void);
+int sqoc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SYMQOC_B200_H */

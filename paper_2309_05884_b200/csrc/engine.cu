@@ -1,0 +1,403 @@
+// C-ABI implementation of the GRAPE fidelity+gradient engine (include/symqoc_b200.h).
+//
+// Host responsibilities: own the per-block generators / targets on the device,
+// pick a kernel family per block (tiny fused kernel for d <= 16, batched-GEMM
+// path for larger blocks), fork one stream per block off the caller's stream,
+// and reduce per-block contributions in a fixed order (deterministic F / grad).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/symqoc_b200.h"
+#include "large.cuh"
+#include "tiny.cuh"
+
+namespace sqoc {
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define SQOC_CUDA(call)                                                                      \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(SQOC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+constexpr size_t kMaxSmem = 227 * 1024;
+
+struct BlockPlan {
+  int d = 0;
+  bool tiny = false;
+  double weight = 1.0;
+  double2* gen = nullptr;     // (K+1) d*d, -i dt H
+  double2* x0 = nullptr;      // state objective
+  double2* target = nullptr;  // V or psi_f
+  double2* park = nullptr;    // tiny: [slots][2][d*R]
+  size_t park_slots = 0;
+  int nwarps = 1;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  LargeBlock large;           // batched-GEMM path state (d > kTinyMaxDim)
+};
+
+}  // namespace sqoc
+
+struct sqoc_problem {
+  int device = 0;
+  int nblocks = 0, K = 0, N = 0, objective = 0, max_batch = 0;
+  double dt = 0.0;
+  std::vector<sqoc::BlockPlan> blocks;
+  double* u_dev = nullptr;      // [max_batch][K][N] staging for host-memory calls
+  double* grad_dev = nullptr;   // [max_batch][K][N]
+  double* gradb = nullptr;      // [nblocks][max_batch][K][N] per-block contributions
+  double2* tau_dev = nullptr;   // [max_batch][nblocks]
+  double* F_dev = nullptr;      // [max_batch]
+  double* w_dev = nullptr;      // [nblocks]
+  int* flag_dev = nullptr;      // non-finite flag
+  cudaEvent_t fork = nullptr;
+  int launches = 0;
+};
+
+namespace sqoc {
+
+// ---------------------------------------------------------------- finalize
+__global__ void finalize_kernel(int batch, int nblocks, int KN, const double2* __restrict__ tau,
+                                const double* __restrict__ w, const double* __restrict__ gradb,
+                                size_t gradb_stride, double* __restrict__ F, double* __restrict__ grad,
+                                int* flag) {
+  const size_t total = (size_t)batch * KN;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    double g = 0.0;
+    for (int b = 0; b < nblocks; ++b) g += gradb[b * gradb_stride + i];
+    if (!isfinite(g)) atomicOr(flag, 1);
+    grad[i] = g;
+  }
+  for (size_t s = blockIdx.x * (size_t)blockDim.x + threadIdx.x; s < (size_t)batch; s += (size_t)gridDim.x * blockDim.x) {
+    double f = 0.0;
+    for (int b = 0; b < nblocks; ++b) {
+      const double2 t = tau[s * nblocks + b];
+      f += w[b] * (t.x * t.x + t.y * t.y);
+    }
+    if (!isfinite(f)) atomicOr(flag, 1);
+    F[s] = f;
+  }
+}
+
+// ---------------------------------------------------------------- tiny dispatch
+template <int D, bool GATE>
+static int launch_tiny_t(const TinyParams& tp, int grid, int nwarps, size_t smem, cudaStream_t st) {
+  static bool attr_set = false;
+  auto kern = grape_tiny_kernel<D, GATE>;
+  if (!attr_set) {
+    SQOC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+    attr_set = true;
+  }
+  kern<<<grid, nwarps * 32, smem, st>>>(tp);
+  SQOC_CUDA(cudaGetLastError());
+  return SQOC_OK;
+}
+
+template <bool GATE>
+static int launch_tiny(int d, const TinyParams& tp, int grid, int nwarps, size_t smem, cudaStream_t st) {
+  switch (d) {
+#define SQOC_CASE(D) \
+  case D:            \
+    return launch_tiny_t<D, GATE>(tp, grid, nwarps, smem, st);
+    SQOC_CASE(1) SQOC_CASE(2) SQOC_CASE(3) SQOC_CASE(4) SQOC_CASE(5) SQOC_CASE(6) SQOC_CASE(7) SQOC_CASE(8)
+    SQOC_CASE(9) SQOC_CASE(10) SQOC_CASE(11) SQOC_CASE(12) SQOC_CASE(13) SQOC_CASE(14) SQOC_CASE(15) SQOC_CASE(16)
+#undef SQOC_CASE
+    default:
+      return fail(SQOC_ERR_UNSUPPORTED, "tiny path supports d <= 16");
+  }
+}
+
+static int choose_nwarps(int d, int K, int batch) {
+  const int pg = 32 / d;
+  const int need = (batch + pg - 1) / pg;
+  int nw = 8;
+  while (nw > 1 && tiny_smem_bytes(d, K, nw) > kMaxSmem) --nw;
+  return std::max(1, std::min(nw, need));
+}
+
+static std::vector<double2> to_generator(const double* h, int d, double dt) {
+  // a = -i dt H : (x + i y) -> (dt y) - i (dt x)
+  std::vector<double2> a((size_t)d * d);
+  for (size_t i = 0; i < a.size(); ++i) a[i] = make_double2(dt * h[2 * i + 1], -dt * h[2 * i]);
+  return a;
+}
+
+static void free_problem(sqoc_problem* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  for (auto& b : p->blocks) {
+    cudaFree(b.gen);
+    cudaFree(b.x0);
+    cudaFree(b.target);
+    cudaFree(b.park);
+    large_free(b.large);
+    if (b.stream) cudaStreamDestroy(b.stream);
+    if (b.done) cudaEventDestroy(b.done);
+  }
+  cudaFree(p->u_dev);
+  cudaFree(p->grad_dev);
+  cudaFree(p->gradb);
+  cudaFree(p->tau_dev);
+  cudaFree(p->F_dev);
+  cudaFree(p->w_dev);
+  cudaFree(p->flag_dev);
+  if (p->fork) cudaEventDestroy(p->fork);
+  delete p;
+}
+
+}  // namespace sqoc
+
+using namespace sqoc;
+
+extern "C" {
+
+const char* sqoc_last_error(void) { return g_last_error.c_str(); }
+int sqoc_abi_version(void) { return SQOC_ABI_VERSION; }
+int sqoc_tiny_max_dim(void) { return kTinyMaxDim; }
+int sqoc_last_launch_count(const sqoc_problem* p) { return p ? p->launches : 0; }
+
+int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, int n_controls,
+                const double* const* h0, const double* const* hk, int objective,
+                const double* const* initial, const double* const* target, const double* weights,
+                int n_slices, double dt, int max_batch) {
+  if (!out) return fail(SQOC_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (n_blocks < 1 || !dims || !h0 || !hk || !target) return fail(SQOC_ERR_ARG, "missing block arrays");
+  if (n_controls < 1 || n_controls > kMaxControls) return fail(SQOC_ERR_ARG, "n_controls must be in 1..4");
+  if (objective != SQOC_OBJ_STATE && objective != SQOC_OBJ_GATE) return fail(SQOC_ERR_ARG, "unknown objective");
+  if (objective == SQOC_OBJ_STATE && !initial) return fail(SQOC_ERR_ARG, "state objective needs initial states");
+  if (n_slices < 0 || max_batch < 1 || !(dt > 0.0) || !std::isfinite(dt)) return fail(SQOC_ERR_ARG, "bad grid or batch");
+  for (int b = 0; b < n_blocks; ++b)
+    if (dims[b] < 1) return fail(SQOC_ERR_ARG, "block dimension must be >= 1");
+
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(SQOC_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  sqoc_problem* p = new sqoc_problem();
+  p->device = device;
+  p->nblocks = n_blocks;
+  p->K = n_controls;
+  p->N = n_slices;
+  p->objective = objective;
+  p->max_batch = max_batch;
+  p->dt = dt;
+  p->blocks.resize(n_blocks);
+  const size_t KN = (size_t)n_controls * n_slices;
+  std::vector<double> w(n_blocks);
+  int rc = SQOC_OK;
+  auto chk = [&](cudaError_t ce, const char* what) {
+    if (ce != cudaSuccess && rc == SQOC_OK) rc = fail(SQOC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(ce));
+  };
+  for (int b = 0; b < n_blocks && rc == SQOC_OK; ++b) {
+    BlockPlan& bp = p->blocks[b];
+    const int d = dims[b];
+    bp.d = d;
+    bp.tiny = d <= kTinyMaxDim;
+    w[b] = weights ? weights[b]
+                   : (objective == SQOC_OBJ_GATE ? 1.0 / ((double)n_blocks * d * d) : 1.0);
+    std::vector<double2> g;
+    g.reserve((size_t)(n_controls + 1) * d * d);
+    auto a0 = to_generator(h0[b], d, dt);
+    g.insert(g.end(), a0.begin(), a0.end());
+    for (int k = 0; k < n_controls; ++k) {
+      auto ak = to_generator(hk[b] + (size_t)k * 2 * d * d, d, dt);
+      g.insert(g.end(), ak.begin(), ak.end());
+    }
+    chk(cudaMalloc(&bp.gen, g.size() * sizeof(double2)), "cudaMalloc gen");
+    if (rc) break;
+    chk(cudaMemcpy(bp.gen, g.data(), g.size() * sizeof(double2), cudaMemcpyHostToDevice), "copy gen");
+    const size_t tsz = (objective == SQOC_OBJ_GATE ? (size_t)d * d : (size_t)d) * sizeof(double2);
+    chk(cudaMalloc(&bp.target, tsz), "cudaMalloc target");
+    if (rc) break;
+    chk(cudaMemcpy(bp.target, target[b], tsz, cudaMemcpyHostToDevice), "copy target");
+    if (objective == SQOC_OBJ_STATE) {
+      chk(cudaMalloc(&bp.x0, d * sizeof(double2)), "cudaMalloc x0");
+      if (rc) break;
+      chk(cudaMemcpy(bp.x0, initial[b], d * sizeof(double2), cudaMemcpyHostToDevice), "copy x0");
+    }
+    chk(cudaStreamCreateWithFlags(&bp.stream, cudaStreamNonBlocking), "stream");
+    chk(cudaEventCreateWithFlags(&bp.done, cudaEventDisableTiming), "event");
+    if (bp.tiny) {
+      const int R = objective == SQOC_OBJ_GATE ? d : 1;
+      const int pg = 32 / d;
+      bp.nwarps = choose_nwarps(d, n_controls, max_batch);
+      const int per_cta = pg * bp.nwarps;
+      bp.park_slots = (size_t)((max_batch + per_cta - 1) / per_cta) * per_cta;
+      chk(cudaMalloc(&bp.park, bp.park_slots * 2 * d * R * sizeof(double2)), "cudaMalloc park");
+    } else {
+      int lrc = large_init(bp.large, d, n_controls, n_slices, objective == SQOC_OBJ_GATE, max_batch);
+      if (lrc != SQOC_OK) rc = fail(lrc, large_last_error());
+    }
+  }
+  if (rc == SQOC_OK) {
+    chk(cudaMalloc(&p->u_dev, std::max<size_t>(1, max_batch * KN) * sizeof(double)), "cudaMalloc u");
+    chk(cudaMalloc(&p->grad_dev, std::max<size_t>(1, max_batch * KN) * sizeof(double)), "cudaMalloc grad");
+    chk(cudaMalloc(&p->gradb, std::max<size_t>(1, n_blocks * max_batch * KN) * sizeof(double)), "cudaMalloc gradb");
+    chk(cudaMalloc(&p->tau_dev, (size_t)max_batch * n_blocks * sizeof(double2)), "cudaMalloc tau");
+    chk(cudaMalloc(&p->F_dev, max_batch * sizeof(double)), "cudaMalloc F");
+    chk(cudaMalloc(&p->w_dev, n_blocks * sizeof(double)), "cudaMalloc w");
+    chk(cudaMalloc(&p->flag_dev, sizeof(int)), "cudaMalloc flag");
+    if (rc == SQOC_OK) chk(cudaMemcpy(p->w_dev, w.data(), n_blocks * sizeof(double), cudaMemcpyHostToDevice), "copy w");
+    chk(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming), "event");
+    for (int b = 0; b < n_blocks; ++b) p->blocks[b].weight = w[b];
+  }
+  if (rc != SQOC_OK) {
+    free_problem(p);
+    return rc;
+  }
+  *out = p;
+  return SQOC_OK;
+}
+
+int sqoc_destroy(sqoc_problem* p) {
+  free_problem(p);
+  return SQOC_OK;
+}
+
+int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* grad, double* tau, int memory,
+              void* stream) {
+  if (!p) return fail(SQOC_ERR_ARG, "problem is NULL");
+  if (batch < 1 || batch > p->max_batch) return fail(SQOC_ERR_ARG, "batch outside 1..max_batch");
+  if (memory != SQOC_MEM_HOST && memory != SQOC_MEM_DEVICE) return fail(SQOC_ERR_ARG, "unknown memory kind");
+  if (!u && p->N > 0) return fail(SQOC_ERR_ARG, "u is NULL");
+  SQOC_CUDA(cudaSetDevice(p->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t KN = (size_t)p->K * p->N;
+  const bool dev = memory == SQOC_MEM_DEVICE;
+  const double* u_dev = u;
+  p->launches = 0;
+  if (!dev && KN) {
+    SQOC_CUDA(cudaMemcpyAsync(p->u_dev, u, batch * KN * sizeof(double), cudaMemcpyHostToDevice, st));
+    u_dev = p->u_dev;
+  }
+  double* grad_dev = (dev && grad) ? grad : p->grad_dev;
+  double* F_dev = (dev && F) ? F : p->F_dev;
+  SQOC_CUDA(cudaMemsetAsync(p->flag_dev, 0, sizeof(int), st));
+  SQOC_CUDA(cudaEventRecord(p->fork, st));
+  const bool gate = p->objective == SQOC_OBJ_GATE;
+  for (int b = 0; b < p->nblocks; ++b) {
+    BlockPlan& bp = p->blocks[b];
+    SQOC_CUDA(cudaStreamWaitEvent(bp.stream, p->fork, 0));
+    double* gout = p->gradb + (size_t)b * p->max_batch * KN;
+    if (p->N == 0) {
+      // empty grid: X_N = X_0 (qoc.py test_empty_grid_gives_empty_gradient)
+    }
+    if (bp.tiny) {
+      TinyParams tp;
+      tp.K = p->K;
+      tp.N = p->N;
+      tp.batch = batch;
+      tp.gen = bp.gen;
+      tp.x0 = bp.x0;
+      tp.target = bp.target;
+      tp.u = u_dev;
+      tp.weight = bp.weight;
+      tp.tau_out = p->tau_dev + b;
+      tp.tau_stride = p->nblocks;
+      tp.grad_out = gout;
+      tp.park = bp.park;
+      const int pg = 32 / bp.d;
+      int nw = std::max(1, std::min(bp.nwarps, (batch + pg - 1) / pg));
+      tp.nwarps = nw;
+      const int grid = (batch + pg * nw - 1) / (pg * nw);
+      const size_t smem = tiny_smem_bytes(bp.d, p->K, nw);
+      int rc = gate ? launch_tiny<true>(bp.d, tp, grid, nw, smem, bp.stream)
+                    : launch_tiny<false>(bp.d, tp, grid, nw, smem, bp.stream);
+      if (rc != SQOC_OK) return rc;
+      p->launches += 1;
+    } else {
+      LargeArgs la;
+      la.u = u_dev;
+      la.batch = batch;
+      la.gen = bp.gen;
+      la.x0 = bp.x0;
+      la.target = bp.target;
+      la.weight = bp.weight;
+      la.tau_out = p->tau_dev + b;
+      la.tau_stride = p->nblocks;
+      la.grad_out = gout;
+      int launches = 0;
+      int rc = large_eval(bp.large, la, bp.stream, &launches);
+      if (rc != SQOC_OK) return fail(rc, large_last_error());
+      p->launches += launches;
+    }
+    SQOC_CUDA(cudaEventRecord(bp.done, bp.stream));
+    SQOC_CUDA(cudaStreamWaitEvent(st, bp.done, 0));
+  }
+  {
+    const size_t total = std::max<size_t>(batch * KN, batch);
+    const int threads = 256;
+    const int grid = (int)std::min<size_t>((total + threads - 1) / threads, 148 * 8);
+    finalize_kernel<<<std::max(grid, 1), threads, 0, st>>>(batch, p->nblocks, (int)KN, p->tau_dev, p->w_dev,
+                                                           p->gradb, (size_t)p->max_batch * KN, F_dev, grad_dev,
+                                                           p->flag_dev);
+    SQOC_CUDA(cudaGetLastError());
+    p->launches += 1;
+  }
+  int flag = 0;
+  SQOC_CUDA(cudaMemcpyAsync(&flag, p->flag_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (!dev) {
+    if (F) SQOC_CUDA(cudaMemcpyAsync(F, F_dev, batch * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (grad && KN) SQOC_CUDA(cudaMemcpyAsync(grad, grad_dev, batch * KN * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (tau)
+      SQOC_CUDA(cudaMemcpyAsync(tau, p->tau_dev, (size_t)batch * p->nblocks * sizeof(double2), cudaMemcpyDeviceToHost, st));
+  } else if (tau) {
+    SQOC_CUDA(cudaMemcpyAsync(tau, p->tau_dev, (size_t)batch * p->nblocks * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  }
+  SQOC_CUDA(cudaStreamSynchronize(st));
+  if (flag) return fail(SQOC_ERR_NONFINITE, "objective or gradient became non-finite");
+  return SQOC_OK;
+}
+
+int sqoc_state_gradient(int device, int d, const double* h0, const double* hx, const double* hy,
+                        const double* psi0, const double* psi_f, const double* bx, const double* by,
+                        int n_steps, double tau, double* gx, double* gy, double* P) {
+  if (d < 1 || !h0 || !hx || !hy || !psi0 || !psi_f || n_steps < 0) return fail(SQOC_ERR_ARG, "bad arguments");
+  if (n_steps > 0 && !(tau > 0.0)) return fail(SQOC_ERR_ARG, "tau must be > 0");
+  std::vector<double> hk((size_t)4 * d * d);
+  std::memcpy(hk.data(), hx, sizeof(double) * 2 * d * d);
+  std::memcpy(hk.data() + 2 * (size_t)d * d, hy, sizeof(double) * 2 * d * d);
+  const double* h0s[1] = {h0};
+  const double* hks[1] = {hk.data()};
+  const double* ini[1] = {psi0};
+  const double* tgt[1] = {psi_f};
+  const double w = 1.0;
+  sqoc_problem* p = nullptr;
+  int rc = sqoc_create(&p, device, 1, &d, 2, h0s, hks, SQOC_OBJ_STATE, ini, tgt, &w, n_steps,
+                       n_steps > 0 ? tau : 1.0, 1);
+  if (rc != SQOC_OK) return rc;
+  std::vector<double> u((size_t)2 * n_steps), g((size_t)2 * n_steps);
+  for (int j = 0; j < n_steps; ++j) {
+    u[j] = bx[j];
+    u[n_steps + j] = by[j];
+  }
+  double F = 0.0;
+  rc = sqoc_eval(p, u.data(), 1, &F, g.data(), nullptr, SQOC_MEM_HOST, nullptr);
+  if (rc == SQOC_OK) {
+    for (int j = 0; j < n_steps; ++j) {
+      gx[j] = g[j];
+      gy[j] = g[n_steps + j];
+    }
+    *P = F;
+  }
+  std::string keep = g_last_error;
+  sqoc_destroy(p);
+  g_last_error = keep;
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+"""Host-side owner of one GRAPE problem on the GPU (wraps sqoc_create / sqoc_eval).
+
+``GrapeEngine(system).objective(u) -> (F, grad)`` is the BASELINE API; the
+reference-shaped ``qoc.gradient`` adapter is in ``qoc.py``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+
+def _cplx(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+
+
+class GrapeEngine:
+    """Device-resident generators/targets of a ``systems.GrapeSystem``-like object.
+
+    Required attributes of ``system``: ``blocks`` (each with ``h0``, ``hk``),
+    ``objective`` ('gate'|'state'), ``targets``, ``initial`` (state), ``dt``,
+    ``n_slices``, and optionally ``block_weights()``.
+    """
+
+    def __init__(self, system, max_batch: int = 1, device: int = 0):
+        self.lib = _lib.load()
+        self.system = system
+        self.K = len(system.blocks[0].hk)
+        self.N = int(system.n_slices)
+        self.nblocks = len(system.blocks)
+        self.max_batch = int(max_batch)
+        self.device = device
+        gate = system.objective == "gate"
+        dims = [int(b.h0.shape[0]) for b in system.blocks]
+        self.dims = dims
+        keep = []
+
+        def dptr(arr):
+            arr = np.ascontiguousarray(arr)
+            keep.append(arr)
+            return arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+        h0 = (ctypes.POINTER(ctypes.c_double) * self.nblocks)()
+        hk = (ctypes.POINTER(ctypes.c_double) * self.nblocks)()
+        tg = (ctypes.POINTER(ctypes.c_double) * self.nblocks)()
+        ini = (ctypes.POINTER(ctypes.c_double) * self.nblocks)()
+        for b, blk in enumerate(system.blocks):
+            d = dims[b]
+            if len(blk.hk) != self.K:
+                raise ValueError("all blocks need the same number of controls")
+            h0[b] = dptr(_cplx(blk.h0).view(np.float64))
+            hk[b] = dptr(np.concatenate([_cplx(h).reshape(-1) for h in blk.hk]).view(np.float64))
+            t = _cplx(system.targets[b])
+            if t.shape != ((d, d) if gate else (d,)):
+                raise ValueError(f"target of block {b} has shape {t.shape}")
+            tg[b] = dptr(t.view(np.float64))
+            if not gate:
+                ini[b] = dptr(_cplx(system.initial[b]).view(np.float64))
+        w = getattr(system, "block_weights", None)
+        weights = None if w is None else np.ascontiguousarray(w(), dtype=np.float64)
+        dims_arr = (ctypes.c_int * self.nblocks)(*dims)
+        handle = ctypes.c_void_p()
+        rc = self.lib.sqoc_create(
+            ctypes.byref(handle), device, self.nblocks, dims_arr, self.K, h0, hk,
+            _lib.OBJ_GATE if gate else _lib.OBJ_STATE, None if gate else ini, tg,
+            None if weights is None else weights.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+            self.N, float(system.dt), self.max_batch,
+        )
+        _lib.check(rc, "sqoc_create")
+        self.handle = handle
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.sqoc_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def last_launches(self) -> int:
+        return self.lib.sqoc_last_launch_count(self.handle)
+
+    def evaluate(self, u, want_tau: bool = False):
+        """Host arrays in/out. u: (K, N) or (B, K, N). Returns F, grad (, tau)."""
+        u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+        single = u.ndim == 2
+        ub = u[None] if single else u
+        if ub.shape[1:] != (self.K, self.N):
+            raise ValueError(f"u must have shape (B, {self.K}, {self.N}), got {u.shape}")
+        if not np.all(np.isfinite(ub)):
+            raise ValueError("control samples must be finite")
+        B = ub.shape[0]
+        F = np.empty(B)
+        grad = np.empty_like(ub)
+        tau = np.empty((B, self.nblocks), dtype=np.complex128)
+        rc = self.lib.sqoc_eval(self.handle, ub.ctypes.data, B, F.ctypes.data, grad.ctypes.data,
+                                tau.ctypes.data, _lib.MEM_HOST, None)
+        _lib.check(rc, "sqoc_eval")
+        if single:
+            F, grad, tau = F[0], grad[0], tau[0]
+        return (F, grad, tau) if want_tau else (F, grad)
+
+    def objective(self, u):
+        """objective(u) -> (F, grad): the BASELINE host API."""
+        return self.evaluate(u)
+
+    def evaluate_device(self, u_ptr: int, batch: int, F_ptr: int, grad_ptr: int, tau_ptr: int = 0,
+                        stream: int = 0):
+        """Device pointers in/out (e.g. torch ``data_ptr()``); blocking."""
+        rc = self.lib.sqoc_eval(self.handle, u_ptr, batch, F_ptr or None, grad_ptr or None, tau_ptr or None,
+                                _lib.MEM_DEVICE, stream or None)
+        _lib.check(rc, "sqoc_eval")

@@ -1,0 +1,62 @@
+"""Host block bases reproduce the reference's block indexing and matrices."""
+
+import numpy as np
+import pytest
+
+from paper_2309_05884_b200 import pauli, symmetry, systems
+
+
+@pytest.mark.parametrize("n", [6, 8, 10])
+def test_dn_block_sizes_match_reference(golden, n):
+    assert tuple(b.dim for b in symmetry.dn_full_basis(n)) == tuple(golden[f"dn{n}_sizes"])
+
+
+def test_bracelet_dims_match_reference(golden):
+    dims = [symmetry.bracelet_block(n).dim for n in range(3, 15)]
+    assert dims == list(golden["bracelet_dims"])
+    # Table 1 of the paper
+    assert dims == [4, 6, 8, 13, 18, 30, 46, 78, 126, 224, 380, 687]
+
+
+def test_dn6_generators_match_reference(golden):
+    sysm = systems.gate_ring(6, 10.0, 10)
+    for b, blk in enumerate(sysm.blocks):
+        for name, m in zip(("h0", "hx", "hy"), (blk.h0, *blk.hk)):
+            np.testing.assert_allclose(m, golden[f"dn6_b{b}_{name}"], atol=1e-13)
+
+
+def test_sn12_sector_generators_match_reference(golden):
+    sysm = systems.gate_all_to_all(12, 10.0, 10)
+    assert [b.dim for b in sysm.blocks] == [13, 11, 9, 7, 5, 3, 1]
+    for blk in sysm.blocks:
+        d = blk.dim
+        for name, m in zip(("h0", "hx", "hy"), (blk.h0, *blk.hk)):
+            np.testing.assert_allclose(m, golden[f"sn12_d{d}_{name}"], atol=1e-12)
+
+
+def test_bracelet_block_is_dn_a1_block():
+    a1 = symmetry.dn_full_basis(8)[0]
+    br = symmetry.bracelet_block(8)
+    np.testing.assert_allclose(a1.columns.toarray(), br.columns.toarray(), atol=1e-15)
+
+
+@pytest.mark.parametrize("n", [5, 6, 7])
+def test_dn_basis_block_diagonalises_heisenberg_and_controls(n):
+    blocks = symmetry.dn_full_basis(n)
+    a = np.hstack([b.columns.toarray() for b in blocks])
+    np.testing.assert_allclose(a.T @ a, np.eye(1 << n), atol=1e-12)
+    ops = [systems.ring_heisenberg(n), *systems.global_controls(n)]
+    mask = np.ones((1 << n, 1 << n), dtype=bool)
+    s = 0
+    for b in blocks:
+        mask[s:s + b.dim, s:s + b.dim] = False
+        s += b.dim
+    for op in ops:
+        m = a.T @ pauli.realize(op).toarray() @ a
+        assert np.abs(m[mask]).max() <= 1e-12
+
+
+def test_dn14_block_sizes():
+    """n=14 is refused by the reference (adjoint.py:231-232); sizes from the character formula."""
+    sizes = [b.dim for b in symmetry.dn_full_basis(14)]
+    assert sizes == [687, 495, 549, 613] + [1161, 1161, 1179, 1179] * 3
