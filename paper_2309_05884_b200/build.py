@@ -6,7 +6,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = [os.path.join(HERE, "csrc", "engine.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "large.cu")]
 DEPS = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + [
     os.path.join(HERE, "..", "include", "symqoc_b200.h")
 ]
@@ -14,7 +14,7 @@ OUT = os.path.join(HERE, "libsymqoc_b200.so")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
 
 
@@ -28,10 +28,21 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or not up_to_date():
         nvcc = os.environ.get("NVCC", "nvcc")
-        cmd = [nvcc, *NVCC_FLAGS, "-o", OUT + ".tmp", *SOURCES, "-lcudart"]
+        objs, procs = [], []
+        for src in SOURCES:  # compile translation units in parallel
+            obj = os.path.join(HERE, "csrc", os.path.basename(src) + ".o")
+            cmd = [nvcc, *NVCC_FLAGS, "-c", "-o", obj, src]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            procs.append(subprocess.Popen(cmd))
+            objs.append(obj)
+        for pr in procs:
+            if pr.wait() != 0:
+                raise RuntimeError("nvcc failed")
+        link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT + ".tmp", *objs, "-lcudart"]
         if verbose:
-            print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
+            print(" ".join(link), flush=True)
+        subprocess.run(link, check=True)
         os.replace(OUT + ".tmp", OUT)
     return OUT
 

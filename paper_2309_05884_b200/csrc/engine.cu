@@ -48,7 +48,6 @@ struct BlockPlan {
   int nwarps = 1;
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
-  LargeBlock large;           // batched-GEMM path state (d > kTinyMaxDim)
 };
 
 }  // namespace sqoc
@@ -66,6 +65,9 @@ struct sqoc_problem {
   double* w_dev = nullptr;      // [nblocks]
   int* flag_dev = nullptr;      // non-finite flag
   cudaEvent_t fork = nullptr;
+  sqoc::LargeGroup* large = nullptr;  // all blocks with d > kTinyMaxDim, advanced together
+  cudaStream_t large_stream = nullptr;
+  cudaEvent_t large_done = nullptr;
   int launches = 0;
 };
 
@@ -145,7 +147,6 @@ static void free_problem(sqoc_problem* p) {
     cudaFree(b.x0);
     cudaFree(b.target);
     cudaFree(b.park);
-    large_free(b.large);
     if (b.stream) cudaStreamDestroy(b.stream);
     if (b.done) cudaEventDestroy(b.done);
   }
@@ -157,6 +158,12 @@ static void free_problem(sqoc_problem* p) {
   cudaFree(p->w_dev);
   cudaFree(p->flag_dev);
   if (p->fork) cudaEventDestroy(p->fork);
+  if (p->large) {
+    large_free(*p->large);
+    delete p->large;
+  }
+  if (p->large_stream) cudaStreamDestroy(p->large_stream);
+  if (p->large_done) cudaEventDestroy(p->large_done);
   delete p;
 }
 
@@ -198,6 +205,7 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
   p->blocks.resize(n_blocks);
   const size_t KN = (size_t)n_controls * n_slices;
   std::vector<double> w(n_blocks);
+  std::vector<LargeBlockSpec> large_specs;
   int rc = SQOC_OK;
   auto chk = [&](cudaError_t ce, const char* what) {
     if (ce != cudaSuccess && rc == SQOC_OK) rc = fail(SQOC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(ce));
@@ -239,9 +247,34 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
       bp.park_slots = (size_t)((max_batch + per_cta - 1) / per_cta) * per_cta;
       chk(cudaMalloc(&bp.park, bp.park_slots * 2 * d * R * sizeof(double2)), "cudaMalloc park");
     } else {
-      int lrc = large_init(bp.large, d, n_controls, n_slices, objective == SQOC_OBJ_GATE, max_batch);
-      if (lrc != SQOC_OK) rc = fail(lrc, large_last_error());
+      LargeBlockSpec ls{};
+      ls.global_index = b;
+      ls.d = d;
+      ls.gen = bp.gen;
+      ls.x0 = bp.x0;
+      ls.target = bp.target;
+      ls.weight = w[b];
+      for (int k = 0; k <= n_controls; ++k) {  // inf-norm of a_k (max row sum of |re| + |im|)
+        double best = 0.0;
+        for (int i = 0; i < d; ++i) {
+          double rs = 0.0;
+          for (int c = 0; c < d; ++c) {
+            const double2 z = g[(size_t)k * d * d + (size_t)i * d + c];
+            rs += std::fabs(z.x) + std::fabs(z.y);
+          }
+          best = std::max(best, rs);
+        }
+        ls.gen_norm[k] = best;
+      }
+      large_specs.push_back(ls);
     }
+  }
+  if (rc == SQOC_OK && !large_specs.empty()) {
+    p->large = new LargeGroup();
+    int lrc = large_init(*p->large, large_specs, n_controls, n_slices, objective == SQOC_OBJ_GATE);
+    if (lrc != SQOC_OK) rc = fail(lrc, p->large->err);
+    chk(cudaStreamCreateWithFlags(&p->large_stream, cudaStreamNonBlocking), "stream");
+    chk(cudaEventCreateWithFlags(&p->large_done, cudaEventDisableTiming), "event");
   }
   if (rc == SQOC_OK) {
     chk(cudaMalloc(&p->u_dev, std::max<size_t>(1, max_batch * KN) * sizeof(double)), "cudaMalloc u");
@@ -296,7 +329,8 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
     if (p->N == 0) {
       // empty grid: X_N = X_0 (qoc.py test_empty_grid_gives_empty_gradient)
     }
-    if (bp.tiny) {
+    if (!bp.tiny) continue;
+    {
       TinyParams tp;
       tp.K = p->K;
       tp.N = p->N;
@@ -319,24 +353,24 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
                     : launch_tiny<false>(bp.d, tp, grid, nw, smem, bp.stream);
       if (rc != SQOC_OK) return rc;
       p->launches += 1;
-    } else {
-      LargeArgs la;
-      la.u = u_dev;
-      la.batch = batch;
-      la.gen = bp.gen;
-      la.x0 = bp.x0;
-      la.target = bp.target;
-      la.weight = bp.weight;
-      la.tau_out = p->tau_dev + b;
-      la.tau_stride = p->nblocks;
-      la.grad_out = gout;
-      int launches = 0;
-      int rc = large_eval(bp.large, la, bp.stream, &launches);
-      if (rc != SQOC_OK) return fail(rc, large_last_error());
-      p->launches += launches;
     }
     SQOC_CUDA(cudaEventRecord(bp.done, bp.stream));
     SQOC_CUDA(cudaStreamWaitEvent(st, bp.done, 0));
+  }
+  if (p->large) {
+    SQOC_CUDA(cudaStreamWaitEvent(p->large_stream, p->fork, 0));
+    LargeArgs la;
+    la.u = u_dev;
+    la.batch = batch;
+    la.tau_out = p->tau_dev;
+    la.tau_stride = p->nblocks;
+    la.gradb = p->gradb;
+    la.gradb_block_stride = (size_t)p->max_batch * KN;
+    int rc = large_eval(*p->large, la, p->large_stream);
+    if (rc != SQOC_OK) return fail(rc, p->large->err);
+    p->launches += p->large->launches;
+    SQOC_CUDA(cudaEventRecord(p->large_done, p->large_stream));
+    SQOC_CUDA(cudaStreamWaitEvent(st, p->large_done, 0));
   }
   {
     const size_t total = std::max<size_t>(batch * KN, batch);

@@ -1,28 +1,84 @@
-// Batched-GEMM path for large symmetry blocks (d > 16).  (stub, filled in next)
+// Batched-GEMM path for large symmetry blocks (d > kTinyMaxDim): D_n blocks of
+// cfg 2 / cfg 3 and the unsymmetrised 2^n space of cfg 4.
+//
+// All large blocks of a problem are advanced together: every step below is ONE
+// launch whose work list holds one GEMM per block (zgemm.cuh), so the 16 D_14
+// blocks (495..1179) fill the 148 SMs together.  Per slice j (same algebra as
+// tiny.cuh, Taylor degree m = 3 nb and s squarings chosen once per evaluation
+// from the bound ||A_j|| <= ||a_0|| + sum_k |u_kj| ||a_k||):
+//
+//   forward : A, A2 = A A, A3 = A2 A, Horner T <- T A3 + Q_t, T <- T T (s x),
+//             X <- U X                                         (nb + 2 + s GEMMs)
+//   backward: Ad = 2^-s X Lam^dag, pairs (A2,dA2), (A3,dA3), Horner pairs,
+//             squaring pairs -> (U, N = L_R(A, X Lam^dag)); trace epilogue
+//             dtau_k = Tr(U^dag N E_k) (no D stored); X <- U^dag X, Lam <- U^dag Lam.
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "zgemm.cuh"
+
 namespace sqoc {
 
-struct LargeBlock {
-  int d = 0;
-};
-
 struct LargeArgs {
-  const double* u;
+  const double* u;   // [batch][K][N]
   int batch;
-  const double2* gen;
-  const double2* x0;
-  const double2* target;
-  double weight;
-  double2* tau_out;
+  double2* tau_out;  // tau of (s, large block i) at tau_out[s * tau_stride + global_block[i]]
   int tau_stride;
-  double* grad_out;
+  double* gradb;     // per-block contributions [global block][max_batch][K][N]
+  size_t gradb_block_stride;
 };
 
-inline const char* large_last_error() { return "large-block path not built yet"; }
-inline int large_init(LargeBlock& lb, int d, int, int, bool, int) { lb.d = d; return 4; }
-inline int large_eval(LargeBlock&, const LargeArgs&, cudaStream_t, int*) { return 4; }
-inline void large_free(LargeBlock&) {}
+struct LargeBlockSpec {
+  int global_index;
+  int d;
+  const double2* gen;     // (K+1) d*d
+  const double2* x0;      // state objective: psi_0
+  const double2* target;  // V or psi_f
+  double weight;
+  double gen_norm[5];     // inf-norm bounds of a_0..a_K
+};
+
+struct LargeGroup {
+  int nblk = 0, K = 0, N = 0;  // X / Lam have d columns per block (gate) or 1 (state)
+  bool gate = true;
+  std::vector<LargeBlockSpec> blocks;
+  std::vector<size_t> off;    // block offsets into square workspace arrays (double2 units)
+  std::vector<size_t> offr;   // block offsets into d x R arrays
+  size_t total = 0, totalr = 0;
+  double2 *A = nullptr, *Ad = nullptr, *A2 = nullptr, *dA2 = nullptr, *A3 = nullptr, *dA3 = nullptr;
+  double2 *T[2] = {nullptr, nullptr}, *dT[2] = {nullptr, nullptr};
+  double2 *X[2] = {nullptr, nullptr}, *L[2] = {nullptr, nullptr};
+  double2* trace_part = nullptr;  // [sum tiles][K]
+  std::vector<int> trace_tile_off;
+  int trace_tiles = 0;
+  double2* tau_dev = nullptr;     // [nblk]
+  double* norm_dev = nullptr;     // scalar (max bound)
+  double* gnorm_dev = nullptr;    // [nblk][K+1]
+  // device copies of per-block info for elementwise kernels
+  int* d_dev = nullptr;
+  size_t* off_dev = nullptr;
+  size_t* offr_dev = nullptr;
+  const double2** gen_dev = nullptr;
+  const double2** tgt_dev = nullptr;
+  const double2** x0_dev = nullptr;
+  double* w_dev = nullptr;
+  int* gidx_dev = nullptr;
+  // GEMM work lists, built once (device), keyed by op + buffer parities
+  std::map<std::tuple<int, int, int, int>, std::pair<GemmItem*, int>> lists;  // (items, count)
+  std::map<std::tuple<int, int, int, int>, int> list_tiles;
+  std::vector<void*> list_mem;
+  int* tile_off_dev = nullptr;    // [nblk + 1] trace tile offsets
+  int launches = 0;
+  std::string err;
+};
+
+int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, int N, bool gate);
+int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st);
+void large_free(LargeGroup& g);
 
 }  // namespace sqoc

@@ -1,0 +1,241 @@
+// Batched complex FP64 GEMM on the sm_100a FP64 tensor path (mma.sync m8n8k4 -> DMMA.8x8x4).
+//
+// tcgen05/UMMA has no FP64 kind, so the FP64 tensor cores are reached through
+// warp-level mma.sync; on B200 DMMA runs at 64 FMA/clk/SM (36.9 TFLOP/s measured,
+// profiles/r01_fp64_peak.txt).  Complex products use 4 real DMMAs (re*re - im*im,
+// re*im + im*re) on interleaved (re, im) tiles: one LDS.128 gives both parts of
+// a fragment element.
+//
+// Work list: an array of GemmItem (one independent GEMM each, possibly with two
+// K segments C = A0 B0 + A1 B1), tiles mapped by a prefix sum so blocks of
+// different sizes share one launch.  Operands may be conjugate-transposed.
+// Epilogues: C = alpha acc + beta0 E0 + beta1 E1 + gamma [diag] I, or a fused
+// trace sum_pq acc[p][q] F_k[q][p] written as per-tile partials (no C store).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sqoc {
+
+enum { OP_N = 0, OP_C = 1 };
+enum { EPI_STORE = 0, EPI_TRACE = 1 };
+
+struct GemmItem {
+  const double2* A0;
+  const double2* B0;
+  const double2* A1;
+  const double2* B1;
+  double2* C;
+  const double2* E0;
+  const double2* E1;
+  const double2* F;   // trace epilogue: nF matrices, F + f * fstride
+  double2* tr_out;    // trace epilogue: [tiles][nF] partials
+  long fstride;
+  int m, n, k, nseg;
+  int lda, ldb, ldc;
+  int diag;           // gamma applies to this item
+  int tile_start, tiles_n;
+  int nF;
+};
+
+struct GemmArgs {
+  double alpha, beta0, beta1, gamma;
+};
+
+constexpr int GBM = 64, GBN = 64, GBK = 8, GSTAGES = 4, GTHREADS = 128;
+constexpr int LD_KMAJ = GBK + 4;  // tiles stored [row][k]: ld = 12 (== 4 mod 8, conflict-free)
+constexpr int LD_NMAJ = GBM + 2;  // tiles stored [k][col]: ld = 66 (== 2 mod 8, conflict-free)
+constexpr int G_A_ELEMS = (GBM * LD_KMAJ > GBK * LD_NMAJ) ? GBM * LD_KMAJ : GBK * LD_NMAJ;  // 768 vs 528
+constexpr size_t G_SMEM = sizeof(double2) * GSTAGES * 2 * G_A_ELEMS;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Load one K-step (GBK) of op(A) (rows m0.., k0..) and op(B) (k0.., cols n0..) into a stage.
+template <int TA, int TB>
+__device__ __forceinline__ void gemm_load_stage(double2* sA, double2* sB, const double2* A, const double2* B,
+                                                const GemmItem& it, int m0, int n0, int k0) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int r = 0; r < (GBM * GBK) / GTHREADS; ++r) {
+    const int i = tid + r * GTHREADS;
+    if (TA == OP_N) {  // A[m][k] row-major; smem [m][k]
+      const int row = i / GBK, col = i % GBK;
+      const int gm = m0 + row, gk = k0 + col;
+      const bool ok = gm < it.m && gk < it.k;
+      cp_async16(sA + row * LD_KMAJ + col, ok ? A + (size_t)gm * it.lda + gk : A, ok);
+    } else {  // op(A)[m][k] = conj(A[k][m]); smem [k][m]
+      const int row = i / GBM, col = i % GBM;
+      const int gk = k0 + row, gm = m0 + col;
+      const bool ok = gm < it.m && gk < it.k;
+      cp_async16(sA + row * LD_NMAJ + col, ok ? A + (size_t)gk * it.lda + gm : A, ok);
+    }
+    if (TB == OP_N) {  // B[k][n]; smem [k][n]
+      const int row = i / GBN, col = i % GBN;
+      const int gk = k0 + row, gn = n0 + col;
+      const bool ok = gn < it.n && gk < it.k;
+      cp_async16(sB + row * LD_NMAJ + col, ok ? B + (size_t)gk * it.ldb + gn : B, ok);
+    } else {  // op(B)[k][n] = conj(B[n][k]); smem [n][k]
+      const int row = i / GBK, col = i % GBK;
+      const int gn = n0 + row, gk = k0 + col;
+      const bool ok = gn < it.n && gk < it.k;
+      cp_async16(sB + row * LD_KMAJ + col, ok ? B + (size_t)gn * it.ldb + gk : B, ok);
+    }
+  }
+}
+
+template <int TA, int TB, int EPI>
+__global__ void __launch_bounds__(GTHREADS) zgemm_kernel(const GemmItem* __restrict__ items, int nitems,
+                                                         GemmArgs args) {
+  extern __shared__ double2 gsm[];
+  // ---- locate the item owning this tile (items sorted by tile_start) ----
+  int lo = 0, hi = nitems - 1;
+  const int tile = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (items[mid].tile_start <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmItem it = items[lo];
+  const int local = tile - it.tile_start;
+  const int m0 = (local / it.tiles_n) * GBM;
+  const int n0 = (local % it.tiles_n) * GBN;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int lr = lane >> 2, lc = lane & 3;
+
+  double acc[4][4][4];  // [mi][ni][re0, re1, im0, im1]
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+
+  const int kt_per_seg = (it.k + GBK - 1) / GBK;
+  const int kt_total = kt_per_seg * it.nseg;
+  double2* sAbase = gsm;
+  double2* sBbase = gsm + GSTAGES * G_A_ELEMS;
+
+  auto issue = [&](int kt) {
+    if (kt < kt_total) {
+      const int seg = kt / kt_per_seg;
+      const int k0 = (kt - seg * kt_per_seg) * GBK;
+      const int st = kt % GSTAGES;
+      gemm_load_stage<TA, TB>(sAbase + st * G_A_ELEMS, sBbase + st * G_A_ELEMS, seg ? it.A1 : it.A0,
+                              seg ? it.B1 : it.B0, it, m0, n0, k0);
+    }
+    cp_async_commit();
+  };
+
+#pragma unroll
+  for (int s = 0; s < GSTAGES - 1; ++s) issue(s);
+
+  for (int kt = 0; kt < kt_total; ++kt) {
+    cp_async_wait<GSTAGES - 2>();
+    __syncthreads();
+    issue(kt + GSTAGES - 1);
+    const int st = kt % GSTAGES;
+    const double2* sA = sAbase + st * G_A_ELEMS;
+    const double2* sB = sBbase + st * G_A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < GBK; kk += 4) {
+      double ar[4], ai[4], nai[4], br[4], bi[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int m = wm + mi * 8 + lr, k = kk + lc;
+        double2 a;
+        if (TA == OP_N) a = sA[m * LD_KMAJ + k];
+        else { a = sA[k * LD_NMAJ + m]; a.y = -a.y; }
+        ar[mi] = a.x; ai[mi] = a.y; nai[mi] = -a.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int n = wn + ni * 8 + lr, k = kk + lc;
+        double2 b;
+        if (TB == OP_N) b = sB[k * LD_NMAJ + n];
+        else { b = sB[n * LD_KMAJ + k]; b.y = -b.y; }
+        br[ni] = b.x; bi[ni] = b.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          dmma(acc[mi][ni][0], acc[mi][ni][1], ar[mi], br[ni]);
+          dmma(acc[mi][ni][0], acc[mi][ni][1], nai[mi], bi[ni]);
+          dmma(acc[mi][ni][2], acc[mi][ni][3], ar[mi], bi[ni]);
+          dmma(acc[mi][ni][2], acc[mi][ni][3], ai[mi], br[ni]);
+        }
+    }
+  }
+  cp_async_wait<0>();
+
+  if (EPI == EPI_STORE) {
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int m = m0 + wm + mi * 8 + lr;
+          const int n = n0 + wn + ni * 8 + 2 * lc + v;
+          if (m < it.m && n < it.n) {
+            double2 c = make_double2(args.alpha * acc[mi][ni][v], args.alpha * acc[mi][ni][2 + v]);
+            const size_t off = (size_t)m * it.ldc + n;
+            if (it.E0) { const double2 e = it.E0[off]; c.x += args.beta0 * e.x; c.y += args.beta0 * e.y; }
+            if (it.E1) { const double2 e = it.E1[off]; c.x += args.beta1 * e.x; c.y += args.beta1 * e.y; }
+            if (it.diag && m == n) c.x += args.gamma;
+            it.C[off] = c;
+          }
+        }
+  } else {
+    // fused trace: partial_f = sum_{p,q in tile} alpha acc[p][q] F_f[q][p]
+    __shared__ double2 red[GTHREADS / 32][4];
+    for (int f = 0; f < it.nF; ++f) {
+      const double2* F = it.F + f * it.fstride;
+      double sx = 0.0, sy = 0.0;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int p = m0 + wm + mi * 8 + lr;
+            const int q = n0 + wn + ni * 8 + 2 * lc + v;
+            if (p < it.m && q < it.n) {
+              const double2 e = F[(size_t)q * it.ldc + p];
+              const double cr = args.alpha * acc[mi][ni][v], ci = args.alpha * acc[mi][ni][2 + v];
+              sx += cr * e.x - ci * e.y;
+              sy += cr * e.y + ci * e.x;
+            }
+          }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      }
+      if (lane == 0) red[warp][f] = make_double2(sx, sy);
+    }
+    __syncthreads();
+    if (threadIdx.x < it.nF) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int w = 0; w < GTHREADS / 32; ++w) { s.x += red[w][threadIdx.x].x; s.y += red[w][threadIdx.x].y; }
+      it.tr_out[(size_t)local * it.nF + threadIdx.x] = s;
+    }
+  }
+}
+
+}  // namespace sqoc
