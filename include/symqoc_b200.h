@@ -83,6 +83,12 @@ int sqoc_state_gradient(int device, int d, const double* h0, const double* hx, c
                         const double* psi0, const double* psi_f, const double* bx, const double* by,
                         int n_steps, double tau, double* gx, double* gy, double* P);
 
+/* Per-block device timing: when on, sqoc_eval records CUDA events around each
+ * block's work on the stream that launches it; sqoc_block_time_ms returns the
+ * last evaluation's duration for block `block` (large blocks share one group). */
+int sqoc_set_timing(sqoc_problem* p, int on);
+int sqoc_block_time_ms(const sqoc_problem* p, int block, double* ms);
+
 /* Device kernel launches issued by the last sqoc_eval on this problem. */
 int sqoc_last_launch_count(const sqoc_problem* p);
 

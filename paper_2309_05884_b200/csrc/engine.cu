@@ -48,6 +48,7 @@ struct BlockPlan {
   int nwarps = 1;
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;  // per-block device timing (sqoc_set_timing)
 };
 
 }  // namespace sqoc
@@ -68,6 +69,8 @@ struct sqoc_problem {
   sqoc::LargeGroup* large = nullptr;  // all blocks with d > kTinyMaxDim, advanced together
   cudaStream_t large_stream = nullptr;
   cudaEvent_t large_done = nullptr;
+  cudaEvent_t large_t0 = nullptr, large_t1 = nullptr;
+  bool timing = false;
   int launches = 0;
 };
 
@@ -149,6 +152,8 @@ static void free_problem(sqoc_problem* p) {
     cudaFree(b.park);
     if (b.stream) cudaStreamDestroy(b.stream);
     if (b.done) cudaEventDestroy(b.done);
+    if (b.t0) cudaEventDestroy(b.t0);
+    if (b.t1) cudaEventDestroy(b.t1);
   }
   cudaFree(p->u_dev);
   cudaFree(p->grad_dev);
@@ -164,6 +169,8 @@ static void free_problem(sqoc_problem* p) {
   }
   if (p->large_stream) cudaStreamDestroy(p->large_stream);
   if (p->large_done) cudaEventDestroy(p->large_done);
+  if (p->large_t0) cudaEventDestroy(p->large_t0);
+  if (p->large_t1) cudaEventDestroy(p->large_t1);
   delete p;
 }
 
@@ -239,6 +246,8 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
     }
     chk(cudaStreamCreateWithFlags(&bp.stream, cudaStreamNonBlocking), "stream");
     chk(cudaEventCreateWithFlags(&bp.done, cudaEventDisableTiming), "event");
+    chk(cudaEventCreate(&bp.t0), "event");
+    chk(cudaEventCreate(&bp.t1), "event");
     if (bp.tiny) {
       const int R = objective == SQOC_OBJ_GATE ? d : 1;
       const int pg = 32 / d;
@@ -275,6 +284,8 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
     if (lrc != SQOC_OK) rc = fail(lrc, p->large->err);
     chk(cudaStreamCreateWithFlags(&p->large_stream, cudaStreamNonBlocking), "stream");
     chk(cudaEventCreateWithFlags(&p->large_done, cudaEventDisableTiming), "event");
+    chk(cudaEventCreate(&p->large_t0), "event");
+    chk(cudaEventCreate(&p->large_t1), "event");
   }
   if (rc == SQOC_OK) {
     chk(cudaMalloc(&p->u_dev, std::max<size_t>(1, max_batch * KN) * sizeof(double)), "cudaMalloc u");
@@ -330,6 +341,7 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
       // empty grid: X_N = X_0 (qoc.py test_empty_grid_gives_empty_gradient)
     }
     if (!bp.tiny) continue;
+    if (p->timing) SQOC_CUDA(cudaEventRecord(bp.t0, bp.stream));
     {
       TinyParams tp;
       tp.K = p->K;
@@ -354,6 +366,7 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
       if (rc != SQOC_OK) return rc;
       p->launches += 1;
     }
+    if (p->timing) SQOC_CUDA(cudaEventRecord(bp.t1, bp.stream));
     SQOC_CUDA(cudaEventRecord(bp.done, bp.stream));
     SQOC_CUDA(cudaStreamWaitEvent(st, bp.done, 0));
   }
@@ -366,8 +379,10 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
     la.tau_stride = p->nblocks;
     la.gradb = p->gradb;
     la.gradb_block_stride = (size_t)p->max_batch * KN;
+    if (p->timing) SQOC_CUDA(cudaEventRecord(p->large_t0, p->large_stream));
     int rc = large_eval(*p->large, la, p->large_stream);
     if (rc != SQOC_OK) return fail(rc, p->large->err);
+    if (p->timing) SQOC_CUDA(cudaEventRecord(p->large_t1, p->large_stream));
     p->launches += p->large->launches;
     SQOC_CUDA(cudaEventRecord(p->large_done, p->large_stream));
     SQOC_CUDA(cudaStreamWaitEvent(st, p->large_done, 0));
@@ -394,6 +409,22 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
   }
   SQOC_CUDA(cudaStreamSynchronize(st));
   if (flag) return fail(SQOC_ERR_NONFINITE, "objective or gradient became non-finite");
+  return SQOC_OK;
+}
+
+int sqoc_set_timing(sqoc_problem* p, int on) {
+  if (!p) return fail(SQOC_ERR_ARG, "problem is NULL");
+  p->timing = on != 0;
+  return SQOC_OK;
+}
+
+int sqoc_block_time_ms(const sqoc_problem* p, int block, double* ms) {
+  if (!p || !ms || block < 0 || block >= p->nblocks) return fail(SQOC_ERR_ARG, "bad block index");
+  const BlockPlan& bp = p->blocks[block];
+  float t = 0.f;
+  cudaError_t e = bp.tiny ? cudaEventElapsedTime(&t, bp.t0, bp.t1) : cudaEventElapsedTime(&t, p->large_t0, p->large_t1);
+  if (e != cudaSuccess) return fail(SQOC_ERR_CUDA, std::string("cudaEventElapsedTime: ") + cudaGetErrorString(e));
+  *ms = t;
   return SQOC_OK;
 }
 

@@ -84,6 +84,23 @@ class GrapeEngine:
             pass
 
     @property
+    def large_blocks(self) -> list:
+        tiny_max = self.lib.sqoc_tiny_max_dim()
+        return [b for b, d in enumerate(self.dims) if d > tiny_max]
+
+    def set_timing(self, on: bool) -> None:
+        _lib.check(self.lib.sqoc_set_timing(self.handle, 1 if on else 0), "sqoc_set_timing")
+
+    def block_times_ms(self) -> list:
+        """Device time of each block's work in the last evaluation (needs set_timing(True))."""
+        out = []
+        for b in range(self.nblocks):
+            ms = ctypes.c_double()
+            _lib.check(self.lib.sqoc_block_time_ms(self.handle, b, ctypes.byref(ms)), "sqoc_block_time_ms")
+            out.append(ms.value)
+        return out
+
+    @property
     def last_launches(self) -> int:
         return self.lib.sqoc_last_launch_count(self.handle)
 
@@ -110,6 +127,11 @@ class GrapeEngine:
     def objective(self, u):
         """objective(u) -> (F, grad): the BASELINE host API."""
         return self.evaluate(u)
+
+    def evaluate_host_ptr(self, u_ptr: int, batch: int, F_ptr: int, grad_ptr: int):
+        """Host pointers (e.g. pinned torch tensors); copies happen inside the call."""
+        rc = self.lib.sqoc_eval(self.handle, u_ptr, batch, F_ptr or None, grad_ptr or None, None, _lib.MEM_HOST, None)
+        _lib.check(rc, "sqoc_eval")
 
     def evaluate_device(self, u_ptr: int, batch: int, F_ptr: int, grad_ptr: int, tau_ptr: int = 0,
                         stream: int = 0):
