@@ -73,6 +73,20 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
 int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* grad, double* tau,
               int memory, void* stream);
 
+/* Optional tighter norm bounds for the propagator plan: bounds[b * (n_controls+1) + k]
+ * >= ||H_k,b||_2 (k = 0 is H0).  A_j = -i dt (H0 + sum_k u_kj H_k) is normal, so
+ * dt (||H0||_2 + sum_k |u_kj| ||H_k||_2) bounds ||A_j||_2 and the Taylor truncation
+ * error rigorously.  Without this call the plan uses infinity-norms (also rigorous,
+ * looser: more products per slice). */
+int sqoc_set_norm_bounds(sqoc_problem* p, const double* bounds);
+
+/* Large-block schedule: -1 auto (default), 0 slice-sequential (no history; memory
+ * O(sum d_b^2)), 1 history (all slices resident, slice-batched GEMMs; memory
+ * O(N sum d_b^2)).  sqoc_last_schedule reports what the last sqoc_eval used
+ * (-1 when the problem has no large blocks). */
+int sqoc_set_schedule(sqoc_problem* p, int schedule);
+int sqoc_last_schedule(const sqoc_problem* p);
+
 /* Free all device memory of the problem. */
 int sqoc_destroy(sqoc_problem* p);
 

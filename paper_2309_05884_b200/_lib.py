@@ -37,6 +37,9 @@ SIGNATURES = {
     "sqoc_state_gradient": (_I, [_I, _I, _D, _D, _D, _D, _D, _D, _D, _I, ctypes.c_double, _D, _D, _D]),
     "sqoc_last_launch_count": (_I, [_P]),
     "sqoc_set_timing": (_I, [_P, _I]),
+    "sqoc_set_schedule": (_I, [_P, _I]),
+    "sqoc_last_schedule": (_I, [_P]),
+    "sqoc_set_norm_bounds": (_I, [_P, _D]),
     "sqoc_block_time_ms": (_I, [_P, _I, _D]),
     "sqoc_tiny_max_dim": (_I, []),
     "sqoc_last_error": (ctypes.c_char_p, []),

@@ -412,6 +412,29 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
   return SQOC_OK;
 }
 
+int sqoc_set_norm_bounds(sqoc_problem* p, const double* bounds) {
+  if (!p || !bounds) return fail(SQOC_ERR_ARG, "problem or bounds is NULL");
+  const int K1 = p->K + 1;
+  for (int i = 0; i < p->nblocks * K1; ++i)
+    if (!(bounds[i] >= 0.0) || !std::isfinite(bounds[i])) return fail(SQOC_ERR_ARG, "bounds must be finite and >= 0");
+  if (p->large) {
+    std::vector<double> gn;
+    for (const auto& ls : p->large->blocks)
+      for (int k = 0; k < K1; ++k) gn.push_back(p->dt * bounds[ls.global_index * K1 + k]);
+    int rc = large_set_norms(*p->large, gn);
+    if (rc != SQOC_OK) return fail(rc, p->large->err);
+  }
+  return SQOC_OK;
+}
+
+int sqoc_set_schedule(sqoc_problem* p, int schedule) {
+  if (!p || schedule < -1 || schedule > 1) return fail(SQOC_ERR_ARG, "schedule must be -1 (auto), 0 or 1");
+  if (p->large) p->large->force_mode = schedule;
+  return SQOC_OK;
+}
+
+int sqoc_last_schedule(const sqoc_problem* p) { return (p && p->large) ? p->large->mode : -1; }
+
 int sqoc_set_timing(sqoc_problem* p, int on) {
   if (!p) return fail(SQOC_ERR_ARG, "problem is NULL");
   p->timing = on != 0;

@@ -47,15 +47,18 @@ __global__ void bound_kernel(const double* __restrict__ u, int K, int N, int nbl
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
 }
 
-__global__ void build_a_kernel(int j, int K, int N, const double* __restrict__ u, const int* __restrict__ dims,
+// A[z][b] = (a_0 + sum_k u_k,(j0+z) a_k) * scale  for slice z of a slice batch (blockIdx.z)
+__global__ void build_a_kernel(int j0, int K, int N, const double* __restrict__ u, const int* __restrict__ dims,
                                const size_t* __restrict__ off, const double2* const* __restrict__ gen, double scale,
-                               double2* __restrict__ A) {
+                               double2* __restrict__ A, size_t slice_stride) {
   const int b = blockIdx.y;
+  const int j = j0 + blockIdx.z;
   const int d = dims[b];
   const size_t dd = (size_t)d * d;
   const double2* g = gen[b];
   double uk[4];
   for (int k = 0; k < 4; ++k) uk[k] = k < K ? u[k * N + j] : 0.0;
+  double2* out = A + blockIdx.z * slice_stride + off[b];
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < dd; i += (size_t)gridDim.x * blockDim.x) {
     double2 a = g[i];
     for (int k = 0; k < K; ++k) {
@@ -63,26 +66,75 @@ __global__ void build_a_kernel(int j, int K, int N, const double* __restrict__ u
       a.x = fma(uk[k], e.x, a.x);
       a.y = fma(uk[k], e.y, a.y);
     }
-    A[off[b] + i] = make_double2(a.x * scale, a.y * scale);
+    out[i] = make_double2(a.x * scale, a.y * scale);
   }
 }
 
-// T = cm A3 + c0 I + c1 A + c2 A2 ;  dT = cm dA3 + c1 Ad + c2 dA2 (when pair)
+// T = cm A3 + c0 I + c1 A + c2 A2 ;  dT = cm dA3 + c1 Ad + c2 dA2 (when pair); slice batch on blockIdx.z
 __global__ void horner_init_kernel(int pair, const int* __restrict__ dims, const size_t* __restrict__ off, double cm,
                                    double c0, double c1, double c2, const double2* __restrict__ A,
                                    const double2* __restrict__ A2, const double2* __restrict__ A3,
                                    const double2* __restrict__ Ad, const double2* __restrict__ dA2,
-                                   const double2* __restrict__ dA3, double2* __restrict__ T, double2* __restrict__ dT) {
+                                   const double2* __restrict__ dA3, double2* __restrict__ T, double2* __restrict__ dT,
+                                   size_t slice_stride) {
   const int b = blockIdx.y;
   const int d = dims[b];
   const size_t dd = (size_t)d * d;
+  const size_t base = blockIdx.z * slice_stride + off[b];
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < dd; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t o = off[b] + i;
-    double2 t = make_double2(cm * A3[o].x + c1 * A[o].x + c2 * A2[o].x, cm * A3[o].y + c1 * A[o].y + c2 * A2[o].y);
-    if (i / d == i % d) t.x += c0;
-    T[o] = t;
+    const size_t o = base + i;
+    if (T) {
+      double2 t = make_double2(cm * A3[o].x + c1 * A[o].x + c2 * A2[o].x, cm * A3[o].y + c1 * A[o].y + c2 * A2[o].y);
+      if (i / d == i % d) t.x += c0;
+      T[o] = t;
+    }
     if (pair)
       dT[o] = make_double2(cm * dA3[o].x + c1 * Ad[o].x + c2 * dA2[o].x, cm * dA3[o].y + c1 * Ad[o].y + c2 * dA2[o].y);
+  }
+}
+
+// g[z][b][k] = sum_pq M[z][b][p][q] * a_k[q][p]   (one CTA per (block, slice); fixed tree)
+__global__ void slice_trace_kernel(int K, const int* __restrict__ dims, const size_t* __restrict__ off,
+                                   const double2* const* __restrict__ gent, const double2* __restrict__ M,
+                                   size_t slice_stride, double2* __restrict__ out, int nblk) {
+  __shared__ double2 red[4][256];
+  const int b = blockIdx.x, z = blockIdx.y;
+  const int d = dims[b];
+  const size_t dd = (size_t)d * d;
+  const double2* m = M + z * slice_stride + off[b];
+  double sx[4] = {0, 0, 0, 0}, sy[4] = {0, 0, 0, 0};
+  for (size_t i = threadIdx.x; i < dd; i += blockDim.x) {
+    const double2 v = m[i];
+    for (int k = 0; k < K; ++k) {
+      const double2 e = gent[b][(size_t)k * dd + i];  // a_k^T stored row-major
+      sx[k] += v.x * e.x - v.y * e.y;
+      sy[k] += v.x * e.y + v.y * e.x;
+    }
+  }
+  for (int k = 0; k < K; ++k) red[k][threadIdx.x] = make_double2(sx[k], sy[k]);
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int k = 0; k < K; ++k) {
+        red[k][threadIdx.x].x += red[k][threadIdx.x + st].x;
+        red[k][threadIdx.x].y += red[k][threadIdx.x + st].y;
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < K) out[((size_t)z * nblk + b) * K + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// gradb[gidx_b][k][j] = 2 w_b Re(conj(tau_b) g[j][b][k])
+__global__ void hist_grad_kernel(int K, int N, int nblk, const double2* __restrict__ g, const double2* __restrict__ tau,
+                                 const double* __restrict__ w, const int* __restrict__ gidx, double* __restrict__ gradb,
+                                 size_t block_stride) {
+  const size_t total = (size_t)N * nblk * K;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int k = i % K;
+    const int b = (i / K) % nblk;
+    const int j = i / ((size_t)K * nblk);
+    const double2 v = g[i], t = tau[b];
+    gradb[gidx[b] * block_stride + (size_t)k * N + j] = 2.0 * w[b] * (t.x * v.x + t.y * v.y);
   }
 }
 
@@ -158,6 +210,23 @@ __global__ void trace_reduce_kernel(int j, int K, int N, const int* __restrict__
       gradb[gidx[b] * block_stride + (size_t)k * N + j] = 2.0 * w[b] * (t.x * g.x + t.y * g.y);
     }
     __syncthreads();
+  }
+}
+
+// out[k][c][r] = in[k][r][c]  (K stacked d x d matrices)
+__global__ void transpose_kernel(const double2* __restrict__ in, double2* __restrict__ out, int d) {
+  __shared__ double2 tile[32][33];
+  const size_t base = (size_t)blockIdx.z * d * d;
+  const int x = blockIdx.x * 32 + threadIdx.x;
+  for (int yy = threadIdx.y; yy < 32; yy += 8) {
+    const int y = blockIdx.y * 32 + yy;
+    if (x < d && y < d) tile[yy][threadIdx.x] = in[base + (size_t)y * d + x];
+  }
+  __syncthreads();
+  const int ox = blockIdx.y * 32 + threadIdx.x;
+  for (int yy = threadIdx.y; yy < 32; yy += 8) {
+    const int oy = blockIdx.x * 32 + yy;
+    if (ox < d && oy < d) out[base + (size_t)oy * d + ox] = tile[threadIdx.x][yy];
   }
 }
 
@@ -342,8 +411,33 @@ int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, 
   LCHK(cudaMemcpy(g.w_dev, w.data(), g.nblk * sizeof(double), cudaMemcpyHostToDevice));
   LCHK(cudaMalloc(&g.gidx_dev, g.nblk * sizeof(int)));
   LCHK(cudaMemcpy(g.gidx_dev, gidx.data(), g.nblk * sizeof(int), cudaMemcpyHostToDevice));
+  {  // a_k^T per block for the history-mode slice traces
+    std::vector<const double2*> gt;
+    for (int b = 0; b < g.nblk; ++b) {
+      const int d = blocks[b].d;
+      double2* t = nullptr;
+      LCHK(cudaMalloc(&t, (size_t)K * d * d * sizeof(double2)));
+      transpose_kernel<<<dim3((d + 31) / 32, (d + 31) / 32, K), dim3(32, 8)>>>(blocks[b].gen + (size_t)d * d, t, d);
+      LCHK(cudaGetLastError());
+      g.gent_mem.push_back(t);
+      gt.push_back(t);
+    }
+    LCHK(cudaMalloc(&g.gent_dev, g.nblk * sizeof(double2*)));
+    LCHK(cudaMemcpy(g.gent_dev, gt.data(), g.nblk * sizeof(double2*), cudaMemcpyHostToDevice));
+  }
   LCHK(cudaMalloc(&g.tile_off_dev, (g.nblk + 1) * sizeof(int)));
   LCHK(cudaMemcpy(g.tile_off_dev, g.trace_tile_off.data(), (g.nblk + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  return SQOC_OK;
+}
+
+int large_set_norms(LargeGroup& g, const std::vector<double>& gn) {
+  if (gn.size() != (size_t)g.nblk * (g.K + 1)) {
+    g.err = "norm bound array has the wrong size";
+    return SQOC_ERR_ARG;
+  }
+  for (int b = 0; b < g.nblk; ++b)
+    for (int k = 0; k <= g.K; ++k) g.blocks[b].gen_norm[k] = gn[(size_t)b * (g.K + 1) + k];
+  LCHK(cudaMemcpy(g.gnorm_dev, gn.data(), gn.size() * sizeof(double), cudaMemcpyHostToDevice));
   return SQOC_OK;
 }
 
@@ -362,10 +456,203 @@ void large_free(LargeGroup& g) {
   cudaFree(g.w_dev);
   cudaFree(g.gidx_dev);
   cudaFree(g.tile_off_dev);
+  double2* hb[] = {g.h_chain, g.h_X, g.h_L, g.h_dA, g.h_dA2, g.h_dA3, g.h_dH[0], g.h_dH[1], g.h_g};
+  for (auto x : hb) cudaFree(x);
+  for (auto m : g.gent_mem) cudaFree(m);
+  g.gent_mem.clear();
+  cudaFree(g.gent_dev);
+  for (auto m : g.hlist_mem) cudaFree(m);
+  g.hlist_mem.clear();
+  g.hlists.clear();
   for (auto m : g.list_mem) cudaFree(m);
   g.list_mem.clear();
   g.lists.clear();
   g.list_tiles.clear();
+}
+
+// ------------------------------------------------------------------ history schedule
+enum HOp { H_A2, H_A3, H_H, H_S, H_X, H_L, H_B, H_DA2, H_DA3, H_DH, H_DS };
+
+static size_t history_bytes(const LargeGroup& g, int C) {
+  const size_t N = g.N;
+  return sizeof(double2) * ((size_t)(C + 5) * N * g.total + 2 * (N + 1) * g.totalr + N * g.nblk * g.K);
+}
+
+static void hist_free(LargeGroup& g) {
+  double2* hb[] = {g.h_chain, g.h_X, g.h_L, g.h_dA, g.h_dA2, g.h_dA3, g.h_dH[0], g.h_dH[1], g.h_g};
+  for (auto x : hb) cudaFree(x);
+  g.h_chain = g.h_X = g.h_L = g.h_dA = g.h_dA2 = g.h_dA3 = g.h_dH[0] = g.h_dH[1] = g.h_g = nullptr;
+  for (auto m : g.hlist_mem) cudaFree(m);
+  g.hlist_mem.clear();
+  g.hlists.clear();
+  g.h_C = 0;
+}
+
+static int hist_alloc(LargeGroup& g, int nb, int sq) {
+  const int C = 3 + nb + sq;
+  g.h_nb = nb;
+  g.h_s = sq;
+  if (C <= g.h_C) return SQOC_OK;  // buffers large enough; lists depend on (nb, s) via keys
+  hist_free(g);
+  const size_t N = g.N, sq_bytes = N * g.total * sizeof(double2);
+  LCHK(cudaMalloc(&g.h_chain, (size_t)C * sq_bytes));
+  LCHK(cudaMalloc(&g.h_X, (N + 1) * g.totalr * sizeof(double2)));
+  LCHK(cudaMalloc(&g.h_L, (N + 1) * g.totalr * sizeof(double2)));
+  double2** d5[] = {&g.h_dA, &g.h_dA2, &g.h_dA3, &g.h_dH[0], &g.h_dH[1]};
+  for (auto pp : d5) LCHK(cudaMalloc(pp, sq_bytes));
+  LCHK(cudaMalloc(&g.h_g, N * g.nblk * g.K * sizeof(double2)));
+  g.h_C = C;
+  return SQOC_OK;
+}
+
+// Work list for history op `op` (index idx, parity p), over slices [i0, i1) x blocks.
+static ListRef hist_list(LargeGroup& g, int op, int idx, int p, int i0, int i1) {
+  auto key = std::make_tuple(op * 1000000 + idx * 4 + p, g.h_nb * 100 + g.h_s, i0, i1);
+  auto it = g.hlists.find(key);
+  if (it != g.hlists.end()) return it->second;
+  std::vector<GemmItem> v;
+  const int nb = g.h_nb;
+  for (int i = i0; i < i1; ++i)
+    for (int b = 0; b < g.nblk; ++b) {
+      const int d = g.blocks[b].d, R = g.gate ? d : 1;
+      const size_t o = (size_t)i * g.total + g.off[b];
+      auto ch = [&](int c) { return g.h_chain + (size_t)c * g.N * g.total + o; };
+      double2 *A = ch(0), *A2 = ch(1), *A3 = ch(2), *U = ch(3 + nb + g.h_s - 1);
+      double2 *dA = g.h_dA + o, *dA2 = g.h_dA2 + o, *dA3 = g.h_dA3 + o;
+      double2 *dHp = g.h_dH[p] + o, *dHn = g.h_dH[1 - p] + o;
+      double2* Xi = g.h_X + (size_t)i * g.totalr + g.offr[b];
+      double2* Xn = g.h_X + (size_t)(i + 1) * g.totalr + g.offr[b];
+      double2* Li = g.h_L + (size_t)i * g.totalr + g.offr[b];
+      double2* Ln = g.h_L + (size_t)(i + 1) * g.totalr + g.offr[b];
+      switch (op) {
+        case H_A2: v.push_back(mk(A, A, 0, 0, A2, 0, 0, d, d, d, 1, d, d, d, 0)); break;
+        case H_A3: v.push_back(mk(A2, A, 0, 0, A3, 0, 0, d, d, d, 1, d, d, d, 0)); break;
+        case H_H: v.push_back(mk(ch(3 + idx - 1), A3, 0, 0, ch(3 + idx), A, A2, d, d, d, 1, d, d, d, 1)); break;
+        case H_S: v.push_back(mk(ch(3 + nb - 1 + idx - 1), ch(3 + nb - 1 + idx - 1), 0, 0, ch(3 + nb - 1 + idx), 0, 0,
+                                 d, d, d, 1, d, d, d, 0)); break;
+        case H_X: v.push_back(mk(U, Xi, 0, 0, Xn, 0, 0, d, R, d, 1, d, R, R, 0)); break;
+        case H_L: v.push_back(mk(U, Ln, 0, 0, Li, 0, 0, d, R, d, 1, d, R, R, 0)); break;
+        case H_B: v.push_back(mk(Xi, Ln, 0, 0, dA, 0, 0, d, d, R, 1, R, R, d, 0)); break;
+        case H_DA2: v.push_back(mk(A, dA, dA, A, dA2, 0, 0, d, d, d, 2, d, d, d, 0)); break;
+        case H_DA3: v.push_back(mk(A2, dA, dA2, A, dA3, 0, 0, d, d, d, 2, d, d, d, 0)); break;
+        case H_DH: v.push_back(mk(dHp, A3, ch(3 + idx - 1), dA3, dHn, dA, dA2, d, d, d, 2, d, d, d, 0)); break;
+        case H_DS: {
+          double2* S = ch(3 + nb - 1 + idx - 1);
+          v.push_back(mk(S, dHp, dHp, S, dHn, 0, 0, d, d, d, 2, d, d, d, 0));
+          break;
+        }
+      }
+    }
+  int t = 0;
+  for (auto& x : v) {
+    x.tile_start = t;
+    t += tiles_of(x.m, x.n);
+  }
+  ListRef ref;
+  if (cudaMalloc(&ref.dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return ListRef{};
+  cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
+  ref.n = (int)v.size();
+  ref.tiles = t;
+  g.hlist_mem.push_back(ref.dev);
+  g.hlists[key] = ref;
+  return ref;
+}
+
+static int hgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArgs a, cudaStream_t st) {
+  ListRef l = hist_list(g, op, idx, p, i0, i1);
+  if (!l.dev) {
+    g.err = "history work list allocation failed";
+    return SQOC_ERR_CUDA;
+  }
+  cudaError_t e;
+  if (op == H_L) e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
+  else if (op == H_B) e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
+  else e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
+  if (e != cudaSuccess) {
+    g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
+    return SQOC_ERR_CUDA;
+  }
+  g.launches++;
+  return SQOC_OK;
+}
+
+static int large_eval_history(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, int nb, int sq,
+                              cudaStream_t st) {
+  const int K = g.K, N = g.N, nblk = g.nblk;
+  int maxd = 0;
+  for (auto& b : g.blocks) maxd = std::max(maxd, b.d);
+  const unsigned ew_x = (unsigned)std::max<size_t>(1, std::min<size_t>(((size_t)maxd * maxd + 255) / 256, 64));
+  const dim3 grid_all(ew_x, nblk, N);
+  const double scale = std::ldexp(1.0, -sq);
+  const double cm = inv_fact(3 * nb);
+  const size_t stride = g.total;
+  auto ch = [&](int c) { return g.h_chain + (size_t)c * N * g.total; };
+  GemmArgs one{1.0, 0.0, 0.0, 0.0};
+  int rc;
+  // ---- forward: all propagators, every intermediate kept ----
+  build_a_kernel<<<grid_all, 256, 0, st>>>(0, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, ch(0), stride);
+  LCHK(cudaGetLastError());
+  g.launches++;
+  if ((rc = hgemm(g, H_A2, 0, 0, 0, N, one, st))) return rc;
+  if ((rc = hgemm(g, H_A3, 0, 0, 0, N, one, st))) return rc;
+  {
+    const int q = nb - 1;
+    horner_init_kernel<<<grid_all, 256, 0, st>>>(0, g.d_dev, g.off_dev, cm, inv_fact(3 * q), inv_fact(3 * q + 1),
+                                                 inv_fact(3 * q + 2), ch(0), ch(1), ch(2), nullptr, nullptr, nullptr,
+                                                 ch(3), nullptr, stride);
+    LCHK(cudaGetLastError());
+    g.launches++;
+  }
+  for (int t = 1; t <= nb - 1; ++t) {
+    const int q = nb - 1 - t;
+    if ((rc = hgemm(g, H_H, t, 0, 0, N, GemmArgs{1.0, inv_fact(3 * q + 1), inv_fact(3 * q + 2), inv_fact(3 * q)}, st)))
+      return rc;
+  }
+  for (int i = 1; i <= sq; ++i)
+    if ((rc = hgemm(g, H_S, i, 0, 0, N, one, st))) return rc;
+  // ---- forward / backward recurrences (sequential over slices, batched over blocks) ----
+  const dim3 ew_grid(ew_x, nblk);
+  init_xl_kernel<<<ew_grid, 256, 0, st>>>(g.gate, 1, g.d_dev, g.offr_dev, g.x0_dev, g.tgt_dev, g.h_X,
+                                          g.h_L + (size_t)N * g.totalr);
+  LCHK(cudaGetLastError());
+  g.launches++;
+  for (int i = 0; i < N; ++i)
+    if ((rc = hgemm(g, H_X, 0, 0, i, i + 1, one, st))) return rc;
+  tau_kernel<<<nblk, 256, 0, st>>>(g.gate, 1, g.d_dev, g.offr_dev, g.h_X + (size_t)N * g.totalr, g.tgt_dev, g.tau_dev,
+                                   a.tau_out + (size_t)s_idx * a.tau_stride, g.gidx_dev);
+  LCHK(cudaGetLastError());
+  g.launches++;
+  for (int i = N - 1; i >= 0; --i)
+    if ((rc = hgemm(g, H_L, 0, 0, i, i + 1, one, st))) return rc;
+  // ---- Frechet derivatives of every slice: L_R(A_i, X_i Lam_{i+1}^dag), derivative-only chain ----
+  if ((rc = hgemm(g, H_B, 0, 0, 0, N, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
+  if ((rc = hgemm(g, H_DA2, 0, 0, 0, N, one, st))) return rc;
+  if ((rc = hgemm(g, H_DA3, 0, 0, 0, N, one, st))) return rc;
+  {
+    const int q = nb - 1;
+    horner_init_kernel<<<grid_all, 256, 0, st>>>(1, g.d_dev, g.off_dev, cm, 0.0, inv_fact(3 * q + 1),
+                                                 inv_fact(3 * q + 2), nullptr, nullptr, nullptr, g.h_dA, g.h_dA2,
+                                                 g.h_dA3, nullptr, g.h_dH[0], stride);
+    LCHK(cudaGetLastError());
+    g.launches++;
+  }
+  int p = 0;
+  for (int t = 1; t <= nb - 1; ++t) {
+    const int q = nb - 1 - t;
+    if ((rc = hgemm(g, H_DH, t, p, 0, N, GemmArgs{1.0, inv_fact(3 * q + 1), inv_fact(3 * q + 2), 0.0}, st))) return rc;
+    p ^= 1;
+  }
+  for (int i = 1; i <= sq; ++i) {
+    if ((rc = hgemm(g, H_DS, i, p, 0, N, one, st))) return rc;
+    p ^= 1;
+  }
+  slice_trace_kernel<<<dim3(nblk, N), 256, 0, st>>>(K, g.d_dev, g.off_dev, g.gent_dev, g.h_dH[p], stride, g.h_g, nblk);
+  LCHK(cudaGetLastError());
+  hist_grad_kernel<<<256, 256, 0, st>>>(K, N, nblk, g.h_g, g.tau_dev, g.w_dev, g.gidx_dev,
+                                        a.gradb + (size_t)s_idx * K * N, a.gradb_block_stride);
+  LCHK(cudaGetLastError());
+  g.launches += 2;
+  return SQOC_OK;
 }
 
 int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
@@ -388,6 +675,24 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
     g.launches++;
     int nb, sq;
     choose_taylor_host(bound, nb, sq);
+    {  // history schedule when every slice's chain fits comfortably in free memory
+      bool use_hist = g.force_mode == 1;
+      if (g.force_mode == -1 && N > 0) {
+        size_t free_b = 0, total_b = 0;
+        LCHK(cudaMemGetInfo(&free_b, &total_b));
+        const size_t have = g.h_C ? history_bytes(g, g.h_C) : 0;
+        use_hist = history_bytes(g, 3 + nb + sq) <= (size_t)(0.6 * (double)(free_b + have));
+      }
+      if (use_hist && N > 0) {
+        int rc = hist_alloc(g, nb, sq);
+        if (rc != SQOC_OK) return rc;
+        g.mode = 1;
+        rc = large_eval_history(g, a, s, u, nb, sq, st);
+        if (rc != SQOC_OK) return rc;
+        continue;
+      }
+      g.mode = 0;
+    }
     const double scale = std::ldexp(1.0, -sq);
     const double cm = inv_fact(3 * nb);
     // ---- forward sweep ----
@@ -397,7 +702,7 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
     int q = 0, r = 0;
     GemmArgs one{1.0, 0.0, 0.0, 0.0};
     for (int j = 0; j < N; ++j) {
-      build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A);
+      build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
       LCHK(cudaGetLastError());
       g.launches++;
       int rc;
@@ -406,7 +711,7 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
       const int t0 = nb - 1;
       horner_init_kernel<<<ew_grid, 256, 0, st>>>(0, g.d_dev, g.off_dev, cm, inv_fact(3 * t0), inv_fact(3 * t0 + 1),
                                                   inv_fact(3 * t0 + 2), g.A, g.A2, g.A3, g.Ad, g.dA2, g.dA3, g.T[0],
-                                                  g.dT[0]);
+                                                  g.dT[0], 0);
       LCHK(cudaGetLastError());
       g.launches++;
       int p = 0;
@@ -428,7 +733,7 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
     g.launches++;
     // ---- backward sweep ----
     for (int j = N - 1; j >= 0; --j) {
-      build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A);
+      build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
       LCHK(cudaGetLastError());
       g.launches++;
       int rc;
@@ -438,7 +743,7 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
       const int t0 = nb - 1;
       horner_init_kernel<<<ew_grid, 256, 0, st>>>(1, g.d_dev, g.off_dev, cm, inv_fact(3 * t0), inv_fact(3 * t0 + 1),
                                                   inv_fact(3 * t0 + 2), g.A, g.A2, g.A3, g.Ad, g.dA2, g.dA3, g.T[0],
-                                                  g.dT[0]);
+                                                  g.dT[0], 0);
       LCHK(cudaGetLastError());
       g.launches++;
       int p = 0;

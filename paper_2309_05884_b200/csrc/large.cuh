@@ -43,6 +43,11 @@ struct LargeBlockSpec {
   double gen_norm[5];     // inf-norm bounds of a_0..a_K
 };
 
+struct ListRef {
+  GemmItem* dev = nullptr;
+  int n = 0, tiles = 0;
+};
+
 struct LargeGroup {
   int nblk = 0, K = 0, N = 0;  // X / Lam have d columns per block (gate) or 1 (state)
   bool gate = true;
@@ -73,12 +78,26 @@ struct LargeGroup {
   std::map<std::tuple<int, int, int, int>, int> list_tiles;
   std::vector<void*> list_mem;
   int* tile_off_dev = nullptr;    // [nblk + 1] trace tile offsets
+  // ---- history schedule: every slice resident, slice-batched GEMMs (chosen when memory allows) ----
+  int h_nb = -1, h_s = -1, h_C = 0;
+  double2* h_chain = nullptr;       // [C][N][total]: A, A2, A3, H_0..H_{nb-1}, S_1..S_s
+  double2* h_X = nullptr;           // [N+1][totalr]
+  double2* h_L = nullptr;           // [N+1][totalr]
+  double2 *h_dA = nullptr, *h_dA2 = nullptr, *h_dA3 = nullptr, *h_dH[2] = {nullptr, nullptr};  // [N][total]
+  double2* h_g = nullptr;           // [N][nblk][K] traces
+  const double2** gent_dev = nullptr;  // per block a_k^T (K d*d), for the slice traces
+  std::vector<void*> gent_mem;
+  std::map<std::tuple<int, int, int, int>, ListRef> hlists;
+  std::vector<void*> hlist_mem;
+  int mode = -1;                    // last schedule used: 0 sequential, 1 history
+  int force_mode = -1;              // -1 auto, 0 sequential, 1 history
   int launches = 0;
   std::string err;
 };
 
 int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, int N, bool gate);
 int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st);
+int large_set_norms(LargeGroup& g, const std::vector<double>& gnorm);
 void large_free(LargeGroup& g);
 
 }  // namespace sqoc

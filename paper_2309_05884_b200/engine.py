@@ -13,6 +13,21 @@ import numpy as np
 from . import _lib
 
 
+def spectral_norm_bound(h: np.ndarray) -> float:
+    """Upper bound of ||H||_2 for a Hermitian generator (host setup, not the hot path).
+
+    Dense eigvalsh up to d = 512, Lanczos (ARPACK, largest magnitude) above; a
+    relative margin of 1e-6 covers the iteration tolerance.
+    """
+    h = np.asarray(h)
+    if h.shape[0] <= 512:
+        return float(np.abs(np.linalg.eigvalsh(h)).max()) * (1 + 1e-12) + 1e-300
+    from scipy.sparse.linalg import eigsh
+
+    lam = eigsh(h, k=1, which="LM", return_eigenvectors=False, tol=1e-10)
+    return float(np.abs(lam).max()) * (1 + 1e-6)
+
+
 def _cplx(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
 
@@ -25,7 +40,7 @@ class GrapeEngine:
     ``n_slices``, and optionally ``block_weights()``.
     """
 
-    def __init__(self, system, max_batch: int = 1, device: int = 0):
+    def __init__(self, system, max_batch: int = 1, device: int = 0, spectral_bounds: bool = True):
         self.lib = _lib.load()
         self.system = system
         self.K = len(system.blocks[0].hk)
@@ -71,6 +86,10 @@ class GrapeEngine:
         )
         _lib.check(rc, "sqoc_create")
         self.handle = handle
+        if spectral_bounds and max(dims) > self.lib.sqoc_tiny_max_dim():
+            bounds = np.array([[spectral_norm_bound(m) for m in (blk.h0, *blk.hk)] for blk in system.blocks])
+            _lib.check(self.lib.sqoc_set_norm_bounds(self.handle, np.ascontiguousarray(bounds).ctypes.data_as(
+                ctypes.POINTER(ctypes.c_double))), "sqoc_set_norm_bounds")
 
     def close(self):
         if getattr(self, "handle", None):
@@ -87,6 +106,16 @@ class GrapeEngine:
     def large_blocks(self) -> list:
         tiny_max = self.lib.sqoc_tiny_max_dim()
         return [b for b, d in enumerate(self.dims) if d > tiny_max]
+
+    SCHEDULES = {"auto": -1, "sequential": 0, "history": 1}
+
+    def set_schedule(self, name: str) -> None:
+        """Large-block schedule: 'auto', 'sequential' (O(sum d^2) memory) or 'history' (slice-batched)."""
+        _lib.check(self.lib.sqoc_set_schedule(self.handle, self.SCHEDULES[name]), "sqoc_set_schedule")
+
+    @property
+    def last_schedule(self) -> str:
+        return {-1: "none", 0: "sequential", 1: "history"}[self.lib.sqoc_last_schedule(self.handle)]
 
     def set_timing(self, on: bool) -> None:
         _lib.check(self.lib.sqoc_set_timing(self.handle, 1 if on else 0), "sqoc_set_timing")

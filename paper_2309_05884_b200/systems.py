@@ -179,18 +179,24 @@ def gate_all_to_all(n: int, T: float, n_slices: int, seed: int = 0) -> GrapeSyst
 
 
 def config(index: int, seed: int = 0, **overrides) -> GrapeSystem:
-    """BASELINE.json configs[index]."""
+    """BASELINE.json configs[index].
+
+    ``n_slices`` may be overridden for short runs; dt stays the config's dt
+    (T scales with N) unless ``T`` is given too.
+    """
+    base_n = {0: 100, 1: 1000, 2: 500, 3: 500, 4: 200}[index]
+    n_sl = overrides.get("n_slices", base_n)
+    T = overrides.get("T", 10.0 * n_sl / base_n)
     if index == 0:
-        return state_transfer_ring(overrides.get("n", 6), 10.0, overrides.get("n_slices", 100), seed)
+        return state_transfer_ring(overrides.get("n", 6), T, n_sl, seed)
     if index == 1:
-        return gate_all_to_all(overrides.get("n", 12), 10.0, overrides.get("n_slices", 1000), seed)
+        return gate_all_to_all(overrides.get("n", 12), T, n_sl, seed)
     if index == 2:
-        return gate_ring(overrides.get("n", 10), 10.0, overrides.get("n_slices", 500), seed)
+        return gate_ring(overrides.get("n", 10), T, n_sl, seed)
     if index == 3:
-        return gate_ring(overrides.get("n", 14), 10.0, overrides.get("n_slices", 500), seed)
+        return gate_ring(overrides.get("n", 14), T, n_sl, seed)
     if index == 4:
-        return state_transfer_ring(overrides.get("n", 12), 10.0, overrides.get("n_slices", 200), seed,
-                                   full=overrides.get("full", True))
+        return state_transfer_ring(overrides.get("n", 12), T, n_sl, seed, full=overrides.get("full", True))
     raise ValueError(f"no config {index}")
 
 

@@ -16,11 +16,17 @@ def rel(a, b):
     return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300)
 
 
-def test_d8_ring_mixed_tiny_and_large_blocks():
+SCHEDULES = ["sequential", "history"]
+
+
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_d8_ring_mixed_tiny_and_large_blocks(schedule):
     s = systems.gate_ring(8, 10.0, 30)  # blocks 30,6,13,21,30,30,33,33,30,30
     eng = GrapeEngine(s, max_batch=2)
+    eng.set_schedule(schedule)
     u = s.controls(4, batch=2)
     F, g, tau = eng.evaluate(u, want_tau=True)
+    assert eng.last_schedule == schedule
     for b in range(2):
         Fo, go, per_block = O.objective(s, u[b])
         assert abs(F[b] - Fo) <= F_TOL
@@ -28,9 +34,11 @@ def test_d8_ring_mixed_tiny_and_large_blocks():
         np.testing.assert_allclose(s.block_weights() * np.abs(tau[b]) ** 2, per_block, atol=F_TOL)
 
 
-def test_cfg2_blocks_short_grid_against_oracle():
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_cfg2_blocks_short_grid_against_oracle(schedule):
     s = systems.config(2, n_slices=24)
     eng = GrapeEngine(s, max_batch=1)
+    eng.set_schedule(schedule)
     u = s.controls(9)
     F, g = eng.objective(u)
     Fo, go, _ = O.objective(s, u)
@@ -44,6 +52,11 @@ def test_cfg2_full_grid_fidelity_and_fd_gradient():
     eng = GrapeEngine(s, max_batch=1)
     u = s.controls(0)
     F, g = eng.objective(u)
+    assert eng.last_schedule == "history"  # auto picks the slice-batched schedule at this size
+    eng.set_schedule("sequential")
+    F2, g2 = eng.objective(u)
+    assert abs(F - F2) <= F_TOL and rel(g2, g) <= G_TOL
+    eng.set_schedule("auto")
     w = s.block_weights()
     Fo = 0.0
     for b, blk in enumerate(s.blocks):
@@ -63,9 +76,11 @@ def test_cfg2_full_grid_fidelity_and_fd_gradient():
         assert abs(fd - g[k, j]) / max(abs(fd), abs(g[k, j]), rms) < 1e-6
 
 
-def test_state_transfer_full_space_d64_against_oracle():
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_state_transfer_full_space_d64_against_oracle(schedule):
     s = systems.state_transfer_ring(6, 10.0, 40, seed=3, full=True)  # 64 x 64 dense
     eng = GrapeEngine(s, max_batch=1)
+    eng.set_schedule(schedule)
     u = s.controls(1)
     F, g = eng.objective(u)
     Fo, go, _ = O.objective(s, u)
@@ -78,7 +93,8 @@ def test_symmetric_equals_conventional_state_transfer():
     full = systems.state_transfer_ring(10, 10.0, 20, seed=5, full=True)
     blk = systems.state_transfer_ring(10, 10.0, 20, seed=5, full=False)
     u = full.controls(2)
-    Ff, gf = GrapeEngine(full, max_batch=1).objective(u)
+    ef = GrapeEngine(full, max_batch=1)
+    Ff, gf = ef.objective(u)
     Fb, gb = GrapeEngine(blk, max_batch=1).objective(u)
     assert abs(Ff - Fb) <= F_TOL
     assert rel(gf, gb) <= G_TOL
