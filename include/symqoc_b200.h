@@ -82,10 +82,15 @@ int sqoc_set_norm_bounds(sqoc_problem* p, const double* bounds);
 
 /* Large-block schedule: -1 auto (default), 0 slice-sequential (no history; memory
  * O(sum d_b^2)), 1 history (all slices resident, slice-batched GEMMs; memory
- * O(N sum d_b^2)).  sqoc_last_schedule reports what the last sqoc_eval used
- * (-1 when the problem has no large blocks). */
+ * O(N sum d_b^2)), 2 state-vector (state objective only: U_j history, psi/chi
+ * sweeps and an augmented Taylor action for the gradient; memory O(N sum d_b^2)).
+ * sqoc_last_schedule reports what the last sqoc_eval used (-1 = no large blocks). */
 int sqoc_set_schedule(sqoc_problem* p, int schedule);
 int sqoc_last_schedule(const sqoc_problem* p);
+
+/* Propagator plan of the last large-block evaluation: Taylor degree 3*taylor_blocks,
+ * `squarings` squarings, and the number of augmented-action terms (state-vector). */
+int sqoc_last_plan(const sqoc_problem* p, int* taylor_blocks, int* squarings, int* action_terms);
 
 /* Free all device memory of the problem. */
 int sqoc_destroy(sqoc_problem* p);

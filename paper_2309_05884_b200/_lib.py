@@ -39,6 +39,7 @@ SIGNATURES = {
     "sqoc_set_timing": (_I, [_P, _I]),
     "sqoc_set_schedule": (_I, [_P, _I]),
     "sqoc_last_schedule": (_I, [_P]),
+    "sqoc_last_plan": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "sqoc_set_norm_bounds": (_I, [_P, _D]),
     "sqoc_block_time_ms": (_I, [_P, _I, _D]),
     "sqoc_tiny_max_dim": (_I, []),

@@ -428,12 +428,20 @@ int sqoc_set_norm_bounds(sqoc_problem* p, const double* bounds) {
 }
 
 int sqoc_set_schedule(sqoc_problem* p, int schedule) {
-  if (!p || schedule < -1 || schedule > 1) return fail(SQOC_ERR_ARG, "schedule must be -1 (auto), 0 or 1");
+  if (!p || schedule < -1 || schedule > 2) return fail(SQOC_ERR_ARG, "schedule must be -1 (auto), 0, 1 or 2");
   if (p->large) p->large->force_mode = schedule;
   return SQOC_OK;
 }
 
 int sqoc_last_schedule(const sqoc_problem* p) { return (p && p->large) ? p->large->mode : -1; }
+
+int sqoc_last_plan(const sqoc_problem* p, int* taylor_blocks, int* squarings, int* action_terms) {
+  if (!p || !taylor_blocks || !squarings || !action_terms) return fail(SQOC_ERR_ARG, "NULL argument");
+  *taylor_blocks = p->large ? p->large->last_nb : 0;
+  *squarings = p->large ? p->large->last_s : 0;
+  *action_terms = p->large ? p->large->last_taylor_terms : 0;
+  return SQOC_OK;
+}
 
 int sqoc_set_timing(sqoc_problem* p, int on) {
   if (!p) return fail(SQOC_ERR_ARG, "problem is NULL");

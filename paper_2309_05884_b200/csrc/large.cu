@@ -230,6 +230,99 @@ __global__ void transpose_kernel(const double2* __restrict__ in, double2* __rest
   }
 }
 
+// Augmented Taylor action, one term for every (block, slice): rows of V are y_i, x_1,i, .., x_K,i.
+// W_k = V a_k^T (row r of W_k = a_k v_r).  New terms:
+//   y_i   <- (W_0[y_i] + sum_k u_k,i W_k[y_i]) / l
+//   x_k,i <- (W_0[x_k,i] + sum_k' u_k',i W_k'[x_k,i] + W_k[y_i]) / l ;  acc_k,i += x_k,i
+__global__ void sv_combine_kernel(int l, int K, int N, const double* __restrict__ u, const int* __restrict__ dims,
+                                  const size_t* __restrict__ offr, double2* __restrict__ V,
+                                  const double2* __restrict__ W, size_t wstride, double2* __restrict__ acc) {
+  const int b = blockIdx.y;
+  const int d = dims[b];
+  const size_t vb = (size_t)(K + 1) * N * offr[b];
+  const size_t ab = (size_t)K * N * offr[b];
+  const size_t n = (size_t)N * d;
+  const double inv_l = 1.0 / l;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = e / d;
+    const size_t c = e % d;
+    double uk[4];
+    for (int k = 0; k < 4; ++k) uk[k] = k < K ? u[k * N + i] : 0.0;
+    const size_t ry = vb + (size_t)i * d + c;  // y row
+    double2 wy[5];
+    for (int k = 0; k <= K; ++k) wy[k] = W[k * wstride + ry];
+    double2 ny = wy[0];
+    for (int k = 0; k < K; ++k) { ny.x += uk[k] * wy[k + 1].x; ny.y += uk[k] * wy[k + 1].y; }
+    for (int k = 0; k < K; ++k) {
+      const size_t rx = vb + ((size_t)(k + 1) * N + i) * d + c;
+      double2 nx = W[rx];
+      for (int q = 0; q < K; ++q) {
+        const double2 w = W[(q + 1) * wstride + rx];
+        nx.x += uk[q] * w.x;
+        nx.y += uk[q] * w.y;
+      }
+      nx.x = (nx.x + wy[k + 1].x) * inv_l;
+      nx.y = (nx.y + wy[k + 1].y) * inv_l;
+      V[rx] = nx;
+      double2* ac = acc + ab + ((size_t)k * N + i) * d + c;
+      ac->x += nx.x;
+      ac->y += nx.y;
+    }
+    V[ry] = make_double2(ny.x * inv_l, ny.y * inv_l);
+  }
+}
+
+// V: y_i = psi_i, x_k,i = 0;  acc = 0
+__global__ void sv_init_kernel(int K, int N, const int* __restrict__ dims, const size_t* __restrict__ offr,
+                               size_t totalr, const double2* __restrict__ psi, double2* __restrict__ V,
+                               double2* __restrict__ acc) {
+  const int b = blockIdx.y;
+  const int d = dims[b];
+  const size_t vb = (size_t)(K + 1) * N * offr[b];
+  const size_t ab = (size_t)K * N * offr[b];
+  const size_t n = (size_t)N * d;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = e / d;
+    const size_t c = e % d;
+    V[vb + e] = psi[(size_t)i * totalr + offr[b] + c];
+    for (int k = 0; k < K; ++k) {
+      V[vb + ((size_t)(k + 1) * N) * d + e] = make_double2(0.0, 0.0);
+      acc[ab + (size_t)k * N * d + e] = make_double2(0.0, 0.0);
+    }
+  }
+}
+
+// g[i][b][k] = <chi_{i+1}, acc_k,i>   (one CTA per (block, slice))
+__global__ void sv_dot_kernel(int K, int N, int nblk, const int* __restrict__ dims, const size_t* __restrict__ offr,
+                              size_t totalr, const double2* __restrict__ chi, const double2* __restrict__ acc,
+                              double2* __restrict__ g) {
+  __shared__ double2 red[4][256];
+  const int b = blockIdx.x, i = blockIdx.y;
+  const int d = dims[b];
+  const size_t ab = (size_t)K * N * offr[b];
+  const double2* c = chi + (size_t)(i + 1) * totalr + offr[b];
+  double sx[4] = {0, 0, 0, 0}, sy[4] = {0, 0, 0, 0};
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    const double2 cv = c[e];
+    for (int k = 0; k < K; ++k) {
+      const double2 a = acc[ab + ((size_t)k * N + i) * d + e];
+      sx[k] += cv.x * a.x + cv.y * a.y;
+      sy[k] += cv.x * a.y - cv.y * a.x;
+    }
+  }
+  for (int k = 0; k < K; ++k) red[k][threadIdx.x] = make_double2(sx[k], sy[k]);
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+      for (int k = 0; k < K; ++k) {
+        red[k][threadIdx.x].x += red[k][threadIdx.x + st].x;
+        red[k][threadIdx.x].y += red[k][threadIdx.x + st].y;
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < K) g[((size_t)i * nblk + b) * K + threadIdx.x] = red[threadIdx.x][0];
+}
+
 // ------------------------------------------------------------------ host side
 template <int TA, int TB, int EPI>
 static cudaError_t launch_gemm(const GemmItem* items, int n, int tiles, GemmArgs a, cudaStream_t st) {
@@ -411,6 +504,20 @@ int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, 
   LCHK(cudaMemcpy(g.w_dev, w.data(), g.nblk * sizeof(double), cudaMemcpyHostToDevice));
   LCHK(cudaMalloc(&g.gidx_dev, g.nblk * sizeof(int)));
   LCHK(cudaMemcpy(g.gidx_dev, gidx.data(), g.nblk * sizeof(int), cudaMemcpyHostToDevice));
+  {  // a_k^T for k = 0..K per block (state-vector schedule: W_k = V a_k^T)
+    std::vector<const double2*> gt;
+    for (int b = 0; b < g.nblk; ++b) {
+      const int d = blocks[b].d;
+      double2* t = nullptr;
+      LCHK(cudaMalloc(&t, (size_t)(K + 1) * d * d * sizeof(double2)));
+      transpose_kernel<<<dim3((d + 31) / 32, (d + 31) / 32, K + 1), dim3(32, 8)>>>(blocks[b].gen, t, d);
+      LCHK(cudaGetLastError());
+      g.gentall_mem.push_back(t);
+      gt.push_back(t);
+    }
+    LCHK(cudaMalloc(&g.gentall_dev, g.nblk * sizeof(double2*)));
+    LCHK(cudaMemcpy(g.gentall_dev, gt.data(), g.nblk * sizeof(double2*), cudaMemcpyHostToDevice));
+  }
   {  // a_k^T per block for the history-mode slice traces
     std::vector<const double2*> gt;
     for (int b = 0; b < g.nblk; ++b) {
@@ -460,6 +567,11 @@ void large_free(LargeGroup& g) {
   for (auto x : hb) cudaFree(x);
   for (auto m : g.gent_mem) cudaFree(m);
   g.gent_mem.clear();
+  for (auto m : g.gentall_mem) cudaFree(m);
+  g.gentall_mem.clear();
+  cudaFree(g.gentall_dev);
+  double2* sv[] = {g.sv_U, g.sv_chunk, g.sv_psi, g.sv_chi, g.sv_V, g.sv_W, g.sv_acc, g.sv_g};
+  for (auto x : sv) cudaFree(x);
   cudaFree(g.gent_dev);
   for (auto m : g.hlist_mem) cudaFree(m);
   g.hlist_mem.clear();
@@ -655,6 +767,194 @@ static int large_eval_history(LargeGroup& g, const LargeArgs& a, int s_idx, cons
   return SQOC_OK;
 }
 
+// ------------------------------------------------------------------ state-vector schedule
+enum SOp { SV_A2, SV_A3, SV_H, SV_S, SV_PSI, SV_CHI, SV_W };
+
+static size_t sv_fixed_bytes(const LargeGroup& g) {
+  const size_t N = g.N, K = g.K;
+  return sizeof(double2) * (N * g.total + 2 * (N + 1) * g.totalr + (K + 1) * N * g.totalr * (K + 2) +
+                            K * N * g.totalr + N * g.nblk * K);
+}
+
+static int sv_alloc(LargeGroup& g) {
+  if (g.sv_U) return SQOC_OK;
+  const size_t N = g.N, K = g.K;
+  LCHK(cudaMalloc(&g.sv_U, N * g.total * sizeof(double2)));
+  LCHK(cudaMalloc(&g.sv_psi, (N + 1) * g.totalr * sizeof(double2)));
+  LCHK(cudaMalloc(&g.sv_chi, (N + 1) * g.totalr * sizeof(double2)));
+  LCHK(cudaMalloc(&g.sv_V, (K + 1) * N * g.totalr * sizeof(double2)));
+  LCHK(cudaMalloc(&g.sv_W, (K + 1) * (K + 1) * N * g.totalr * sizeof(double2)));
+  LCHK(cudaMalloc(&g.sv_acc, K * N * g.totalr * sizeof(double2)));
+  LCHK(cudaMalloc(&g.sv_g, N * g.nblk * K * sizeof(double2)));
+  size_t free_b = 0, total_b = 0;
+  LCHK(cudaMemGetInfo(&free_b, &total_b));
+  const size_t per_slice = 5 * g.total * sizeof(double2);
+  g.sv_S = (int)std::max<size_t>(1, std::min<size_t>(N, (size_t)(0.5 * (double)free_b) / per_slice));
+  g.sv_S = std::min(g.sv_S, 64);
+  LCHK(cudaMalloc(&g.sv_chunk, (size_t)g.sv_S * per_slice));
+  return SQOC_OK;
+}
+
+static ListRef sv_list(LargeGroup& g, int op, int idx, int p, int i0, int i1) {
+  auto key = std::make_tuple(2000000000 + op * 1000000 + idx * 4 + p, g.last_nb * 100 + g.last_s, i0, i1);
+  auto it = g.hlists.find(key);
+  if (it != g.hlists.end()) return it->second;
+  std::vector<GemmItem> v;
+  const size_t S = g.sv_S, sl = g.total;
+  auto cb = [&](int c, int z, int b) { return g.sv_chunk + ((size_t)c * S + z) * sl + g.off[b]; };
+  if (op == SV_W) {
+    for (int b = 0; b < g.nblk; ++b) {
+      const int d = g.blocks[b].d;
+      const size_t rows = (size_t)(g.K + 1) * g.N;
+      const double2* Vb = g.sv_V + rows * g.offr[b];
+      double2* Wb = g.sv_W + (size_t)idx * rows * g.totalr + rows * g.offr[b];
+      const double2* Bt = static_cast<const double2*>(g.gentall_mem[b]);
+      v.push_back(mk(Vb, Bt + (size_t)idx * d * d, 0, 0, Wb, 0, 0, (int)rows, d, d, 1, d, d, d, 0));
+    }
+  } else {
+    for (int z = i0; z < i1; ++z)
+      for (int b = 0; b < g.nblk; ++b) {
+        const int d = g.blocks[b].d;
+        double2 *A = cb(0, z, b), *A2 = cb(1, z, b), *A3 = cb(2, z, b), *Tp = cb(3 + p, z, b), *Tn = cb(4 - p, z, b);
+        double2* U = g.sv_U + (size_t)z * sl + g.off[b];
+        double2* Pi = g.sv_psi + (size_t)z * g.totalr + g.offr[b];
+        double2* Pn = g.sv_psi + (size_t)(z + 1) * g.totalr + g.offr[b];
+        double2* Ci = g.sv_chi + (size_t)z * g.totalr + g.offr[b];
+        double2* Cn = g.sv_chi + (size_t)(z + 1) * g.totalr + g.offr[b];
+        switch (op) {
+          case SV_A2: v.push_back(mk(A, A, 0, 0, A2, 0, 0, d, d, d, 1, d, d, d, 0)); break;
+          case SV_A3: v.push_back(mk(A2, A, 0, 0, A3, 0, 0, d, d, d, 1, d, d, d, 0)); break;
+          case SV_H: v.push_back(mk(Tp, A3, 0, 0, Tn, A, A2, d, d, d, 1, d, d, d, 1)); break;
+          case SV_S: v.push_back(mk(Tp, Tp, 0, 0, Tn, 0, 0, d, d, d, 1, d, d, d, 0)); break;
+          case SV_PSI: v.push_back(mk(U, Pi, 0, 0, Pn, 0, 0, d, 1, d, 1, d, 1, 1, 0)); break;
+          case SV_CHI: v.push_back(mk(U, Cn, 0, 0, Ci, 0, 0, d, 1, d, 1, d, 1, 1, 0)); break;
+        }
+      }
+  }
+  int t = 0;
+  for (auto& x : v) {
+    x.tile_start = t;
+    t += tiles_of(x.m, x.n);
+  }
+  ListRef ref;
+  if (cudaMalloc(&ref.dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return ListRef{};
+  cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
+  ref.n = (int)v.size();
+  ref.tiles = t;
+  g.hlist_mem.push_back(ref.dev);
+  g.hlists[key] = ref;
+  return ref;
+}
+
+static int svgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArgs a, cudaStream_t st) {
+  ListRef l = sv_list(g, op, idx, p, i0, i1);
+  if (!l.dev) {
+    g.err = "state-vector work list allocation failed";
+    return SQOC_ERR_CUDA;
+  }
+  cudaError_t e = (op == SV_CHI) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st)
+                                 : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
+  if (e != cudaSuccess) {
+    g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
+    return SQOC_ERR_CUDA;
+  }
+  g.launches++;
+  return SQOC_OK;
+}
+
+// Number of Taylor terms m with beta^(m+1)/(m+1)! / (1 - beta/(m+2)) <= 1e-17.
+static int taylor_terms(double beta) {
+  double term = 1.0;
+  for (int m = 1; m < 200; ++m) {
+    term *= beta / m;  // beta^m / m!
+    const double next = term * beta / (m + 1);
+    if (beta < m + 2 && next / (1.0 - beta / (m + 2)) <= 1e-17) return m;
+  }
+  return 200;
+}
+
+static int large_eval_state_vector(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, int nb, int sq,
+                                   double bound, cudaStream_t st) {
+  const int K = g.K, N = g.N, nblk = g.nblk;
+  int maxd = 0;
+  for (auto& b : g.blocks) maxd = std::max(maxd, b.d);
+  const unsigned ew_x = (unsigned)std::max<size_t>(1, std::min<size_t>(((size_t)maxd * maxd + 255) / 256, 256));
+  const double scale = std::ldexp(1.0, -sq);
+  const double cm = inv_fact(3 * nb);
+  const size_t S = g.sv_S, sl = g.total;
+  GemmArgs one{1.0, 0.0, 0.0, 0.0};
+  int rc;
+  // ---- propagators U_i, chunk by chunk, kept for both vector sweeps ----
+  for (int i0 = 0; i0 < N; i0 += (int)S) {
+    const int n_here = std::min<int>((int)S, N - i0);
+    const dim3 grid(ew_x, nblk, n_here);
+    build_a_kernel<<<grid, 256, 0, st>>>(i0, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.sv_chunk, sl);
+    LCHK(cudaGetLastError());
+    g.launches++;
+    if ((rc = svgemm(g, SV_A2, 0, 0, 0, n_here, one, st))) return rc;
+    if ((rc = svgemm(g, SV_A3, 0, 0, 0, n_here, one, st))) return rc;
+    const int q0 = nb - 1;
+    horner_init_kernel<<<grid, 256, 0, st>>>(0, g.d_dev, g.off_dev, cm, inv_fact(3 * q0), inv_fact(3 * q0 + 1),
+                                             inv_fact(3 * q0 + 2), g.sv_chunk, g.sv_chunk + S * sl,
+                                             g.sv_chunk + 2 * S * sl, nullptr, nullptr, nullptr,
+                                             g.sv_chunk + 3 * S * sl, nullptr, sl);
+    LCHK(cudaGetLastError());
+    g.launches++;
+    int p = 0;
+    for (int t = nb - 2; t >= 0; --t) {
+      if ((rc = svgemm(g, SV_H, 0, p, 0, n_here, GemmArgs{1.0, inv_fact(3 * t + 1), inv_fact(3 * t + 2), inv_fact(3 * t)},
+                       st)))
+        return rc;
+      p ^= 1;
+    }
+    for (int i = 0; i < sq; ++i) {
+      if ((rc = svgemm(g, SV_S, 0, p, 0, n_here, one, st))) return rc;
+      p ^= 1;
+    }
+    LCHK(cudaMemcpyAsync(g.sv_U + (size_t)i0 * sl, g.sv_chunk + (size_t)(3 + p) * S * sl,
+                         (size_t)n_here * sl * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  }
+  // ---- psi / chi sweeps (sequential over slices, batched over blocks) ----
+  const dim3 ew_grid(ew_x, nblk);
+  init_xl_kernel<<<ew_grid, 256, 0, st>>>(0, 1, g.d_dev, g.offr_dev, g.x0_dev, g.tgt_dev, g.sv_psi,
+                                          g.sv_chi + (size_t)N * g.totalr);
+  LCHK(cudaGetLastError());
+  g.launches++;
+  for (int i = 0; i < N; ++i)
+    if ((rc = svgemm(g, SV_PSI, 0, 0, i, i + 1, one, st))) return rc;
+  tau_kernel<<<nblk, 256, 0, st>>>(0, 1, g.d_dev, g.offr_dev, g.sv_psi + (size_t)N * g.totalr, g.tgt_dev, g.tau_dev,
+                                   a.tau_out + (size_t)s_idx * a.tau_stride, g.gidx_dev);
+  LCHK(cudaGetLastError());
+  g.launches++;
+  for (int i = N - 1; i >= 0; --i)
+    if ((rc = svgemm(g, SV_CHI, 0, 0, i, i + 1, one, st))) return rc;
+  // ---- dtau/du_k,i = <chi_{i+1}| L(A_i, a_k) |psi_i> by the augmented Taylor action ----
+  double emax = 0.0;
+  for (auto& b : g.blocks)
+    for (int k = 1; k <= K; ++k) emax = std::max(emax, b.gen_norm[k]);
+  const int m = taylor_terms(bound + emax);
+  g.last_taylor_terms = m;
+  const dim3 vgrid((unsigned)std::min<size_t>(((size_t)N * maxd + 255) / 256, 4096), nblk);
+  sv_init_kernel<<<vgrid, 256, 0, st>>>(K, N, g.d_dev, g.offr_dev, g.totalr, g.sv_psi, g.sv_V, g.sv_acc);
+  LCHK(cudaGetLastError());
+  g.launches++;
+  const size_t wstride = (size_t)(K + 1) * N * g.totalr;
+  for (int l = 1; l <= m; ++l) {
+    for (int k = 0; k <= K; ++k)
+      if ((rc = svgemm(g, SV_W, k, 0, 0, 0, one, st))) return rc;
+    sv_combine_kernel<<<vgrid, 256, 0, st>>>(l, K, N, u, g.d_dev, g.offr_dev, g.sv_V, g.sv_W, wstride, g.sv_acc);
+    LCHK(cudaGetLastError());
+    g.launches++;
+  }
+  sv_dot_kernel<<<dim3(nblk, N), 256, 0, st>>>(K, N, nblk, g.d_dev, g.offr_dev, g.totalr, g.sv_chi, g.sv_acc, g.sv_g);
+  LCHK(cudaGetLastError());
+  hist_grad_kernel<<<256, 256, 0, st>>>(K, N, nblk, g.sv_g, g.tau_dev, g.w_dev, g.gidx_dev,
+                                        a.gradb + (size_t)s_idx * K * N, a.gradb_block_stride);
+  LCHK(cudaGetLastError());
+  g.launches += 2;
+  return SQOC_OK;
+}
+
 int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
   const int K = g.K, N = g.N, nblk = g.nblk;
   int maxd = 0;
@@ -675,6 +975,25 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
     g.launches++;
     int nb, sq;
     choose_taylor_host(bound, nb, sq);
+    g.last_nb = nb;
+    g.last_s = sq;
+    if (!g.gate && N > 0 && g.force_mode != 0 && g.force_mode != 1) {  // state-vector schedule
+      bool use_sv = g.force_mode == 2;
+      if (!use_sv) {
+        size_t free_b = 0, total_b = 0;
+        LCHK(cudaMemGetInfo(&free_b, &total_b));
+        const size_t have = g.sv_U ? sv_fixed_bytes(g) : 0;
+        use_sv = sv_fixed_bytes(g) + 5 * g.total * sizeof(double2) <= (size_t)(0.7 * (double)(free_b + have));
+      }
+      if (use_sv) {
+        int rc = sv_alloc(g);
+        if (rc != SQOC_OK) return rc;
+        g.mode = 2;
+        rc = large_eval_state_vector(g, a, s, u, nb, sq, bound, st);
+        if (rc != SQOC_OK) return rc;
+        continue;
+      }
+    }
     {  // history schedule when every slice's chain fits comfortably in free memory
       bool use_hist = g.force_mode == 1;
       if (g.force_mode == -1 && N > 0) {

@@ -89,8 +89,21 @@ struct LargeGroup {
   std::vector<void*> gent_mem;
   std::map<std::tuple<int, int, int, int>, ListRef> hlists;
   std::vector<void*> hlist_mem;
-  int mode = -1;                    // last schedule used: 0 sequential, 1 history
-  int force_mode = -1;              // -1 auto, 0 sequential, 1 history
+  // ---- state-vector schedule (state objective): U_j history, vector sweeps, augmented Taylor action ----
+  double2* sv_U = nullptr;          // [N][total]
+  double2* sv_chunk = nullptr;      // [5][S][total]: A, A2, A3, T0, T1
+  int sv_S = 0;
+  double2* sv_psi = nullptr;        // [N+1][totalr]
+  double2* sv_chi = nullptr;        // [N+1][totalr]
+  double2* sv_V = nullptr;          // per block b: [(K+1) N][d_b] rows y_i, x_1,i .. x_K,i
+  double2* sv_W = nullptr;          // [K+1] x same shape as sv_V
+  double2* sv_acc = nullptr;        // per block: [K N][d_b]
+  double2* sv_g = nullptr;          // [N][nblk][K]
+  const double2** gentall_dev = nullptr;  // per block a_k^T for k = 0..K
+  std::vector<void*> gentall_mem;
+  int last_nb = 0, last_s = 0, last_taylor_terms = 0;
+  int mode = -1;                    // last schedule used: 0 sequential, 1 history, 2 state-vector
+  int force_mode = -1;              // -1 auto, 0 sequential, 1 history, 2 state-vector
   int launches = 0;
   std::string err;
 };

@@ -107,7 +107,7 @@ class GrapeEngine:
         tiny_max = self.lib.sqoc_tiny_max_dim()
         return [b for b, d in enumerate(self.dims) if d > tiny_max]
 
-    SCHEDULES = {"auto": -1, "sequential": 0, "history": 1}
+    SCHEDULES = {"auto": -1, "sequential": 0, "history": 1, "state-vector": 2}
 
     def set_schedule(self, name: str) -> None:
         """Large-block schedule: 'auto', 'sequential' (O(sum d^2) memory) or 'history' (slice-batched)."""
@@ -115,7 +115,14 @@ class GrapeEngine:
 
     @property
     def last_schedule(self) -> str:
-        return {-1: "none", 0: "sequential", 1: "history"}[self.lib.sqoc_last_schedule(self.handle)]
+        return {-1: "none", 0: "sequential", 1: "history", 2: "state-vector"}[self.lib.sqoc_last_schedule(self.handle)]
+
+    @property
+    def last_plan(self) -> dict:
+        nb, s, m = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _lib.check(self.lib.sqoc_last_plan(self.handle, ctypes.byref(nb), ctypes.byref(s), ctypes.byref(m)),
+                   "sqoc_last_plan")
+        return {"taylor_degree": 3 * nb.value, "squarings": s.value, "action_terms": m.value}
 
     def set_timing(self, on: bool) -> None:
         _lib.check(self.lib.sqoc_set_timing(self.handle, 1 if on else 0), "sqoc_set_timing")

@@ -76,13 +76,14 @@ def test_cfg2_full_grid_fidelity_and_fd_gradient():
         assert abs(fd - g[k, j]) / max(abs(fd), abs(g[k, j]), rms) < 1e-6
 
 
-@pytest.mark.parametrize("schedule", SCHEDULES)
+@pytest.mark.parametrize("schedule", SCHEDULES + ["state-vector"])
 def test_state_transfer_full_space_d64_against_oracle(schedule):
     s = systems.state_transfer_ring(6, 10.0, 40, seed=3, full=True)  # 64 x 64 dense
     eng = GrapeEngine(s, max_batch=1)
     eng.set_schedule(schedule)
     u = s.controls(1)
     F, g = eng.objective(u)
+    assert eng.last_schedule == schedule
     Fo, go, _ = O.objective(s, u)
     assert abs(F - Fo) <= F_TOL
     assert rel(g, go) <= G_TOL
@@ -95,9 +96,23 @@ def test_symmetric_equals_conventional_state_transfer():
     u = full.controls(2)
     ef = GrapeEngine(full, max_batch=1)
     Ff, gf = ef.objective(u)
+    assert ef.last_schedule == "state-vector"
     Fb, gb = GrapeEngine(blk, max_batch=1).objective(u)
     assert abs(Ff - Fb) <= F_TOL
     assert rel(gf, gb) <= G_TOL
     Fo, go, _ = O.objective(blk, u)
     assert abs(Fb - Fo) <= F_TOL
     assert rel(gb, go) <= G_TOL
+
+
+def test_cfg4_short_grid_schedules_agree():
+    """Unsymmetrised 4096-dim state transfer (cfg 4 system, 3 slices): state-vector vs dense pair chain."""
+    s = systems.config(4, n_slices=3)
+    eng = GrapeEngine(s, max_batch=1)
+    u = s.controls(0)
+    F1, g1 = eng.objective(u)
+    assert eng.last_schedule == "state-vector"
+    eng.set_schedule("sequential")
+    F2, g2 = eng.objective(u)
+    assert abs(F1 - F2) <= F_TOL
+    assert rel(g1, g2) <= G_TOL

@@ -25,4 +25,5 @@ for _ in range(reps):
 ms = min(ts)
 fl = s.flops_per_eval() * batch
 print(f"cfg{cfg} batch={batch} dims={[b.dim for b in s.blocks]}: {ms:.3f} ms/eval-batch, {batch/ms*1e3:.1f} evals/s, "
-      f"{fl/ms/1e9:.2f} TFLOP/s (G-convention), launches={eng.last_launches}, F[0]={F[0].item():.6f}")
+      f"{fl/ms/1e9:.2f} TFLOP/s (G-convention), launches={eng.last_launches}, F[0]={F[0].item():.6f}, "
+      f"schedule={eng.last_schedule}, plan={eng.last_plan}")
