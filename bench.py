@@ -98,7 +98,8 @@ def build_system(cfg: int):
 
 # ---------------------------------------------------------------- CPU reference (oracle port)
 def _cpu_seed_eval(args):
-    cfg, seed, n_blocks_subset, slices = args
+    cfg, seed, n_blocks_subset, slices = args[:4]
+    threads = args[4] if len(args) > 4 else 1
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from threadpoolctl import threadpool_limits
 
@@ -106,7 +107,7 @@ def _cpu_seed_eval(args):
 
     s = build_system_cached(cfg)
     u = s.controls(seed)
-    with threadpool_limits(1):
+    with threadpool_limits(threads):
         if slices is not None:  # sampled slices (per-slice cost is input independent), scaled by the caller
             s2 = _truncate(s, slices)
             grape_oracle.objective(s2, u[:, :slices], blocks=n_blocks_subset)
@@ -146,14 +147,15 @@ def cpu_reference(cfg: int, seconds_budget: float = 12.0, cores: int | None = No
     cores = cores or len(os.sched_getaffinity(0))
     s = build_system_cached(cfg)
     if cfg in (2, 3, 4):
-        slices = {2: 10, 3: 2, 4: 2}[cfg]
+        # sampled slices, all cores to the BLAS/LAPACK of one process (cfg 3/4 eigh of 1161..4096)
+        slices, threads = {2: (10, 1), 3: (1, cores), 4: (1, cores)}[cfg]
         t0 = time.perf_counter()
-        _cpu_seed_eval((cfg, 0, None, slices))
+        _cpu_seed_eval((cfg, 0, None, slices, threads))
         wall = time.perf_counter() - t0
         evals_per_s = (slices / s.n_slices) / wall
         sample = (f"1 evaluation of {CONFIG_NAMES[cfg]} with {slices} of {s.n_slices} slices timed and scaled, "
-                  f"1 process x 1 BLAS thread, {wall:.1f} s")
-        return evals_per_s, 1, sample
+                  f"1 process x {threads} BLAS thread(s), {wall:.1f} s")
+        return evals_per_s, threads, sample
     ctx = mp.get_context("fork")
     n_done, rounds = 0, 0
     t0 = time.perf_counter()

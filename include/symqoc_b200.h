@@ -92,6 +92,21 @@ int sqoc_last_schedule(const sqoc_problem* p);
  * `squarings` squarings, and the number of augmented-action terms (state-vector). */
 int sqoc_last_plan(const sqoc_problem* p, int* taylor_blocks, int* squarings, int* action_terms);
 
+/* Slice-chunk sharding (multi-GPU scan carry).  A rank builds
+ * the problem for its own contiguous slice range [s, e) (n_slices = e - s, the same
+ * dt), then:
+ *   sqoc_chunk_product : out[b] (d_b x d_b) = U_{e-1} ... U_s for every block
+ *                        (gate-objective problem; batch 1);
+ *   sqoc_eval_chunk    : gradient of this rank's slices from the full-grid boundary
+ *                        values: x_start[b] = X before slice s (gate d x d, state d),
+ *                        lam_end[b] = Lambda after slice e-1 ((U_{N-1}..U_e)^dag V),
+ *                        tau[b] = full-grid tau_b (2 doubles each); F = sum_b w_b |tau_b|^2,
+ *                        grad [K][e - s].
+ * Both need every block to be large (d > 16); tiny blocks shard by batch instead. */
+int sqoc_chunk_product(sqoc_problem* p, const double* u, double* const* out, int memory, void* stream);
+int sqoc_eval_chunk(sqoc_problem* p, const double* u, const double* const* x_start, const double* const* lam_end,
+                    const double* tau, double* F, double* grad, int memory, void* stream);
+
 /* Free all device memory of the problem. */
 int sqoc_destroy(sqoc_problem* p);
 

@@ -103,13 +103,16 @@ def state_dtau(psi0, psi_f, u, h0, hk, tau):
     return overlap, dtau
 
 
-def gate_dtau(target, u, h0, hk, tau):
-    """(tau = Tr(V^dag X_N), d tau / d u (K, N) complex) for one block (gap G2)."""
+def gate_dtau(target, u, h0, hk, tau, x0=None, lam_end=None):
+    """(tau = Tr(V^dag X_N), d tau / d u (K, N) complex) for one block (gap G2).
+
+    ``x0`` / ``lam_end`` override X_0 = I and Lam_N = V (slice-chunk boundaries).
+    """
     u = np.asarray(u, dtype=np.float64)
     n_steps = u.shape[1]
     d = h0.shape[0]
     xs = np.empty((n_steps + 1, d, d), dtype=np.complex128)
-    xs[0] = np.eye(d)
+    xs[0] = np.eye(d) if x0 is None else x0
     eig = []
     for j in range(n_steps):
         uj, (w, v) = expm_hermitian(hamiltonian(h0, hk, u[:, j]), tau)
@@ -117,7 +120,7 @@ def gate_dtau(target, u, h0, hk, tau):
         xs[j + 1] = uj @ xs[j]
     tr = np.vdot(target, xs[-1])  # Tr(V^dag X_N) = sum conj(V) * X_N
     dtau = np.zeros(u.shape, dtype=np.complex128)
-    lam = np.array(target, dtype=np.complex128)
+    lam = np.array(target if lam_end is None else lam_end, dtype=np.complex128)
     for j in range(n_steps - 1, -1, -1):
         w, v, uj = eig[j]
         g = frechet_weights(w, tau)
@@ -153,3 +156,32 @@ def objective(system, u, blocks=None):
         f_total += per_block[b]
         grad += 2.0 * w[b] * np.real(np.conj(tr) * dtau)
     return f_total, grad, per_block
+
+
+class OracleChunkEngine:
+    """CPU stand-in for GrapeEngine's slice-chunk interface (tests of parallel.py)."""
+
+    def __init__(self, system):
+        self.system = system
+
+    def chunk_product(self, u):
+        out = []
+        for blk in self.system.blocks:
+            x = np.eye(blk.dim, dtype=np.complex128)
+            for j in range(u.shape[1]):
+                uj, _ = expm_hermitian(hamiltonian(blk.h0, blk.hk, u[:, j]), self.system.dt)
+                x = uj @ x
+            out.append(x)
+        return out
+
+    def eval_chunk(self, u, x_start, lam_end, tau):
+        w = self.system.block_weights()
+        F = float(np.sum(w * np.abs(tau) ** 2))
+        grad = np.zeros(np.shape(u))
+        for b, blk in enumerate(self.system.blocks):
+            if self.system.objective == "gate":
+                _, dt = gate_dtau(lam_end[b], u, blk.h0, blk.hk, self.system.dt, x0=x_start[b], lam_end=lam_end[b])
+            else:
+                _, dt = state_dtau(x_start[b], lam_end[b], u, blk.h0, blk.hk, self.system.dt)
+            grad += 2.0 * w[b] * np.real(np.conj(tau[b]) * dt)
+        return F, grad

@@ -41,6 +41,8 @@ SIGNATURES = {
     "sqoc_last_schedule": (_I, [_P]),
     "sqoc_last_plan": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "sqoc_set_norm_bounds": (_I, [_P, _D]),
+    "sqoc_chunk_product": (_I, [_P, _P, _P, _I, _P]),
+    "sqoc_eval_chunk": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _P]),
     "sqoc_block_time_ms": (_I, [_P, _I, _D]),
     "sqoc_tiny_max_dim": (_I, []),
     "sqoc_last_error": (ctypes.c_char_p, []),

@@ -128,7 +128,7 @@ static int launch_tiny(int d, const TinyParams& tp, int grid, int nwarps, size_t
 }
 
 static int choose_nwarps(int d, int K, int batch) {
-  const int pg = 32 / d;
+  const int pg = 32 / kTinyLanes;
   const int need = (batch + pg - 1) / pg;
   int nw = 8;
   while (nw > 1 && tiny_smem_bytes(d, K, nw) > kMaxSmem) --nw;
@@ -250,7 +250,7 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
     chk(cudaEventCreate(&bp.t1), "event");
     if (bp.tiny) {
       const int R = objective == SQOC_OBJ_GATE ? d : 1;
-      const int pg = 32 / d;
+      const int pg = 32 / kTinyLanes;
       bp.nwarps = choose_nwarps(d, n_controls, max_batch);
       const int per_cta = pg * bp.nwarps;
       bp.park_slots = (size_t)((max_batch + per_cta - 1) / per_cta) * per_cta;
@@ -356,7 +356,7 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
       tp.tau_stride = p->nblocks;
       tp.grad_out = gout;
       tp.park = bp.park;
-      const int pg = 32 / bp.d;
+      const int pg = 32 / kTinyLanes;
       int nw = std::max(1, std::min(bp.nwarps, (batch + pg - 1) / pg));
       tp.nwarps = nw;
       const int grid = (batch + pg * nw - 1) / (pg * nw);
@@ -410,6 +410,117 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
   SQOC_CUDA(cudaStreamSynchronize(st));
   if (flag) return fail(SQOC_ERR_NONFINITE, "objective or gradient became non-finite");
   return SQOC_OK;
+}
+
+// ---------------------------------------------------------------- slice-chunk sharding
+static int bc_stage(sqoc_problem* p, const double* const* src, int memory, double2** dev_bufs,
+                    std::vector<double2*>& keep, cudaStream_t st) {
+  // copy per-block d x R boundary matrices to device scratch; fill dev_bufs[b]
+  const bool gate = p->objective == SQOC_OBJ_GATE;
+  for (int b = 0; b < p->nblocks; ++b) {
+    const size_t n = (size_t)p->blocks[b].d * (gate ? p->blocks[b].d : 1);
+    double2* d = nullptr;
+    SQOC_CUDA(cudaMalloc(&d, n * sizeof(double2)));
+    keep.push_back(d);
+    SQOC_CUDA(cudaMemcpyAsync(d, src[b], n * sizeof(double2),
+                              memory == SQOC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    dev_bufs[b] = d;
+  }
+  return SQOC_OK;
+}
+
+static int chunk_checks(sqoc_problem* p) {
+  if (!p) return fail(SQOC_ERR_ARG, "problem is NULL");
+  if (!p->large) return fail(SQOC_ERR_UNSUPPORTED, "slice-chunk sharding needs large blocks (d > 16)");
+  for (auto& b : p->blocks)
+    if (b.tiny) return fail(SQOC_ERR_UNSUPPORTED, "slice-chunk sharding is not built for tiny blocks (use seed-DP)");
+  return SQOC_OK;
+}
+
+int sqoc_chunk_product(sqoc_problem* p, const double* u, double* const* out, int memory, void* stream) {
+  int rc = chunk_checks(p);
+  if (rc != SQOC_OK) return rc;
+  if (p->objective != SQOC_OBJ_GATE) return fail(SQOC_ERR_ARG, "chunk products need a gate-objective problem");
+  if (!out) return fail(SQOC_ERR_ARG, "out is NULL");
+  SQOC_CUDA(cudaSetDevice(p->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t KN = (size_t)p->K * p->N;
+  const double* u_dev = u;
+  if (memory == SQOC_MEM_HOST) {
+    SQOC_CUDA(cudaMemcpyAsync(p->u_dev, u, KN * sizeof(double), cudaMemcpyHostToDevice, st));
+    u_dev = p->u_dev;
+  }
+  std::vector<double2*> tmp;
+  p->large->fwd_out.assign(p->nblocks, nullptr);
+  for (int b = 0; b < p->nblocks; ++b) {
+    const size_t n = (size_t)p->blocks[b].d * p->blocks[b].d;
+    if (memory == SQOC_MEM_HOST) {
+      double2* d = nullptr;
+      SQOC_CUDA(cudaMalloc(&d, n * sizeof(double2)));
+      tmp.push_back(d);
+      p->large->fwd_out[b] = d;
+    } else {
+      p->large->fwd_out[b] = reinterpret_cast<double2*>(out[b]);
+    }
+  }
+  LargeArgs la;
+  la.u = u_dev;
+  la.batch = 1;
+  la.tau_out = p->tau_dev;
+  la.tau_stride = p->nblocks;
+  la.gradb = p->gradb;
+  la.gradb_block_stride = (size_t)p->max_batch * KN;
+  rc = large_eval(*p->large, la, st);
+  p->large->fwd_out.clear();
+  if (rc != SQOC_OK) {
+    for (auto d : tmp) cudaFree(d);
+    return fail(rc, p->large->err);
+  }
+  p->launches = p->large->launches;
+  if (memory == SQOC_MEM_HOST)
+    for (int b = 0; b < p->nblocks; ++b) {
+      const size_t n = (size_t)p->blocks[b].d * p->blocks[b].d;
+      SQOC_CUDA(cudaMemcpyAsync(out[b], tmp[b], n * sizeof(double2), cudaMemcpyDeviceToHost, st));
+    }
+  SQOC_CUDA(cudaStreamSynchronize(st));
+  for (auto d : tmp) cudaFree(d);
+  return SQOC_OK;
+}
+
+int sqoc_eval_chunk(sqoc_problem* p, const double* u, const double* const* x_start, const double* const* lam_end,
+                    const double* tau, double* F, double* grad, int memory, void* stream) {
+  int rc = chunk_checks(p);
+  if (rc != SQOC_OK) return rc;
+  if (!x_start || !lam_end || !tau) return fail(SQOC_ERR_ARG, "boundary arrays are NULL");
+  SQOC_CUDA(cudaSetDevice(p->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<double2*> keep;
+  std::vector<double2*> xb(p->nblocks), lb(p->nblocks);
+  rc = bc_stage(p, x_start, memory, xb.data(), keep, st);
+  if (rc == SQOC_OK) rc = bc_stage(p, lam_end, memory, lb.data(), keep, st);
+  double2 *xptrs = nullptr, *lptrs = nullptr, *taud = nullptr;
+  if (rc == SQOC_OK) {
+    SQOC_CUDA(cudaMalloc(&xptrs, p->nblocks * sizeof(double2*)));
+    SQOC_CUDA(cudaMalloc(&lptrs, p->nblocks * sizeof(double2*)));
+    SQOC_CUDA(cudaMalloc(&taud, p->nblocks * sizeof(double2)));
+    SQOC_CUDA(cudaMemcpyAsync(xptrs, xb.data(), p->nblocks * sizeof(double2*), cudaMemcpyHostToDevice, st));
+    SQOC_CUDA(cudaMemcpyAsync(lptrs, lb.data(), p->nblocks * sizeof(double2*), cudaMemcpyHostToDevice, st));
+    SQOC_CUDA(cudaMemcpyAsync(taud, tau, p->nblocks * sizeof(double2),
+                              memory == SQOC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    SQOC_CUDA(cudaStreamSynchronize(st));
+    p->large->bc_x_dev = reinterpret_cast<const double2**>(xptrs);
+    p->large->bc_l_dev = reinterpret_cast<const double2**>(lptrs);
+    p->large->bc_tau = taud;
+    rc = sqoc_eval(p, u, 1, F, grad, nullptr, memory, stream);
+    p->large->bc_x_dev = nullptr;
+    p->large->bc_l_dev = nullptr;
+    p->large->bc_tau = nullptr;
+  }
+  cudaFree(xptrs);
+  cudaFree(lptrs);
+  cudaFree(taud);
+  for (auto d : keep) cudaFree(d);
+  return rc;
 }
 
 int sqoc_set_norm_bounds(sqoc_problem* p, const double* bounds) {

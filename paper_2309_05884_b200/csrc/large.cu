@@ -138,19 +138,28 @@ __global__ void hist_grad_kernel(int K, int N, int nblk, const double2* __restri
   }
 }
 
-// X = I (gate) or psi_0 (state);  L = V or psi_f
-__global__ void init_xl_kernel(int gate, int R, const int* __restrict__ dims, const size_t* __restrict__ offr,
-                               const double2* const* __restrict__ x0, const double2* const* __restrict__ tgt,
+// X = I (gate without X_start) or xsrc[b] (state psi_0, or a sharding boundary);  L = lsrc[b]
+__global__ void init_xl_kernel(int gate, int x_from_ptr, const int* __restrict__ dims, const size_t* __restrict__ offr,
+                               const double2* const* __restrict__ xsrc, const double2* const* __restrict__ lsrc,
                                double2* __restrict__ X, double2* __restrict__ L) {
   const int b = blockIdx.y;
   const int d = dims[b];
-  const int r = gate ? d : R;
+  const int r = gate ? d : 1;
   const size_t n = (size_t)d * r;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const size_t o = offr[b] + i;
-    if (gate) X[o] = make_double2((i / r == i % r) ? 1.0 : 0.0, 0.0);
-    else X[o] = x0[b][i];
-    L[o] = tgt[b][i];
+    if (x_from_ptr) X[o] = xsrc[b][i];
+    else X[o] = make_double2((i / r == i % r) ? 1.0 : 0.0, 0.0);
+    L[o] = lsrc[b][i];
+  }
+}
+
+__global__ void set_tau_kernel(int nblk, const double2* __restrict__ given, double2* __restrict__ tau_local,
+                               double2* __restrict__ tau_out, const int* __restrict__ gidx) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nblk) {
+    tau_local[b] = given[b];
+    tau_out[gidx[b]] = given[b];
   }
 }
 
@@ -582,6 +591,39 @@ void large_free(LargeGroup& g) {
   g.list_tiles.clear();
 }
 
+// ------------------------------------------------------------------ boundary conditions
+static int bc_init(LargeGroup& g, double2* X, double2* L, dim3 grid, cudaStream_t st) {
+  const bool xp = g.bc_x_dev != nullptr || !g.gate;
+  init_xl_kernel<<<grid, 256, 0, st>>>(g.gate, xp ? 1 : 0, g.d_dev, g.offr_dev,
+                                       g.bc_x_dev ? g.bc_x_dev : g.x0_dev, g.bc_l_dev ? g.bc_l_dev : g.tgt_dev, X, L);
+  LCHK(cudaGetLastError());
+  g.launches++;
+  return SQOC_OK;
+}
+
+// tau from X_N (or the given full-grid tau); forward-only calls copy X_N out and stop (*done)
+static int bc_tau(LargeGroup& g, const double2* XN, const LargeArgs& a, int s_idx, cudaStream_t st, bool* done) {
+  *done = false;
+  if (!g.fwd_out.empty()) {
+    for (int b = 0; b < g.nblk; ++b) {
+      const size_t n = (size_t)g.blocks[b].d * (g.gate ? g.blocks[b].d : 1);
+      LCHK(cudaMemcpyAsync(g.fwd_out[b], XN + g.offr[b], n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    }
+    *done = true;
+    return SQOC_OK;
+  }
+  if (g.bc_tau) {
+    set_tau_kernel<<<(g.nblk + 127) / 128, 128, 0, st>>>(g.nblk, g.bc_tau, g.tau_dev,
+                                                          a.tau_out + (size_t)s_idx * a.tau_stride, g.gidx_dev);
+  } else {
+    tau_kernel<<<g.nblk, 256, 0, st>>>(g.gate, 1, g.d_dev, g.offr_dev, XN, g.tgt_dev, g.tau_dev,
+                                       a.tau_out + (size_t)s_idx * a.tau_stride, g.gidx_dev);
+  }
+  LCHK(cudaGetLastError());
+  g.launches++;
+  return SQOC_OK;
+}
+
 // ------------------------------------------------------------------ history schedule
 enum HOp { H_A2, H_A3, H_H, H_S, H_X, H_L, H_B, H_DA2, H_DA3, H_DH, H_DS };
 
@@ -724,16 +766,12 @@ static int large_eval_history(LargeGroup& g, const LargeArgs& a, int s_idx, cons
     if ((rc = hgemm(g, H_S, i, 0, 0, N, one, st))) return rc;
   // ---- forward / backward recurrences (sequential over slices, batched over blocks) ----
   const dim3 ew_grid(ew_x, nblk);
-  init_xl_kernel<<<ew_grid, 256, 0, st>>>(g.gate, 1, g.d_dev, g.offr_dev, g.x0_dev, g.tgt_dev, g.h_X,
-                                          g.h_L + (size_t)N * g.totalr);
-  LCHK(cudaGetLastError());
-  g.launches++;
+  if ((rc = bc_init(g, g.h_X, g.h_L + (size_t)N * g.totalr, ew_grid, st))) return rc;
   for (int i = 0; i < N; ++i)
     if ((rc = hgemm(g, H_X, 0, 0, i, i + 1, one, st))) return rc;
-  tau_kernel<<<nblk, 256, 0, st>>>(g.gate, 1, g.d_dev, g.offr_dev, g.h_X + (size_t)N * g.totalr, g.tgt_dev, g.tau_dev,
-                                   a.tau_out + (size_t)s_idx * a.tau_stride, g.gidx_dev);
-  LCHK(cudaGetLastError());
-  g.launches++;
+  bool done = false;
+  if ((rc = bc_tau(g, g.h_X + (size_t)N * g.totalr, a, s_idx, st, &done))) return rc;
+  if (done) return SQOC_OK;
   for (int i = N - 1; i >= 0; --i)
     if ((rc = hgemm(g, H_L, 0, 0, i, i + 1, one, st))) return rc;
   // ---- Frechet derivatives of every slice: L_R(A_i, X_i Lam_{i+1}^dag), derivative-only chain ----
@@ -916,16 +954,12 @@ static int large_eval_state_vector(LargeGroup& g, const LargeArgs& a, int s_idx,
   }
   // ---- psi / chi sweeps (sequential over slices, batched over blocks) ----
   const dim3 ew_grid(ew_x, nblk);
-  init_xl_kernel<<<ew_grid, 256, 0, st>>>(0, 1, g.d_dev, g.offr_dev, g.x0_dev, g.tgt_dev, g.sv_psi,
-                                          g.sv_chi + (size_t)N * g.totalr);
-  LCHK(cudaGetLastError());
-  g.launches++;
+  if ((rc = bc_init(g, g.sv_psi, g.sv_chi + (size_t)N * g.totalr, ew_grid, st))) return rc;
   for (int i = 0; i < N; ++i)
     if ((rc = svgemm(g, SV_PSI, 0, 0, i, i + 1, one, st))) return rc;
-  tau_kernel<<<nblk, 256, 0, st>>>(0, 1, g.d_dev, g.offr_dev, g.sv_psi + (size_t)N * g.totalr, g.tgt_dev, g.tau_dev,
-                                   a.tau_out + (size_t)s_idx * a.tau_stride, g.gidx_dev);
-  LCHK(cudaGetLastError());
-  g.launches++;
+  bool done = false;
+  if ((rc = bc_tau(g, g.sv_psi + (size_t)N * g.totalr, a, s_idx, st, &done))) return rc;
+  if (done) return SQOC_OK;
   for (int i = N - 1; i >= 0; --i)
     if ((rc = svgemm(g, SV_CHI, 0, 0, i, i + 1, one, st))) return rc;
   // ---- dtau/du_k,i = <chi_{i+1}| L(A_i, a_k) |psi_i> by the augmented Taylor action ----
@@ -1015,9 +1049,10 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
     const double scale = std::ldexp(1.0, -sq);
     const double cm = inv_fact(3 * nb);
     // ---- forward sweep ----
-    init_xl_kernel<<<ew_grid, 256, 0, st>>>(g.gate, 1, g.d_dev, g.offr_dev, g.x0_dev, g.tgt_dev, g.X[0], g.L[0]);
-    LCHK(cudaGetLastError());
-    g.launches++;
+    {
+      int rc0 = bc_init(g, g.X[0], g.L[0], ew_grid, st);
+      if (rc0) return rc0;
+    }
     int q = 0, r = 0;
     GemmArgs one{1.0, 0.0, 0.0, 0.0};
     for (int j = 0; j < N; ++j) {
@@ -1046,10 +1081,12 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
       if ((rc = gemm(g, F_X, p, q, 0, one, st))) return rc;
       q ^= 1;
     }
-    tau_kernel<<<nblk, 256, 0, st>>>(g.gate, 1, g.d_dev, g.offr_dev, g.X[q], g.tgt_dev, g.tau_dev,
-                                     a.tau_out + (size_t)s * a.tau_stride, g.gidx_dev);
-    LCHK(cudaGetLastError());
-    g.launches++;
+    {
+      bool done = false;
+      int rc0 = bc_tau(g, g.X[q], a, s, st, &done);
+      if (rc0) return rc0;
+      if (done) continue;
+    }
     // ---- backward sweep ----
     for (int j = N - 1; j >= 0; --j) {
       build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);

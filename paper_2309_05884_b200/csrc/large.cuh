@@ -102,6 +102,12 @@ struct LargeGroup {
   const double2** gentall_dev = nullptr;  // per block a_k^T for k = 0..K
   std::vector<void*> gentall_mem;
   int last_nb = 0, last_s = 0, last_taylor_terms = 0;
+  // boundary conditions for slice-chunk sharding (set by the engine for one sqoc_eval_chunk /
+  // sqoc_chunk_product call, cleared afterwards)
+  const double2** bc_x_dev = nullptr;     // device array of per-block X_start pointers, or null
+  const double2** bc_l_dev = nullptr;     // device array of per-block Lam_end pointers, or null
+  const double2* bc_tau = nullptr;        // device [nblk] full-grid tau_b, or null
+  std::vector<double2*> fwd_out;          // forward-only: X_N of each block copied here
   int mode = -1;                    // last schedule used: 0 sequential, 1 history, 2 state-vector
   int force_mode = -1;              // -1 auto, 0 sequential, 1 history, 2 state-vector
   int launches = 0;

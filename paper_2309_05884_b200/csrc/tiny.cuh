@@ -1,11 +1,16 @@
 // Fused on-chip GRAPE evaluation for tiny symmetry blocks (d <= 16).
 //
-// One group of d lanes owns one (control vector, block) problem; lane r owns
-// row r of every d x d matrix.  Right-hand GEMM operands live in shared memory
-// and are read as warp broadcasts; left operands are the lane's own row.
-// FP64 on sm_100a: DFMA and DMMA run at the same 64 FMA/clk/SM (measured,
-// profiles/r01_fp64_peak.txt), so a DFMA kernel that pads nothing beats a
-// DMMA kernel that pads 13 -> 16.
+// Mapping: 16 lanes own one (control vector, block) problem, two problems per
+// warp.  The 16 lanes form a 4x4 grid; lane (tr, tc) owns the TS x TS register
+// tile rows [tr*TS, tr*TS+TS) x cols [tc*TS, tc*TS+TS) of every d x d product
+// (TS = ceil(d/4)), so each k-step loads 2 TS complex values from shared memory
+// and issues TS^2 complex FMAs.  Why: on sm_100a a shared-memory wavefront feeds
+// 4 B per lane per clock while the FP64 pipe retires 0.5 DFMA per lane per clock,
+// so a kernel needs >= 2 complex FMAs per complex value loaded to be FP64-bound;
+// a row-per-lane mapping gets 1 (measured: LSU 67% busy, FP64 37%,
+// profiles/r01_tiny13_ncu.txt).  DFMA and DMMA both run 64 FMA/clk/SM on B200
+// (profiles/r01_fp64_peak.txt), and DMMA would pad 13 -> 16 in all three
+// dimensions; here the k dimension stays exact (only output tiles pad).
 //
 // Per slice j (A_j = -i dt (H0 + sum_k u_kj H_k), U_j = R(A_j) with
 // R = Taylor_m(A/2^s)^(2^s), Paterson-Stockmeyer with A^2, A^3):
@@ -23,6 +28,7 @@ namespace sqoc {
 constexpr int kTinyMaxDim = 16;
 constexpr int kTinyBuffers = 8;   // d x d matrices per problem in shared memory
 constexpr int kMaxControls = 4;
+constexpr int kTinyLanes = 16;    // lanes per problem
 
 struct TinyParams {
   int K, N, batch;
@@ -34,7 +40,7 @@ struct TinyParams {
   double2* tau_out;       // tau of (problem, block) at tau_out[prob * tau_stride]
   int tau_stride;
   double* grad_out;       // [batch][K][N] contribution of this block
-  double2* park;          // [batch][2][d*R] workspace (X, Lam between phases)
+  double2* park;          // [slots][2][d*R] workspace (X, Lam between phases)
   int nwarps;             // warps per CTA
 };
 
@@ -77,89 +83,120 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
 
-// acc[c] = sum_k L[k] * M[k][c]      (L: own row, M: full matrix in smem, ld D)
-template <int D, int NC>
-__device__ __forceinline__ void row_mul(double2 (&acc)[NC], const double2* L, const double2* M) {
+__device__ __forceinline__ double half_sum(double v) {  // sum over the 16 lanes of a problem (fixed tree)
 #pragma unroll
-  for (int c = 0; c < NC; ++c) acc[c] = czero();
-#pragma unroll 1
-  for (int k = 0; k < D; ++k) {
-    const double2 l = L[k];
-    const double2* m = M + k * NC;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) cfma(acc[c], l, m[c]);
-  }
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
-
-// acc[c] = sum_k conj(U[k][r]) * M[k][c]   (U^dag * M, U full in smem)
-template <int D, int NC>
-__device__ __forceinline__ void row_mul_adj(double2 (&acc)[NC], const double2* U, int r, const double2* M) {
-#pragma unroll
-  for (int c = 0; c < NC; ++c) acc[c] = czero();
-#pragma unroll 1
-  for (int k = 0; k < D; ++k) {
-    const double2 l = cconj(U[k * D + r]);
-    const double2* m = M + k * NC;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) cfma(acc[c], l, m[c]);
-  }
+__device__ __forceinline__ double2 half_sum2(double2 v) { return make_double2(half_sum(v.x), half_sum(v.y)); }
+__device__ __forceinline__ double quad_sum(double v) {  // sum over the 4 lanes sharing a tile row (tc = 0..3)
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
 }
-
-// (T, dT) = (L, dL) x (M, dM):  T = L M,  dT = L dM + dL M
-template <int D>
-__device__ __forceinline__ void row_mul_pair(double2 (&t)[D], double2 (&dt)[D], const double2* L,
-                                             const double2* dL, const double2* M, const double2* dM) {
-#pragma unroll
-  for (int c = 0; c < D; ++c) { t[c] = czero(); dt[c] = czero(); }
-#pragma unroll 1
-  for (int k = 0; k < D; ++k) {
-    const double2 l = L[k], dl = dL[k];
-    const double2* m = M + k * D;
-    const double2* dm = dM + k * D;
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      const double2 mc = m[c];
-      cfma(t[c], l, mc);
-      cfma(dt[c], dl, mc);
-      cfma(dt[c], l, dm[c]);
-    }
-  }
-}
-
-template <int NC>
-__device__ __forceinline__ void store_row(double2* dst, const double2 (&v)[NC], bool wr) {
-  if (wr) {
-#pragma unroll
-    for (int c = 0; c < NC; ++c) dst[c] = v[c];
-  }
-}
-
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
-// Deterministic in-group sum: every lane writes its partial, the group's lanes
-// then all read the d partials in order (same result in every lane).
-template <int D>
-__device__ __forceinline__ double2 group_sum(double2 v, double2* red, int r, bool wr) {
-  __syncwarp();
-  if (wr) red[r] = v;
-  __syncwarp();
-  double2 s = czero();
+// Tile helpers.  Lane owns rows r0..r0+TS-1, cols c0..c0+TS-1 of a D x D matrix (ld D);
+// indices are clamped into range so padding lanes read valid memory (never stored).
+template <int D, int TS>
+struct Tile {
+  int r0, c0;
+  __device__ __forceinline__ int row(int i) const { return min(r0 + i, D - 1); }
+  __device__ __forceinline__ int col(int j) const { return min(c0 + j, D - 1); }
+  __device__ __forceinline__ bool ok(int i, int j) const { return r0 + i < D && c0 + j < D; }
+
+  __device__ __forceinline__ void zero(double2 (&t)[TS][TS]) const {
 #pragma unroll
-  for (int i = 0; i < D; ++i) s = cadd(s, red[i]);
-  __syncwarp();
-  return s;
-}
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int j = 0; j < TS; ++j) t[i][j] = czero();
+  }
+  __device__ __forceinline__ void load(double2 (&t)[TS][TS], const double2* M) const {
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int j = 0; j < TS; ++j) t[i][j] = M[row(i) * D + col(j)];
+  }
+  __device__ __forceinline__ void store(double2* M, const double2 (&t)[TS][TS], bool wr) const {
+    if (!wr) return;
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int j = 0; j < TS; ++j)
+        if (ok(i, j)) M[(r0 + i) * D + c0 + j] = t[i][j];
+  }
+  // t = L M   (L, M: D x D in smem)
+  __device__ __forceinline__ void mul(double2 (&t)[TS][TS], const double2* L, const double2* M) const {
+    zero(t);
+#pragma unroll 2
+    for (int k = 0; k < D; ++k) {
+      double2 l[TS], m[TS];
+#pragma unroll
+      for (int i = 0; i < TS; ++i) l[i] = L[row(i) * D + k];
+#pragma unroll
+      for (int j = 0; j < TS; ++j) m[j] = M[k * D + col(j)];
+#pragma unroll
+      for (int i = 0; i < TS; ++i)
+#pragma unroll
+        for (int j = 0; j < TS; ++j) cfma(t[i][j], l[i], m[j]);
+    }
+  }
+  // t = U^dag M
+  __device__ __forceinline__ void mul_adj(double2 (&t)[TS][TS], const double2* U, const double2* M) const {
+    zero(t);
+#pragma unroll 2
+    for (int k = 0; k < D; ++k) {
+      double2 l[TS], m[TS];
+#pragma unroll
+      for (int i = 0; i < TS; ++i) l[i] = cconj(U[k * D + row(i)]);
+#pragma unroll
+      for (int j = 0; j < TS; ++j) m[j] = M[k * D + col(j)];
+#pragma unroll
+      for (int i = 0; i < TS; ++i)
+#pragma unroll
+        for (int j = 0; j < TS; ++j) cfma(t[i][j], l[i], m[j]);
+    }
+  }
+  // (t, dt) = (L, dL)(M, dM) = (L M, L dM + dL M)
+  __device__ __forceinline__ void pair(double2 (&t)[TS][TS], double2 (&dt)[TS][TS], const double2* L,
+                                       const double2* dL, const double2* M, const double2* dM) const {
+    zero(t);
+    zero(dt);
+#pragma unroll 1
+    for (int k = 0; k < D; ++k) {
+      double2 l[TS], dl[TS], m[TS], dm[TS];
+#pragma unroll
+      for (int i = 0; i < TS; ++i) {
+        l[i] = L[row(i) * D + k];
+        dl[i] = dL[row(i) * D + k];
+      }
+#pragma unroll
+      for (int j = 0; j < TS; ++j) {
+        m[j] = M[k * D + col(j)];
+        dm[j] = dM[k * D + col(j)];
+      }
+#pragma unroll
+      for (int i = 0; i < TS; ++i)
+#pragma unroll
+        for (int j = 0; j < TS; ++j) {
+          cfma(t[i][j], l[i], m[j]);
+          cfma(dt[i][j], dl[i], m[j]);
+          cfma(dt[i][j], l[i], dm[j]);
+        }
+    }
+  }
+};
 
 template <int D, bool GATE>
 __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
   constexpr int R = GATE ? D : 1;  // columns of X and Lam
-  constexpr int PG = 32 / D;       // problems per warp
+  constexpr int TS = (D + 3) / 4;  // register tile edge
   constexpr int DD = D * D;
-  constexpr int PSTRIDE = kTinyBuffers * DD + D;  // per-problem smem (double2)
+  constexpr int PSTRIDE = kTinyBuffers * DD;
   extern __shared__ double2 smem[];
 
   const int K = p.K, N = p.N;
@@ -168,220 +205,284 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g_raw = lane / D;
-  const bool lane_used = g_raw < PG;
-  const int g = lane_used ? g_raw : 0;
-  const int r = lane_used ? lane - g_raw * D : 0;
-  const int slot = (blockIdx.x * p.nwarps + warp) * PG + g;  // problem slot (park is sized for all slots)
-  const bool wr = lane_used && slot < p.batch;  // this lane owns a real problem and may store globally
-  const int prob = slot < p.batch ? slot : p.batch - 1;  // padding slots replay the last problem's u
+  const int half = lane >> 4, q = lane & 15;
+  const int tr = q >> 2, tc = q & 3;
+  Tile<D, TS> tl{tr * TS, tc * TS};
+  const int slot = (blockIdx.x * p.nwarps + warp) * 2 + half;  // park is sized for all slots
+  const bool real = slot < p.batch;                            // owns a real problem (may store globally)
+  const int prob = real ? slot : p.batch - 1;                  // padding slots replay the last problem's u
 
-  double2* buf = gen + (K + 1) * DD + (size_t)(warp * PG + g) * PSTRIDE;
-  double2* B0 = buf;           // X (fwd) | X, A2 (bwd)
-  double2* B1 = B0 + DD;       // Lam, dA2
-  double2* B2 = B1 + DD;       // A
-  double2* B3 = B2 + DD;       // Adot
-  double2* B4 = B3 + DD;       // A3
-  double2* B5 = B4 + DD;       // dA3
-  double2* B6 = B5 + DD;       // T  (-> U)
-  double2* B7 = B6 + DD;       // dT (-> N)
-  double2* red = B7 + DD;      // D partials
+  double2* buf = gen + (K + 1) * DD + (size_t)(warp * 2 + half) * PSTRIDE;
+  double2* B0 = buf;      // X (fwd) | X, A2 (bwd)
+  double2* B1 = B0 + DD;  // A2 (fwd) | Lam, dA2 (bwd)
+  double2* B2 = B1 + DD;  // A
+  double2* B3 = B2 + DD;  // Adot
+  double2* B4 = B3 + DD;  // A3
+  double2* B5 = B4 + DD;  // dA3
+  double2* B6 = B5 + DD;  // T  (-> U)
+  double2* B7 = B6 + DD;  // dT (-> N)
   const double* up = p.u + (size_t)prob * K * N;
   double2* parkX = p.park + (size_t)slot * 2 * D * R;
   double2* parkL = parkX + D * R;
 
-  // ---- build A row r for slice j, return warp-uniform Taylor plan ----
-  auto build_a = [&](int j, double2 (&arow)[D], int& nb, int& s) {
+  // ---- A tile for slice j (scaled by 2^-s), warp-uniform Taylor plan ----
+  auto build_a = [&](int j, double2 (&a)[TS][TS], int& nb, int& s) {
     double uk[kMaxControls];
 #pragma unroll
     for (int k = 0; k < kMaxControls; ++k) uk[k] = (k < K) ? up[k * N + j] : 0.0;
+    double rowsum[TS];
+#pragma unroll
+    for (int i = 0; i < TS; ++i) {
+      rowsum[i] = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < TS; ++jj) {
+        const int o = tl.row(i) * D + tl.col(jj);
+        double2 v = gen[o];
+        for (int k = 0; k < K; ++k) {
+          const double2 e = gen[(k + 1) * DD + o];
+          v.x = fma(uk[k], e.x, v.x);
+          v.y = fma(uk[k], e.y, v.y);
+        }
+        a[i][jj] = v;
+        if (tl.ok(i, jj)) rowsum[i] += fabs(v.x) + fabs(v.y);
+      }
+    }
     double nrm = 0.0;
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-      double2 a = gen[r * D + c];
-      for (int k = 0; k < K; ++k) {
-        const double2 e = gen[(k + 1) * DD + r * D + c];
-        a.x = fma(uk[k], e.x, a.x);
-        a.y = fma(uk[k], e.y, a.y);
-      }
-      arow[c] = a;
-      nrm += fabs(a.x) + fabs(a.y);
-    }
-    nrm = warp_max(wr ? nrm : 0.0);  // plan is warp-uniform, from real problems only
+    for (int i = 0; i < TS; ++i) nrm = fmax(nrm, quad_sum(rowsum[i]));
+    nrm = warp_max(real ? nrm : 0.0);  // plan is warp-uniform, from real problems only
     choose_taylor(nrm, nb, s);
     const double sc = ldexp(1.0, -s);
 #pragma unroll
-    for (int c = 0; c < D; ++c) arow[c] = cscale(arow[c], sc);
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TS; ++jj) a[i][jj] = cscale(a[i][jj], sc);
   };
 
-  // Q_t own row: c_{3t} I + c_{3t+1} A + c_{3t+2} A2
-  auto q_row = [&](int t, int c, const double2* A, const double2* A2) {
-    double2 v = cadd(cscale(A[r * D + c], c_inv_fact[3 * t + 1]), cscale(A2[r * D + c], c_inv_fact[3 * t + 2]));
-    if (c == r) v.x += c_inv_fact[3 * t];
-    return v;
+  // Q_t tile: c_{3t} I + c_{3t+1} A + c_{3t+2} A2 ; dQ_t: c_{3t+1} dA + c_{3t+2} dA2
+  auto add_q = [&](double2 (&t)[TS][TS], int qi, const double2* A, const double2* A2) {
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TS; ++jj) {
+        const int o = tl.row(i) * D + tl.col(jj);
+        t[i][jj] = cadd(t[i][jj], cadd(cscale(A[o], c_inv_fact[3 * qi + 1]), cscale(A2[o], c_inv_fact[3 * qi + 2])));
+        if (tl.r0 + i == tl.c0 + jj) t[i][jj].x += c_inv_fact[3 * qi];
+      }
   };
-  auto dq_row = [&](int t, int c, const double2* dA, const double2* dA2) {
-    return cadd(cscale(dA[r * D + c], c_inv_fact[3 * t + 1]), cscale(dA2[r * D + c], c_inv_fact[3 * t + 2]));
+  auto add_dq = [&](double2 (&t)[TS][TS], int qi, const double2* dA, const double2* dA2) {
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TS; ++jj) {
+        const int o = tl.row(i) * D + tl.col(jj);
+        t[i][jj] = cadd(t[i][jj], cadd(cscale(dA[o], c_inv_fact[3 * qi + 1]), cscale(dA2[o], c_inv_fact[3 * qi + 2])));
+      }
+  };
+  auto scale_tile = [&](double2 (&t)[TS][TS], double c) {
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TS; ++jj) t[i][jj] = cscale(t[i][jj], c);
   };
 
-  // ================= forward sweep: X_N =================
-  double2 row[D];
-  {
-    double2* X = B0;
+  // ---- X-shaped products (R columns): gate -> tiles; state -> one column, k split over tc ----
+  // out = Op(U) Y where Op(U) = U (adj=false) or U^dag (adj=true); Y: D x R; store into Yout (may alias Y)
+  auto mul_x = [&](const double2* U, bool adj, const double2* Y, double2* Yout) {
+    if (GATE) {
+      double2 t[TS][TS];
+      if (adj) tl.mul_adj(t, U, Y);
+      else tl.mul(t, U, Y);
+      __syncwarp();
+      tl.store(Yout, t, true);  // park is sized for every slot, padding slots included
+    } else {
+      double2 v[TS];
+#pragma unroll
+      for (int i = 0; i < TS; ++i) v[i] = czero();
+      for (int k = tc; k < D; k += 4) {
+        const double2 y = Y[k];
+#pragma unroll
+        for (int i = 0; i < TS; ++i) {
+          const double2 l = adj ? cconj(U[k * D + tl.row(i)]) : U[tl.row(i) * D + k];
+          cfma(v[i], l, y);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TS; ++i) v[i] = make_double2(quad_sum(v[i].x), quad_sum(v[i].y));
+      __syncwarp();
+      if (tc == 0) {
+#pragma unroll
+        for (int i = 0; i < TS; ++i)
+          if (tl.r0 + i < D) Yout[tl.r0 + i] = v[i];
+      }
+    }
+  };
+  // copy a D x R matrix between smem and global (own tile / own rows)
+  auto copy_x = [&](double2* dst, const double2* src, bool wr) {
+    if (!wr) return;
     if (GATE) {
 #pragma unroll
-      for (int c = 0; c < R; ++c) row[c] = make_double2(c == r ? 1.0 : 0.0, 0.0);
-    } else {
-      row[0] = p.x0[r];
-    }
-    store_row<R>(X + r * R, *reinterpret_cast<double2(*)[R]>(row), lane_used);
-    __syncwarp();
-    for (int j = 0; j < N; ++j) {
-      int nb, s;
-      build_a(j, row, nb, s);
-      store_row<D>(B2 + r * D, row, lane_used);
-      __syncwarp();
-      row_mul<D, D>(row, B2 + r * D, B2);  // A2
-      store_row<D>(B1 + r * D, row, lane_used);
-      __syncwarp();
-      row_mul<D, D>(row, B1 + r * D, B2);  // A3
-      store_row<D>(B4 + r * D, row, lane_used);
-      __syncwarp();
-      // Horner in A3: T = c_{3nb} A3 + Q_{nb-1}
+      for (int i = 0; i < TS; ++i)
 #pragma unroll
-      for (int c = 0; c < D; ++c) row[c] = cadd(cscale(row[c], c_inv_fact[3 * nb]), q_row(nb - 1, c, B2, B1));
-      for (int t = nb - 2; t >= 0; --t) {
-        store_row<D>(B6 + r * D, row, lane_used);
-        __syncwarp();
-        row_mul<D, D>(row, B6 + r * D, B4);
+        for (int jj = 0; jj < TS; ++jj)
+          if (tl.ok(i, jj)) dst[(tl.r0 + i) * D + tl.c0 + jj] = src[(tl.r0 + i) * D + tl.c0 + jj];
+    } else if (tc == 0) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) row[c] = cadd(row[c], q_row(t, c, B2, B1));
-      }
-      store_row<D>(B6 + r * D, row, lane_used);
-      for (int q = 0; q < s; ++q) {
-        __syncwarp();
-        row_mul<D, D>(row, B6 + r * D, B6);
-        __syncwarp();
-        store_row<D>(B6 + r * D, row, lane_used);
-      }
-      __syncwarp();
-      double2 xr[R];
-      row_mul<D, R>(xr, B6 + r * D, X);  // X_j = U_j X_{j-1}
-      __syncwarp();
-      store_row<R>(X + r * R, xr, lane_used);
-      __syncwarp();
+      for (int i = 0; i < TS; ++i)
+        if (tl.r0 + i < D) dst[tl.r0 + i] = src[tl.r0 + i];
     }
-    // tau = <V, X_N>_F ; park X_N and Lam_N = V
-    double2 part = czero();
-#pragma unroll
-    for (int c = 0; c < R; ++c) {
-      const double2 v = p.target[r * R + c];
-      const double2 x = X[r * R + c];
-      part = cadd(part, cmul(cconj(v), x));
-      if (lane_used) { parkX[r * R + c] = x; parkL[r * R + c] = v; }
-    }
-    const double2 tau = group_sum<D>(part, red, r, lane_used);
-    if (wr && r == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
+  };
 
-    // ================= backward sweep: gradient =================
-    const double2 ctw = cscale(cconj(tau), 2.0 * p.weight);  // dF/du = Re(2 w conj(tau) dtau/du)
-    for (int j = N - 1; j >= 0; --j) {
-      int nb, s;
-      // stage X_j, Lam_j (own rows) into B0 / B1
-      if (lane_used) {
+  double2 t[TS][TS], dt[TS][TS];
+  // ================= forward sweep: X_N =================
+  double2* X = B0;
+  if (GATE) {
 #pragma unroll
-        for (int c = 0; c < R; ++c) { B0[r * R + c] = parkX[r * R + c]; B1[r * R + c] = parkL[r * R + c]; }
-      }
-      build_a(j, row, nb, s);
-      store_row<D>(B2 + r * D, row, lane_used);
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TS; ++jj) t[i][jj] = make_double2(tl.r0 + i == tl.c0 + jj ? 1.0 : 0.0, 0.0);
+    tl.store(X, t, true);
+  } else {
+    copy_x(X, p.x0, true);
+  }
+  __syncwarp();
+  for (int j = 0; j < N; ++j) {
+    int nb, s;
+    build_a(j, t, nb, s);
+    tl.store(B2, t, true);
+    __syncwarp();
+    tl.mul(t, B2, B2);  // A2
+    tl.store(B1, t, true);
+    __syncwarp();
+    tl.mul(t, B1, B2);  // A3
+    tl.store(B4, t, true);
+    __syncwarp();
+    scale_tile(t, c_inv_fact[3 * nb]);  // T = c_{3nb} A3 + Q_{nb-1}
+    add_q(t, nb - 1, B2, B1);
+    tl.store(B6, t, true);
+    for (int qi = nb - 2; qi >= 0; --qi) {
       __syncwarp();
-      {  // C = X Lam^dag (scaled by 2^-s) -> Adot
-        const double sc = ldexp(1.0, -s);
-        double2 crow[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) crow[c] = czero();
-#pragma unroll 1
-        for (int k = 0; k < R; ++k) {
-          const double2 x = B0[r * R + k];
-#pragma unroll
-          for (int c = 0; c < D; ++c) cfma(crow[c], x, cconj(B1[c * R + k]));
-        }
-#pragma unroll
-        for (int c = 0; c < D; ++c) crow[c] = cscale(crow[c], sc);
-        store_row<D>(B3 + r * D, crow, lane_used);
-      }
+      tl.mul(t, B6, B4);
+      add_q(t, qi, B2, B1);
       __syncwarp();
-      double2 drow[D];
-      row_mul_pair<D>(row, drow, B2 + r * D, B3 + r * D, B2, B3);  // (A2, dA2)
-      store_row<D>(B0 + r * D, row, lane_used);
-      store_row<D>(B1 + r * D, drow, lane_used);
-      __syncwarp();
-      row_mul_pair<D>(row, drow, B0 + r * D, B1 + r * D, B2, B3);  // (A3, dA3)
-      store_row<D>(B4 + r * D, row, lane_used);
-      store_row<D>(B5 + r * D, drow, lane_used);
-      __syncwarp();
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        row[c] = cadd(cscale(row[c], c_inv_fact[3 * nb]), q_row(nb - 1, c, B2, B0));
-        drow[c] = cadd(cscale(drow[c], c_inv_fact[3 * nb]), dq_row(nb - 1, c, B3, B1));
-      }
-      for (int t = nb - 2; t >= 0; --t) {
-        store_row<D>(B6 + r * D, row, lane_used);
-        store_row<D>(B7 + r * D, drow, lane_used);
-        __syncwarp();
-        row_mul_pair<D>(row, drow, B6 + r * D, B7 + r * D, B4, B5);
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-          row[c] = cadd(row[c], q_row(t, c, B2, B0));
-          drow[c] = cadd(drow[c], dq_row(t, c, B3, B1));
-        }
-      }
-      store_row<D>(B6 + r * D, row, lane_used);
-      store_row<D>(B7 + r * D, drow, lane_used);
-      for (int q = 0; q < s; ++q) {
-        __syncwarp();
-        row_mul_pair<D>(row, drow, B6 + r * D, B7 + r * D, B6, B7);
-        __syncwarp();
-        store_row<D>(B6 + r * D, row, lane_used);
-        store_row<D>(B7 + r * D, drow, lane_used);
-      }
-      __syncwarp();
-      // restage X_j, Lam_j (B0/B1 were reused)
-      if (lane_used) {
-#pragma unroll
-        for (int c = 0; c < R; ++c) { B0[r * R + c] = parkX[r * R + c]; B1[r * R + c] = parkL[r * R + c]; }
-      }
-      __syncwarp();
-      // D = U^dag N ; dtau/du_k = Tr(D E_k) = sum_q D[r][q] E_k[q][r]
-      row_mul_adj<D, D>(row, B6, r, B7);
-      for (int k = 0; k < K; ++k) {
-        const double2* E = gen + (k + 1) * DD;
-        double2 part2 = czero();
-#pragma unroll
-        for (int q = 0; q < D; ++q) cfma(part2, row[q], E[q * D + r]);
-        const double2 dtau = group_sum<D>(part2, red, r, lane_used);
-        if (wr && r == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau.x - ctw.y * dtau.y;
-      }
-      // X_{j-1} = U^dag X_j, Lam_{j-1} = U^dag Lam_j  -> park
-      double2 xr[R];
-      row_mul_adj<D, R>(xr, B6, r, B0);
-      if (lane_used) {
-#pragma unroll
-        for (int c = 0; c < R; ++c) parkX[r * R + c] = xr[c];
-      }
-      row_mul_adj<D, R>(xr, B6, r, B1);
-      if (lane_used) {
-#pragma unroll
-        for (int c = 0; c < R; ++c) parkL[r * R + c] = xr[c];
-      }
-      __syncwarp();
+      tl.store(B6, t, true);
     }
+    for (int r = 0; r < s; ++r) {
+      __syncwarp();
+      tl.mul(t, B6, B6);
+      __syncwarp();
+      tl.store(B6, t, true);
+    }
+    __syncwarp();
+    mul_x(B6, false, X, X);  // X_j = U_j X_{j-1} (in place after the sync inside)
+    __syncwarp();
+  }
+  // tau = <V, X_N>_F ; park X_N and Lam_N = V
+  double2 part = czero();
+  if (GATE) {
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TS; ++jj)
+        if (tl.ok(i, jj)) {
+          const int o = (tl.r0 + i) * D + tl.c0 + jj;
+          part = cadd(part, cmul(cconj(p.target[o]), X[o]));
+        }
+  } else if (tc == 0) {
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+      if (tl.r0 + i < D) part = cadd(part, cmul(cconj(p.target[tl.r0 + i]), X[tl.r0 + i]));
+  }
+  const double2 tau = half_sum2(part);
+  if (real && q == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
+  copy_x(parkX, X, true);
+  copy_x(parkL, p.target, true);
+  __syncwarp();
+
+  // ================= backward sweep: gradient =================
+  const double2 ctw = cscale(cconj(tau), 2.0 * p.weight);  // dF/du = Re(2 w conj(tau) dtau/du)
+  for (int j = N - 1; j >= 0; --j) {
+    int nb, s;
+    copy_x(B0, parkX, true);  // stage X_j, Lam_j
+    copy_x(B1, parkL, true);
+    build_a(j, t, nb, s);
+    tl.store(B2, t, true);
+    __syncwarp();
+    {  // Adot = 2^-s X_j Lam_j^dag
+      const double sc = ldexp(1.0, -s);
+      tl.zero(t);
+#pragma unroll 1
+      for (int k = 0; k < R; ++k) {
+        double2 l[TS], m[TS];
+#pragma unroll
+        for (int i = 0; i < TS; ++i) l[i] = B0[tl.row(i) * R + k];
+#pragma unroll
+        for (int jj = 0; jj < TS; ++jj) m[jj] = cconj(B1[tl.col(jj) * R + k]);
+#pragma unroll
+        for (int i = 0; i < TS; ++i)
+#pragma unroll
+          for (int jj = 0; jj < TS; ++jj) cfma(t[i][jj], l[i], m[jj]);
+      }
+      scale_tile(t, sc);
+      tl.store(B3, t, true);
+    }
+    __syncwarp();
+    tl.pair(t, dt, B2, B3, B2, B3);  // (A2, dA2)
+    tl.store(B0, t, true);
+    tl.store(B1, dt, true);
+    __syncwarp();
+    tl.pair(t, dt, B0, B1, B2, B3);  // (A3, dA3)
+    tl.store(B4, t, true);
+    tl.store(B5, dt, true);
+    __syncwarp();
+    scale_tile(t, c_inv_fact[3 * nb]);
+    scale_tile(dt, c_inv_fact[3 * nb]);
+    add_q(t, nb - 1, B2, B0);
+    add_dq(dt, nb - 1, B3, B1);
+    tl.store(B6, t, true);
+    tl.store(B7, dt, true);
+    for (int qi = nb - 2; qi >= 0; --qi) {
+      __syncwarp();
+      tl.pair(t, dt, B6, B7, B4, B5);
+      add_q(t, qi, B2, B0);
+      add_dq(dt, qi, B3, B1);
+      __syncwarp();
+      tl.store(B6, t, true);
+      tl.store(B7, dt, true);
+    }
+    for (int r = 0; r < s; ++r) {
+      __syncwarp();
+      tl.pair(t, dt, B6, B7, B6, B7);
+      __syncwarp();
+      tl.store(B6, t, true);
+      tl.store(B7, dt, true);
+    }
+    __syncwarp();
+    copy_x(B0, parkX, true);  // restage X_j, Lam_j (B0/B1 were reused)
+    copy_x(B1, parkL, true);
+    __syncwarp();
+    // D = U^dag N ; dtau/du_k = Tr(D E_k) = sum_pq D[p][q] E_k[q][p]
+    tl.mul_adj(t, B6, B7);
+    for (int k = 0; k < K; ++k) {
+      const double2* E = gen + (k + 1) * DD;
+      double2 pk = czero();
+#pragma unroll
+      for (int i = 0; i < TS; ++i)
+#pragma unroll
+        for (int jj = 0; jj < TS; ++jj)
+          if (tl.ok(i, jj)) cfma(pk, t[i][jj], E[(tl.c0 + jj) * D + tl.r0 + i]);
+      const double2 dtau = half_sum2(pk);
+      if (real && q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau.x - ctw.y * dtau.y;
+    }
+    // X_{j-1} = U^dag X_j, Lam_{j-1} = U^dag Lam_j  -> park (global, own entries)
+    mul_x(B6, true, B0, parkX);
+    mul_x(B6, true, B1, parkL);
+    __syncwarp();
   }
 }
 
 inline size_t tiny_smem_bytes(int d, int K, int nwarps) {
-  const int pg = 32 / d;
-  return sizeof(double2) * ((size_t)(K + 1) * d * d + (size_t)nwarps * pg * (kTinyBuffers * d * d + d));
+  return sizeof(double2) * ((size_t)(K + 1) * d * d + (size_t)nwarps * 2 * kTinyBuffers * d * d);
 }
 
 }  // namespace sqoc

@@ -164,6 +164,30 @@ class GrapeEngine:
         """objective(u) -> (F, grad): the BASELINE host API."""
         return self.evaluate(u)
 
+    # ---- slice-chunk sharding (DESIGN.md section 6) ----
+    def chunk_product(self, u) -> list:
+        """[U_{N-1} ... U_0 per block] for this problem's slices (gate-objective problem)."""
+        u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+        outs = [np.empty((d, d), dtype=np.complex128) for d in self.dims]
+        arr = (ctypes.c_void_p * self.nblocks)(*[o.ctypes.data for o in outs])
+        _lib.check(self.lib.sqoc_chunk_product(self.handle, u.ctypes.data, arr, _lib.MEM_HOST, None),
+                   "sqoc_chunk_product")
+        return outs
+
+    def eval_chunk(self, u, x_start, lam_end, tau):
+        """(F, grad (K, N_local)) of this rank's slices given full-grid boundary values."""
+        u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+        xs = [np.ascontiguousarray(x, dtype=np.complex128) for x in x_start]
+        ls = [np.ascontiguousarray(x, dtype=np.complex128) for x in lam_end]
+        t = np.ascontiguousarray(np.asarray(tau, dtype=np.complex128).reshape(-1))
+        xa = (ctypes.c_void_p * self.nblocks)(*[x.ctypes.data for x in xs])
+        la = (ctypes.c_void_p * self.nblocks)(*[x.ctypes.data for x in ls])
+        F = np.empty(1)
+        grad = np.empty_like(u)
+        _lib.check(self.lib.sqoc_eval_chunk(self.handle, u.ctypes.data, xa, la, t.ctypes.data, F.ctypes.data,
+                                            grad.ctypes.data, _lib.MEM_HOST, None), "sqoc_eval_chunk")
+        return float(F[0]), grad
+
     def evaluate_host_ptr(self, u_ptr: int, batch: int, F_ptr: int, grad_ptr: int):
         """Host pointers (e.g. pinned torch tensors); copies happen inside the call."""
         rc = self.lib.sqoc_eval(self.handle, u_ptr, batch, F_ptr or None, grad_ptr or None, None, _lib.MEM_HOST, None)

@@ -116,3 +116,17 @@ def test_cfg4_short_grid_schedules_agree():
     F2, g2 = eng.objective(u)
     assert abs(F1 - F2) <= F_TOL
     assert rel(g1, g2) <= G_TOL
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slice_chunk_sharding_emulated_on_one_gpu(world):
+    """The multi-GPU scan-carry algorithm (parallel.py) run as `world` emulated ranks through
+    sqoc_chunk_product / sqoc_eval_chunk equals the unsharded evaluation."""
+    from paper_2309_05884_b200 import parallel
+
+    for s in (systems.config(2, n_slices=24), systems.state_transfer_ring(8, 10.0 * 12 / 200, 12, seed=4, full=True)):
+        u = s.controls(6)
+        F0, g0 = GrapeEngine(s, max_batch=1).objective(u)
+        F, g = parallel.emulate_ranks(s, world, lambda sys_: GrapeEngine(sys_, max_batch=1), u)
+        assert abs(F - F0) <= F_TOL
+        assert rel(g, g0) <= G_TOL
