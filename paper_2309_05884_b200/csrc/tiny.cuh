@@ -100,14 +100,19 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-// Tile helpers.  Lane owns rows r0..r0+TS-1, cols c0..c0+TS-1 of a D x D matrix (ld D);
-// indices are clamped into range so padding lanes read valid memory (never stored).
+// Tile helpers.  Lane (tr, tc) owns rows tr + 4i and cols tc + 4j (i, j < TS) of a D x D
+// matrix (ld D).  The interleaved ownership makes the 4 lanes of a tile row read 4
+// consecutive complex values of a matrix row in one LDS.128 wavefront (no bank conflict).
+// Indices are clamped into range so padding lanes read valid memory (never stored).
 template <int D, int TS>
 struct Tile {
-  int r0, c0;
-  __device__ __forceinline__ int row(int i) const { return min(r0 + i, D - 1); }
-  __device__ __forceinline__ int col(int j) const { return min(c0 + j, D - 1); }
-  __device__ __forceinline__ bool ok(int i, int j) const { return r0 + i < D && c0 + j < D; }
+  int tr, tc;
+  __device__ __forceinline__ int row(int i) const { return min(tr + 4 * i, D - 1); }
+  __device__ __forceinline__ int col(int j) const { return min(tc + 4 * j, D - 1); }
+  __device__ __forceinline__ bool ok(int i, int j) const { return tr + 4 * i < D && tc + 4 * j < D; }
+  __device__ __forceinline__ bool row_ok(int i) const { return tr + 4 * i < D; }
+  __device__ __forceinline__ int rrow(int i) const { return tr + 4 * i; }  // unclamped
+  __device__ __forceinline__ int rcol(int j) const { return tc + 4 * j; }
 
   __device__ __forceinline__ void zero(double2 (&t)[TS][TS]) const {
 #pragma unroll
@@ -127,7 +132,7 @@ struct Tile {
     for (int i = 0; i < TS; ++i)
 #pragma unroll
       for (int j = 0; j < TS; ++j)
-        if (ok(i, j)) M[(r0 + i) * D + c0 + j] = t[i][j];
+        if (ok(i, j)) M[rrow(i) * D + rcol(j)] = t[i][j];
   }
   // t = L M   (L, M: D x D in smem)
   __device__ __forceinline__ void mul(double2 (&t)[TS][TS], const double2* L, const double2* M) const {
@@ -168,7 +173,7 @@ struct Tile {
     zero(dt);
 #pragma unroll 1
     for (int k = 0; k < D; ++k) {
-      double2 l[TS], dl[TS], m[TS], dm[TS];
+      double2 l[TS], dl[TS];
 #pragma unroll
       for (int i = 0; i < TS; ++i) {
         l[i] = L[row(i) * D + k];
@@ -176,17 +181,15 @@ struct Tile {
       }
 #pragma unroll
       for (int j = 0; j < TS; ++j) {
-        m[j] = M[k * D + col(j)];
-        dm[j] = dM[k * D + col(j)];
-      }
+        const double2 m = M[k * D + col(j)];
+        const double2 dm = dM[k * D + col(j)];
 #pragma unroll
-      for (int i = 0; i < TS; ++i)
-#pragma unroll
-        for (int j = 0; j < TS; ++j) {
-          cfma(t[i][j], l[i], m[j]);
-          cfma(dt[i][j], dl[i], m[j]);
-          cfma(dt[i][j], l[i], dm[j]);
+        for (int i = 0; i < TS; ++i) {
+          cfma(t[i][j], l[i], m);
+          cfma(dt[i][j], dl[i], m);
+          cfma(dt[i][j], l[i], dm);
         }
+      }
     }
   }
 };
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, q = lane & 15;
   const int tr = q >> 2, tc = q & 3;
-  Tile<D, TS> tl{tr * TS, tc * TS};
+  Tile<D, TS> tl{tr, tc};
   const int slot = (blockIdx.x * p.nwarps + warp) * 2 + half;  // park is sized for all slots
   const bool real = slot < p.batch;                            // owns a real problem (may store globally)
   const int prob = real ? slot : p.batch - 1;                  // padding slots replay the last problem's u
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
       for (int jj = 0; jj < TS; ++jj) {
         const int o = tl.row(i) * D + tl.col(jj);
         t[i][jj] = cadd(t[i][jj], cadd(cscale(A[o], c_inv_fact[3 * qi + 1]), cscale(A2[o], c_inv_fact[3 * qi + 2])));
-        if (tl.r0 + i == tl.c0 + jj) t[i][jj].x += c_inv_fact[3 * qi];
+        if (tl.rrow(i) == tl.rcol(jj)) t[i][jj].x += c_inv_fact[3 * qi];
       }
   };
   auto add_dq = [&](double2 (&t)[TS][TS], int qi, const double2* dA, const double2* dA2) {
@@ -313,7 +316,7 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
       if (tc == 0) {
 #pragma unroll
         for (int i = 0; i < TS; ++i)
-          if (tl.r0 + i < D) Yout[tl.r0 + i] = v[i];
+          if (tl.row_ok(i)) Yout[tl.rrow(i)] = v[i];
       }
     }
   };
@@ -325,11 +328,11 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
       for (int i = 0; i < TS; ++i)
 #pragma unroll
         for (int jj = 0; jj < TS; ++jj)
-          if (tl.ok(i, jj)) dst[(tl.r0 + i) * D + tl.c0 + jj] = src[(tl.r0 + i) * D + tl.c0 + jj];
+          if (tl.ok(i, jj)) dst[tl.rrow(i) * D + tl.rcol(jj)] = src[tl.rrow(i) * D + tl.rcol(jj)];
     } else if (tc == 0) {
 #pragma unroll
       for (int i = 0; i < TS; ++i)
-        if (tl.r0 + i < D) dst[tl.r0 + i] = src[tl.r0 + i];
+        if (tl.row_ok(i)) dst[tl.rrow(i)] = src[tl.rrow(i)];
     }
   };
 
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
 #pragma unroll
     for (int i = 0; i < TS; ++i)
 #pragma unroll
-      for (int jj = 0; jj < TS; ++jj) t[i][jj] = make_double2(tl.r0 + i == tl.c0 + jj ? 1.0 : 0.0, 0.0);
+      for (int jj = 0; jj < TS; ++jj) t[i][jj] = make_double2(tl.rrow(i) == tl.rcol(jj) ? 1.0 : 0.0, 0.0);
     tl.store(X, t, true);
   } else {
     copy_x(X, p.x0, true);
@@ -385,13 +388,13 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
 #pragma unroll
       for (int jj = 0; jj < TS; ++jj)
         if (tl.ok(i, jj)) {
-          const int o = (tl.r0 + i) * D + tl.c0 + jj;
+          const int o = tl.rrow(i) * D + tl.rcol(jj);
           part = cadd(part, cmul(cconj(p.target[o]), X[o]));
         }
   } else if (tc == 0) {
 #pragma unroll
     for (int i = 0; i < TS; ++i)
-      if (tl.r0 + i < D) part = cadd(part, cmul(cconj(p.target[tl.r0 + i]), X[tl.r0 + i]));
+      if (tl.row_ok(i)) part = cadd(part, cmul(cconj(p.target[tl.rrow(i)]), X[tl.rrow(i)]));
   }
   const double2 tau = half_sum2(part);
   if (real && q == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
       for (int i = 0; i < TS; ++i)
 #pragma unroll
         for (int jj = 0; jj < TS; ++jj)
-          if (tl.ok(i, jj)) cfma(pk, t[i][jj], E[(tl.c0 + jj) * D + tl.r0 + i]);
+          if (tl.ok(i, jj)) cfma(pk, t[i][jj], E[tl.rcol(jj) * D + tl.rrow(i)]);
       const double2 dtau = half_sum2(pk);
       if (real && q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau.x - ctw.y * dtau.y;
     }
