@@ -130,7 +130,7 @@ static int launch_tiny(int d, const TinyParams& tp, int grid, int nwarps, size_t
 static int choose_nwarps(int d, int K, int batch) {
   const int pg = 32 / kTinyLanes;
   const int need = (batch + pg - 1) / pg;
-  int nw = 8;
+  int nw = kTinyMaxWarps;
   while (nw > 1 && tiny_smem_bytes(d, K, nw) > kMaxSmem) --nw;
   return std::max(1, std::min(nw, need));
 }

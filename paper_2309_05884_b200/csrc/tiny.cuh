@@ -1,10 +1,14 @@
 // Fused on-chip GRAPE evaluation for tiny symmetry blocks (d <= 16).
 //
-// Mapping: 16 lanes own one (control vector, block) problem, two problems per
-// warp.  The 16 lanes form a 4x4 grid; lane (tr, tc) owns the TS x TS register
-// tile rows [tr*TS, tr*TS+TS) x cols [tc*TS, tc*TS+TS) of every d x d product
-// (TS = ceil(d/4)), so each k-step loads 2 TS complex values from shared memory
-// and issues TS^2 complex FMAs.  Why: on sm_100a a shared-memory wavefront feeds
+// Mapping: one warp owns one (control vector, block) problem.  Its 32 lanes form a
+// 4 x 8 grid; lane (tr, tc) owns the TSR x TSC register tile rows tr + 4i, cols
+// tc + 8j of every d x d product (TSR = ceil(d/4), TSC = ceil(d/8)), so each k-step
+// loads TSR + TSC complex values from shared memory (the 8 lanes of a tile row read
+// 8 consecutive values in one wavefront) and issues TSR*TSC complex FMAs.  One
+// problem per warp (rather than two per warp with 4x4 tiles) doubles the warps an
+// SM can keep resident for the same shared memory, which is what hides the LDS and
+// DFMA latencies (r01: 2 problems/warp ran at 39% FP64 with ~1 warp per SMSP,
+// profiles/r01_tiny13_v2_ncu.txt).  Why tiles at all: on sm_100a a shared-memory wavefront feeds
 // 4 B per lane per clock while the FP64 pipe retires 0.5 DFMA per lane per clock,
 // so a kernel needs >= 2 complex FMAs per complex value loaded to be FP64-bound;
 // a row-per-lane mapping gets 1 (measured: LSU 67% busy, FP64 37%,
@@ -28,7 +32,10 @@ namespace sqoc {
 constexpr int kTinyMaxDim = 16;
 constexpr int kTinyBuffers = 8;   // d x d matrices per problem in shared memory
 constexpr int kMaxControls = 4;
-constexpr int kTinyLanes = 16;    // lanes per problem
+constexpr int kTinyLanes = 32;    // lanes per problem (one warp)
+constexpr int kLaneRows = 4;      // lane grid: 4 tile rows x 8 tile cols
+constexpr int kLaneCols = 8;
+constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
 
 struct TinyParams {
   int K, N, batch;
@@ -83,15 +90,16 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
 
-__device__ __forceinline__ double half_sum(double v) {  // sum over the 16 lanes of a problem (fixed tree)
+__device__ __forceinline__ double warp_sum(double v) {  // sum over the warp (one problem), fixed tree
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ double2 half_sum2(double2 v) { return make_double2(half_sum(v.x), half_sum(v.y)); }
-__device__ __forceinline__ double quad_sum(double v) {  // sum over the 4 lanes sharing a tile row (tc = 0..3)
+__device__ __forceinline__ double2 warp_sum2(double2 v) { return make_double2(warp_sum(v.x), warp_sum(v.y)); }
+__device__ __forceinline__ double row_sum(double v) {  // sum over the 8 lanes sharing a tile row (tc = 0..7)
   v += __shfl_xor_sync(0xffffffffu, v, 1);
   v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
   return v;
 }
 __device__ __forceinline__ double warp_max(double v) {
@@ -100,91 +108,91 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-// Tile helpers.  Lane (tr, tc) owns rows tr + 4i and cols tc + 4j (i, j < TS) of a D x D
-// matrix (ld D).  The interleaved ownership makes the 4 lanes of a tile row read 4
-// consecutive complex values of a matrix row in one LDS.128 wavefront (no bank conflict).
+// Tile helpers.  Lane (tr, tc) owns rows tr + 4i and cols tc + 8j of a D x D matrix
+// (ld D).  The interleaved ownership makes the 8 lanes of a tile row read 8 consecutive
+// complex values of a matrix row in one LDS.128 wavefront (no bank conflict).
 // Indices are clamped into range so padding lanes read valid memory (never stored).
-template <int D, int TS>
+template <int D, int TSR, int TSC>
 struct Tile {
   int tr, tc;
-  __device__ __forceinline__ int row(int i) const { return min(tr + 4 * i, D - 1); }
-  __device__ __forceinline__ int col(int j) const { return min(tc + 4 * j, D - 1); }
-  __device__ __forceinline__ bool ok(int i, int j) const { return tr + 4 * i < D && tc + 4 * j < D; }
-  __device__ __forceinline__ bool row_ok(int i) const { return tr + 4 * i < D; }
-  __device__ __forceinline__ int rrow(int i) const { return tr + 4 * i; }  // unclamped
-  __device__ __forceinline__ int rcol(int j) const { return tc + 4 * j; }
+  __device__ __forceinline__ int row(int i) const { return min(tr + kLaneRows * i, D - 1); }
+  __device__ __forceinline__ int col(int j) const { return min(tc + kLaneCols * j, D - 1); }
+  __device__ __forceinline__ bool ok(int i, int j) const { return tr + kLaneRows * i < D && tc + kLaneCols * j < D; }
+  __device__ __forceinline__ bool row_ok(int i) const { return tr + kLaneRows * i < D; }
+  __device__ __forceinline__ int rrow(int i) const { return tr + kLaneRows * i; }  // unclamped
+  __device__ __forceinline__ int rcol(int j) const { return tc + kLaneCols * j; }
 
-  __device__ __forceinline__ void zero(double2 (&t)[TS][TS]) const {
+  __device__ __forceinline__ void zero(double2 (&t)[TSR][TSC]) const {
 #pragma unroll
-    for (int i = 0; i < TS; ++i)
+    for (int i = 0; i < TSR; ++i)
 #pragma unroll
-      for (int j = 0; j < TS; ++j) t[i][j] = czero();
+      for (int j = 0; j < TSC; ++j) t[i][j] = czero();
   }
-  __device__ __forceinline__ void load(double2 (&t)[TS][TS], const double2* M) const {
+  __device__ __forceinline__ void load(double2 (&t)[TSR][TSC], const double2* M) const {
 #pragma unroll
-    for (int i = 0; i < TS; ++i)
+    for (int i = 0; i < TSR; ++i)
 #pragma unroll
-      for (int j = 0; j < TS; ++j) t[i][j] = M[row(i) * D + col(j)];
+      for (int j = 0; j < TSC; ++j) t[i][j] = M[row(i) * D + col(j)];
   }
-  __device__ __forceinline__ void store(double2* M, const double2 (&t)[TS][TS], bool wr) const {
+  __device__ __forceinline__ void store(double2* M, const double2 (&t)[TSR][TSC], bool wr) const {
     if (!wr) return;
 #pragma unroll
-    for (int i = 0; i < TS; ++i)
+    for (int i = 0; i < TSR; ++i)
 #pragma unroll
-      for (int j = 0; j < TS; ++j)
+      for (int j = 0; j < TSC; ++j)
         if (ok(i, j)) M[rrow(i) * D + rcol(j)] = t[i][j];
   }
   // t = L M   (L, M: D x D in smem)
-  __device__ __forceinline__ void mul(double2 (&t)[TS][TS], const double2* L, const double2* M) const {
+  __device__ __forceinline__ void mul(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
     zero(t);
 #pragma unroll 2
     for (int k = 0; k < D; ++k) {
-      double2 l[TS], m[TS];
+      double2 l[TSR], m[TSC];
 #pragma unroll
-      for (int i = 0; i < TS; ++i) l[i] = L[row(i) * D + k];
+      for (int i = 0; i < TSR; ++i) l[i] = L[row(i) * D + k];
 #pragma unroll
-      for (int j = 0; j < TS; ++j) m[j] = M[k * D + col(j)];
+      for (int j = 0; j < TSC; ++j) m[j] = M[k * D + col(j)];
 #pragma unroll
-      for (int i = 0; i < TS; ++i)
+      for (int i = 0; i < TSR; ++i)
 #pragma unroll
-        for (int j = 0; j < TS; ++j) cfma(t[i][j], l[i], m[j]);
+        for (int j = 0; j < TSC; ++j) cfma(t[i][j], l[i], m[j]);
     }
   }
   // t = U^dag M
-  __device__ __forceinline__ void mul_adj(double2 (&t)[TS][TS], const double2* U, const double2* M) const {
+  __device__ __forceinline__ void mul_adj(double2 (&t)[TSR][TSC], const double2* U, const double2* M) const {
     zero(t);
 #pragma unroll 2
     for (int k = 0; k < D; ++k) {
-      double2 l[TS], m[TS];
+      double2 l[TSR], m[TSC];
 #pragma unroll
-      for (int i = 0; i < TS; ++i) l[i] = cconj(U[k * D + row(i)]);
+      for (int i = 0; i < TSR; ++i) l[i] = cconj(U[k * D + row(i)]);
 #pragma unroll
-      for (int j = 0; j < TS; ++j) m[j] = M[k * D + col(j)];
+      for (int j = 0; j < TSC; ++j) m[j] = M[k * D + col(j)];
 #pragma unroll
-      for (int i = 0; i < TS; ++i)
+      for (int i = 0; i < TSR; ++i)
 #pragma unroll
-        for (int j = 0; j < TS; ++j) cfma(t[i][j], l[i], m[j]);
+        for (int j = 0; j < TSC; ++j) cfma(t[i][j], l[i], m[j]);
     }
   }
   // (t, dt) = (L, dL)(M, dM) = (L M, L dM + dL M)
-  __device__ __forceinline__ void pair(double2 (&t)[TS][TS], double2 (&dt)[TS][TS], const double2* L,
+  __device__ __forceinline__ void pair(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const double2* L,
                                        const double2* dL, const double2* M, const double2* dM) const {
     zero(t);
     zero(dt);
 #pragma unroll 1
     for (int k = 0; k < D; ++k) {
-      double2 l[TS], dl[TS];
+      double2 l[TSR], dl[TSR];
 #pragma unroll
-      for (int i = 0; i < TS; ++i) {
+      for (int i = 0; i < TSR; ++i) {
         l[i] = L[row(i) * D + k];
         dl[i] = dL[row(i) * D + k];
       }
 #pragma unroll
-      for (int j = 0; j < TS; ++j) {
+      for (int j = 0; j < TSC; ++j) {
         const double2 m = M[k * D + col(j)];
         const double2 dm = dM[k * D + col(j)];
 #pragma unroll
-        for (int i = 0; i < TS; ++i) {
+        for (int i = 0; i < TSR; ++i) {
           cfma(t[i][j], l[i], m);
           cfma(dt[i][j], dl[i], m);
           cfma(dt[i][j], l[i], dm);
@@ -195,9 +203,10 @@ struct Tile {
 };
 
 template <int D, bool GATE>
-__global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
+__global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyParams p) {
   constexpr int R = GATE ? D : 1;  // columns of X and Lam
-  constexpr int TS = (D + 3) / 4;  // register tile edge
+  constexpr int TSR = (D + kLaneRows - 1) / kLaneRows;  // register tile rows
+  constexpr int TSC = (D + kLaneCols - 1) / kLaneCols;  // register tile cols
   constexpr int DD = D * D;
   constexpr int PSTRIDE = kTinyBuffers * DD;
   extern __shared__ double2 smem[];
@@ -208,14 +217,13 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = lane >> 4, q = lane & 15;
-  const int tr = q >> 2, tc = q & 3;
-  Tile<D, TS> tl{tr, tc};
-  const int slot = (blockIdx.x * p.nwarps + warp) * 2 + half;  // park is sized for all slots
+  const int tr = lane / kLaneCols, tc = lane % kLaneCols;
+  Tile<D, TSR, TSC> tl{tr, tc};
+  const int slot = blockIdx.x * p.nwarps + warp;  // park is sized for all slots
   const bool real = slot < p.batch;                            // owns a real problem (may store globally)
   const int prob = real ? slot : p.batch - 1;                  // padding slots replay the last problem's u
 
-  double2* buf = gen + (K + 1) * DD + (size_t)(warp * 2 + half) * PSTRIDE;
+  double2* buf = gen + (K + 1) * DD + (size_t)warp * PSTRIDE;
   double2* B0 = buf;      // X (fwd) | X, A2 (bwd)
   double2* B1 = B0 + DD;  // A2 (fwd) | Lam, dA2 (bwd)
   double2* B2 = B1 + DD;  // A
@@ -229,16 +237,16 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
   double2* parkL = parkX + D * R;
 
   // ---- A tile for slice j (scaled by 2^-s), warp-uniform Taylor plan ----
-  auto build_a = [&](int j, double2 (&a)[TS][TS], int& nb, int& s) {
+  auto build_a = [&](int j, double2 (&a)[TSR][TSC], int& nb, int& s) {
     double uk[kMaxControls];
 #pragma unroll
     for (int k = 0; k < kMaxControls; ++k) uk[k] = (k < K) ? up[k * N + j] : 0.0;
-    double rowsum[TS];
+    double rowsum[TSR];
 #pragma unroll
-    for (int i = 0; i < TS; ++i) {
+    for (int i = 0; i < TSR; ++i) {
       rowsum[i] = 0.0;
 #pragma unroll
-      for (int jj = 0; jj < TS; ++jj) {
+      for (int jj = 0; jj < TSC; ++jj) {
         const int o = tl.row(i) * D + tl.col(jj);
         double2 v = gen[o];
         for (int k = 0; k < K; ++k) {
@@ -252,70 +260,70 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
     }
     double nrm = 0.0;
 #pragma unroll
-    for (int i = 0; i < TS; ++i) nrm = fmax(nrm, quad_sum(rowsum[i]));
+    for (int i = 0; i < TSR; ++i) nrm = fmax(nrm, row_sum(rowsum[i]));
     nrm = warp_max(real ? nrm : 0.0);  // plan is warp-uniform, from real problems only
     choose_taylor(nrm, nb, s);
     const double sc = ldexp(1.0, -s);
 #pragma unroll
-    for (int i = 0; i < TS; ++i)
+    for (int i = 0; i < TSR; ++i)
 #pragma unroll
-      for (int jj = 0; jj < TS; ++jj) a[i][jj] = cscale(a[i][jj], sc);
+      for (int jj = 0; jj < TSC; ++jj) a[i][jj] = cscale(a[i][jj], sc);
   };
 
   // Q_t tile: c_{3t} I + c_{3t+1} A + c_{3t+2} A2 ; dQ_t: c_{3t+1} dA + c_{3t+2} dA2
-  auto add_q = [&](double2 (&t)[TS][TS], int qi, const double2* A, const double2* A2) {
+  auto add_q = [&](double2 (&t)[TSR][TSC], int qi, const double2* A, const double2* A2) {
 #pragma unroll
-    for (int i = 0; i < TS; ++i)
+    for (int i = 0; i < TSR; ++i)
 #pragma unroll
-      for (int jj = 0; jj < TS; ++jj) {
+      for (int jj = 0; jj < TSC; ++jj) {
         const int o = tl.row(i) * D + tl.col(jj);
         t[i][jj] = cadd(t[i][jj], cadd(cscale(A[o], c_inv_fact[3 * qi + 1]), cscale(A2[o], c_inv_fact[3 * qi + 2])));
         if (tl.rrow(i) == tl.rcol(jj)) t[i][jj].x += c_inv_fact[3 * qi];
       }
   };
-  auto add_dq = [&](double2 (&t)[TS][TS], int qi, const double2* dA, const double2* dA2) {
+  auto add_dq = [&](double2 (&t)[TSR][TSC], int qi, const double2* dA, const double2* dA2) {
 #pragma unroll
-    for (int i = 0; i < TS; ++i)
+    for (int i = 0; i < TSR; ++i)
 #pragma unroll
-      for (int jj = 0; jj < TS; ++jj) {
+      for (int jj = 0; jj < TSC; ++jj) {
         const int o = tl.row(i) * D + tl.col(jj);
         t[i][jj] = cadd(t[i][jj], cadd(cscale(dA[o], c_inv_fact[3 * qi + 1]), cscale(dA2[o], c_inv_fact[3 * qi + 2])));
       }
   };
-  auto scale_tile = [&](double2 (&t)[TS][TS], double c) {
+  auto scale_tile = [&](double2 (&t)[TSR][TSC], double c) {
 #pragma unroll
-    for (int i = 0; i < TS; ++i)
+    for (int i = 0; i < TSR; ++i)
 #pragma unroll
-      for (int jj = 0; jj < TS; ++jj) t[i][jj] = cscale(t[i][jj], c);
+      for (int jj = 0; jj < TSC; ++jj) t[i][jj] = cscale(t[i][jj], c);
   };
 
   // ---- X-shaped products (R columns): gate -> tiles; state -> one column, k split over tc ----
   // out = Op(U) Y where Op(U) = U (adj=false) or U^dag (adj=true); Y: D x R; store into Yout (may alias Y)
   auto mul_x = [&](const double2* U, bool adj, const double2* Y, double2* Yout) {
     if (GATE) {
-      double2 t[TS][TS];
+      double2 t[TSR][TSC];
       if (adj) tl.mul_adj(t, U, Y);
       else tl.mul(t, U, Y);
       __syncwarp();
       tl.store(Yout, t, true);  // park is sized for every slot, padding slots included
     } else {
-      double2 v[TS];
+      double2 v[TSR];
 #pragma unroll
-      for (int i = 0; i < TS; ++i) v[i] = czero();
-      for (int k = tc; k < D; k += 4) {
+      for (int i = 0; i < TSR; ++i) v[i] = czero();
+      for (int k = tc; k < D; k += kLaneCols) {
         const double2 y = Y[k];
 #pragma unroll
-        for (int i = 0; i < TS; ++i) {
+        for (int i = 0; i < TSR; ++i) {
           const double2 l = adj ? cconj(U[k * D + tl.row(i)]) : U[tl.row(i) * D + k];
           cfma(v[i], l, y);
         }
       }
 #pragma unroll
-      for (int i = 0; i < TS; ++i) v[i] = make_double2(quad_sum(v[i].x), quad_sum(v[i].y));
+      for (int i = 0; i < TSR; ++i) v[i] = make_double2(row_sum(v[i].x), row_sum(v[i].y));
       __syncwarp();
       if (tc == 0) {
 #pragma unroll
-        for (int i = 0; i < TS; ++i)
+        for (int i = 0; i < TSR; ++i)
           if (tl.row_ok(i)) Yout[tl.rrow(i)] = v[i];
       }
     }
@@ -325,25 +333,25 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
     if (!wr) return;
     if (GATE) {
 #pragma unroll
-      for (int i = 0; i < TS; ++i)
+      for (int i = 0; i < TSR; ++i)
 #pragma unroll
-        for (int jj = 0; jj < TS; ++jj)
+        for (int jj = 0; jj < TSC; ++jj)
           if (tl.ok(i, jj)) dst[tl.rrow(i) * D + tl.rcol(jj)] = src[tl.rrow(i) * D + tl.rcol(jj)];
     } else if (tc == 0) {
 #pragma unroll
-      for (int i = 0; i < TS; ++i)
+      for (int i = 0; i < TSR; ++i)
         if (tl.row_ok(i)) dst[tl.rrow(i)] = src[tl.rrow(i)];
     }
   };
 
-  double2 t[TS][TS], dt[TS][TS];
+  double2 t[TSR][TSC], dt[TSR][TSC];
   // ================= forward sweep: X_N =================
   double2* X = B0;
   if (GATE) {
 #pragma unroll
-    for (int i = 0; i < TS; ++i)
+    for (int i = 0; i < TSR; ++i)
 #pragma unroll
-      for (int jj = 0; jj < TS; ++jj) t[i][jj] = make_double2(tl.rrow(i) == tl.rcol(jj) ? 1.0 : 0.0, 0.0);
+      for (int jj = 0; jj < TSC; ++jj) t[i][jj] = make_double2(tl.rrow(i) == tl.rcol(jj) ? 1.0 : 0.0, 0.0);
     tl.store(X, t, true);
   } else {
     copy_x(X, p.x0, true);
@@ -384,20 +392,20 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
   double2 part = czero();
   if (GATE) {
 #pragma unroll
-    for (int i = 0; i < TS; ++i)
+    for (int i = 0; i < TSR; ++i)
 #pragma unroll
-      for (int jj = 0; jj < TS; ++jj)
+      for (int jj = 0; jj < TSC; ++jj)
         if (tl.ok(i, jj)) {
           const int o = tl.rrow(i) * D + tl.rcol(jj);
           part = cadd(part, cmul(cconj(p.target[o]), X[o]));
         }
   } else if (tc == 0) {
 #pragma unroll
-    for (int i = 0; i < TS; ++i)
+    for (int i = 0; i < TSR; ++i)
       if (tl.row_ok(i)) part = cadd(part, cmul(cconj(p.target[tl.rrow(i)]), X[tl.rrow(i)]));
   }
-  const double2 tau = half_sum2(part);
-  if (real && q == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
+  const double2 tau = warp_sum2(part);
+  if (real && lane == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
   copy_x(parkX, X, true);
   copy_x(parkL, p.target, true);
   __syncwarp();
@@ -416,15 +424,15 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
       tl.zero(t);
 #pragma unroll 1
       for (int k = 0; k < R; ++k) {
-        double2 l[TS], m[TS];
+        double2 l[TSR], m[TSC];
 #pragma unroll
-        for (int i = 0; i < TS; ++i) l[i] = B0[tl.row(i) * R + k];
+        for (int i = 0; i < TSR; ++i) l[i] = B0[tl.row(i) * R + k];
 #pragma unroll
-        for (int jj = 0; jj < TS; ++jj) m[jj] = cconj(B1[tl.col(jj) * R + k]);
+        for (int jj = 0; jj < TSC; ++jj) m[jj] = cconj(B1[tl.col(jj) * R + k]);
 #pragma unroll
-        for (int i = 0; i < TS; ++i)
+        for (int i = 0; i < TSR; ++i)
 #pragma unroll
-          for (int jj = 0; jj < TS; ++jj) cfma(t[i][jj], l[i], m[jj]);
+          for (int jj = 0; jj < TSC; ++jj) cfma(t[i][jj], l[i], m[jj]);
       }
       scale_tile(t, sc);
       tl.store(B3, t, true);
@@ -470,12 +478,12 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
       const double2* E = gen + (k + 1) * DD;
       double2 pk = czero();
 #pragma unroll
-      for (int i = 0; i < TS; ++i)
+      for (int i = 0; i < TSR; ++i)
 #pragma unroll
-        for (int jj = 0; jj < TS; ++jj)
+        for (int jj = 0; jj < TSC; ++jj)
           if (tl.ok(i, jj)) cfma(pk, t[i][jj], E[tl.rcol(jj) * D + tl.rrow(i)]);
-      const double2 dtau = half_sum2(pk);
-      if (real && q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau.x - ctw.y * dtau.y;
+      const double2 dtau = warp_sum2(pk);
+      if (real && lane == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau.x - ctw.y * dtau.y;
     }
     // X_{j-1} = U^dag X_j, Lam_{j-1} = U^dag Lam_j  -> park (global, own entries)
     mul_x(B6, true, B0, parkX);
@@ -485,7 +493,7 @@ __global__ void __launch_bounds__(256) grape_tiny_kernel(TinyParams p) {
 }
 
 inline size_t tiny_smem_bytes(int d, int K, int nwarps) {
-  return sizeof(double2) * ((size_t)(K + 1) * d * d + (size_t)nwarps * 2 * kTinyBuffers * d * d);
+  return sizeof(double2) * ((size_t)(K + 1) * d * d + (size_t)nwarps * kTinyBuffers * d * d);
 }
 
 }  // namespace sqoc
