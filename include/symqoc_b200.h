@@ -107,6 +107,11 @@ int sqoc_chunk_product(sqoc_problem* p, const double* u, double* const* out, int
 int sqoc_eval_chunk(sqoc_problem* p, const double* u, const double* const* x_start, const double* const* lam_end,
                     const double* tau, double* F, double* grad, int memory, void* stream);
 
+/* Complex GEMM algorithm of the large-block path (process-wide): 3 = Gauss/3M (three
+ * real DMMA products per complex product, default), 4 = 4M (four).  Both are exact
+ * algorithms; 3M rounds slightly differently (still ~1e-15 relative). */
+int sqoc_set_complex_gemm(int mults);
+
 /* Free all device memory of the problem. */
 int sqoc_destroy(sqoc_problem* p);
 

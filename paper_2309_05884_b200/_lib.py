@@ -37,6 +37,7 @@ SIGNATURES = {
     "sqoc_state_gradient": (_I, [_I, _I, _D, _D, _D, _D, _D, _D, _D, _I, ctypes.c_double, _D, _D, _D]),
     "sqoc_last_launch_count": (_I, [_P]),
     "sqoc_set_timing": (_I, [_P, _I]),
+    "sqoc_set_complex_gemm": (_I, [_I]),
     "sqoc_set_schedule": (_I, [_P, _I]),
     "sqoc_last_schedule": (_I, [_P]),
     "sqoc_last_plan": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),

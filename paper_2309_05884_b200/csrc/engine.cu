@@ -554,6 +554,11 @@ int sqoc_last_plan(const sqoc_problem* p, int* taylor_blocks, int* squarings, in
   return SQOC_OK;
 }
 
+int sqoc_set_complex_gemm(int mults) {
+  if (large_set_complex_gemm(mults) != SQOC_OK) return fail(SQOC_ERR_ARG, "mults must be 3 or 4");
+  return SQOC_OK;
+}
+
 int sqoc_set_timing(sqoc_problem* p, int on) {
   if (!p) return fail(SQOC_ERR_ARG, "problem is NULL");
   p->timing = on != 0;

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../../include/symqoc_b200.h"
 #include "large.cuh"
@@ -333,6 +334,23 @@ __global__ void sv_dot_kernel(int K, int N, int nblk, const int* __restrict__ di
 }
 
 // ------------------------------------------------------------------ host side
+// Complex product algorithm for the large path: 3M (Gauss, 3 DMMAs per complex k-step) by
+// default, 4M with SQOC_GEMM_4M=1 in the environment (checked once per process).
+static int g_gemm_mode = -1;  // -1 unset, 3 or 4
+static bool use_3m() {
+  if (g_gemm_mode < 0) {
+    const char* e = getenv("SQOC_GEMM_4M");
+    g_gemm_mode = (e && e[0] == '1') ? 4 : 3;
+  }
+  return g_gemm_mode == 3;
+}
+
+int large_set_complex_gemm(int mults) {
+  if (mults != 3 && mults != 4) return SQOC_ERR_ARG;
+  g_gemm_mode = mults;
+  return SQOC_OK;
+}
+
 template <int TA, int TB, int EPI>
 static cudaError_t launch_gemm(const GemmItem* items, int n, int tiles, GemmArgs a, cudaStream_t st) {
   static bool attr = false;
@@ -340,9 +358,12 @@ static cudaError_t launch_gemm(const GemmItem* items, int n, int tiles, GemmArgs
     cudaError_t e = cudaFuncSetAttribute(zgemm_kernel<TA, TB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)G_SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(zgemm3m_kernel<TA, TB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+    if (e != cudaSuccess) return e;
     attr = true;
   }
-  zgemm_kernel<TA, TB, EPI><<<tiles, GTHREADS, G_SMEM, st>>>(items, n, a);
+  if (use_3m()) zgemm3m_kernel<TA, TB, EPI><<<tiles, G3THREADS, G_SMEM, st>>>(items, n, a);
+  else zgemm_kernel<TA, TB, EPI><<<tiles, GTHREADS, G_SMEM, st>>>(items, n, a);
   return cudaGetLastError();
 }
 

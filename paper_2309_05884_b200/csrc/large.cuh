@@ -117,6 +117,7 @@ struct LargeGroup {
 int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, int N, bool gate);
 int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st);
 int large_set_norms(LargeGroup& g, const std::vector<double>& gnorm);
+int large_set_complex_gemm(int mults);
 void large_free(LargeGroup& g);
 
 }  // namespace sqoc

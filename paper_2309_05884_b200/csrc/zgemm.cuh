@@ -64,13 +64,13 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 // Load one K-step (GBK) of op(A) (rows m0.., k0..) and op(B) (k0.., cols n0..) into a stage.
-template <int TA, int TB>
+template <int TA, int TB, int NT = GTHREADS>
 __device__ __forceinline__ void gemm_load_stage(double2* sA, double2* sB, const double2* A, const double2* B,
                                                 const GemmItem& it, int m0, int n0, int k0) {
   const int tid = threadIdx.x;
 #pragma unroll
-  for (int r = 0; r < (GBM * GBK) / GTHREADS; ++r) {
-    const int i = tid + r * GTHREADS;
+  for (int r = 0; r < (GBM * GBK) / NT; ++r) {
+    const int i = tid + r * NT;
     if (TA == OP_N) {  // A[m][k] row-major; smem [m][k]
       const int row = i / GBK, col = i % GBK;
       const int gm = m0 + row, gk = k0 + col;
@@ -233,6 +233,155 @@ __global__ void __launch_bounds__(GTHREADS) zgemm_kernel(const GemmItem* __restr
     if (threadIdx.x < it.nF) {
       double2 s = make_double2(0.0, 0.0);
       for (int w = 0; w < GTHREADS / 32; ++w) { s.x += red[w][threadIdx.x].x; s.y += red[w][threadIdx.x].y; }
+      it.tr_out[(size_t)local * it.nF + threadIdx.x] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3M (Gauss) variant: T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi);
+// C = (T1 - T2) + i (T3 - T1 - T2).  Three DMMAs per complex k-step instead of four
+// (the complex FLOP count of the algorithm stays 8 d^3 by convention; the FP64 pipe
+// executes 6 d^3).  8 warps per CTA (2 x 4), warp tile 32 x 16 (4 x 2 DMMA tiles),
+// so the three accumulator sets fit in registers.
+constexpr int G3THREADS = 256;
+
+template <int TA, int TB, int EPI>
+__global__ void __launch_bounds__(G3THREADS, 2) zgemm3m_kernel(const GemmItem* __restrict__ items, int nitems,
+                                                               GemmArgs args) {
+  extern __shared__ double2 gsm[];
+  int lo = 0, hi = nitems - 1;
+  const int tile = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (items[mid].tile_start <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmItem it = items[lo];
+  const int local = tile - it.tile_start;
+  const int m0 = (local / it.tiles_n) * GBM;
+  const int n0 = (local % it.tiles_n) * GBN;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+  const int lr = lane >> 2, lc = lane & 3;
+
+  double acc[4][2][3][2];  // [mi][ni][T1,T2,T3][c0,c1]
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
+
+  const int kt_per_seg = (it.k + GBK - 1) / GBK;
+  const int kt_total = kt_per_seg * it.nseg;
+  double2* sAbase = gsm;
+  double2* sBbase = gsm + GSTAGES * G_A_ELEMS;
+
+  auto issue = [&](int kt) {
+    if (kt < kt_total) {
+      const int seg = kt / kt_per_seg;
+      const int k0 = (kt - seg * kt_per_seg) * GBK;
+      const int st = kt % GSTAGES;
+      gemm_load_stage<TA, TB, G3THREADS>(sAbase + st * G_A_ELEMS, sBbase + st * G_A_ELEMS, seg ? it.A1 : it.A0,
+                                         seg ? it.B1 : it.B0, it, m0, n0, k0);
+    }
+    cp_async_commit();
+  };
+
+#pragma unroll
+  for (int s = 0; s < GSTAGES - 1; ++s) issue(s);
+
+  for (int kt = 0; kt < kt_total; ++kt) {
+    cp_async_wait<GSTAGES - 2>();
+    __syncthreads();
+    issue(kt + GSTAGES - 1);
+    const int st = kt % GSTAGES;
+    const double2* sA = sAbase + st * G_A_ELEMS;
+    const double2* sB = sBbase + st * G_A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < GBK; kk += 4) {
+      double ar[4], ai[4], as[4], br[2], bi[2], bs[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int m = wm + mi * 8 + lr, k = kk + lc;
+        double2 a;
+        if (TA == OP_N) a = sA[m * LD_KMAJ + k];
+        else { a = sA[k * LD_NMAJ + m]; a.y = -a.y; }
+        ar[mi] = a.x; ai[mi] = a.y; as[mi] = a.x + a.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) {
+        const int n = wn + ni * 8 + lr, k = kk + lc;
+        double2 b;
+        if (TB == OP_N) b = sB[k * LD_NMAJ + n];
+        else { b = sB[n * LD_KMAJ + k]; b.y = -b.y; }
+        br[ni] = b.x; bi[ni] = b.y; bs[ni] = b.x + b.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          dmma(acc[mi][ni][0][0], acc[mi][ni][0][1], ar[mi], br[ni]);
+          dmma(acc[mi][ni][1][0], acc[mi][ni][1][1], ai[mi], bi[ni]);
+          dmma(acc[mi][ni][2][0], acc[mi][ni][2][1], as[mi], bs[ni]);
+        }
+    }
+  }
+  cp_async_wait<0>();
+
+  if (EPI == EPI_STORE) {
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int m = m0 + wm + mi * 8 + lr;
+          const int n = n0 + wn + ni * 8 + 2 * lc + v;
+          if (m < it.m && n < it.n) {
+            const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
+            double2 c = make_double2(args.alpha * (t1 - t2), args.alpha * (t3 - t1 - t2));
+            const size_t off = (size_t)m * it.ldc + n;
+            if (it.E0) { const double2 e = it.E0[off]; c.x += args.beta0 * e.x; c.y += args.beta0 * e.y; }
+            if (it.E1) { const double2 e = it.E1[off]; c.x += args.beta1 * e.x; c.y += args.beta1 * e.y; }
+            if (it.diag && m == n) c.x += args.gamma;
+            it.C[off] = c;
+          }
+        }
+  } else {
+    __shared__ double2 red[G3THREADS / 32][4];
+    for (int f = 0; f < it.nF; ++f) {
+      const double2* F = it.F + f * it.fstride;
+      double sx = 0.0, sy = 0.0;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int p = m0 + wm + mi * 8 + lr;
+            const int q = n0 + wn + ni * 8 + 2 * lc + v;
+            if (p < it.m && q < it.n) {
+              const double2 e = F[(size_t)q * it.ldc + p];
+              const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
+              const double cr = args.alpha * (t1 - t2), ci = args.alpha * (t3 - t1 - t2);
+              sx += cr * e.x - ci * e.y;
+              sy += cr * e.y + ci * e.x;
+            }
+          }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      }
+      if (lane == 0) red[warp][f] = make_double2(sx, sy);
+    }
+    __syncthreads();
+    if (threadIdx.x < it.nF) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int w = 0; w < G3THREADS / 32; ++w) { s.x += red[w][threadIdx.x].x; s.y += red[w][threadIdx.x].y; }
       it.tr_out[(size_t)local * it.nF + threadIdx.x] = s;
     }
   }

@@ -130,3 +130,23 @@ def test_slice_chunk_sharding_emulated_on_one_gpu(world):
         F, g = parallel.emulate_ranks(s, world, lambda sys_: GrapeEngine(sys_, max_batch=1), u)
         assert abs(F - F0) <= F_TOL
         assert rel(g, g0) <= G_TOL
+
+
+@pytest.mark.parametrize("mults", [4, 3])
+def test_complex_gemm_algorithms_against_oracle(mults):
+    from paper_2309_05884_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.sqoc_set_complex_gemm(mults) == 0
+    try:
+        s = systems.config(2, n_slices=16)
+        u = s.controls(12)
+        for sched in ("sequential", "history"):
+            eng = GrapeEngine(s, max_batch=1)
+            eng.set_schedule(sched)
+            F, g = eng.objective(u)
+            Fo, go, _ = O.objective(s, u)
+            assert abs(F - Fo) <= F_TOL
+            assert rel(g, go) <= G_TOL
+    finally:
+        lib.sqoc_set_complex_gemm(3)
