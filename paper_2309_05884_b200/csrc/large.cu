@@ -646,7 +646,7 @@ static int bc_tau(LargeGroup& g, const double2* XN, const LargeArgs& a, int s_id
 }
 
 // ------------------------------------------------------------------ history schedule
-enum HOp { H_A2, H_A3, H_H, H_S, H_X, H_L, H_B, H_DA2, H_DA3, H_DH, H_DS };
+enum HOp { H_A2, H_A3, H_H, H_S, H_X, H_L, H_B, H_DA2, H_DA3, H_DH, H_DS, H_XP1, H_XP2, H_XP3, H_LP1, H_LP2, H_LP3 };
 
 static size_t history_bytes(const LargeGroup& g, int C) {
   const size_t N = g.N;
@@ -654,9 +654,9 @@ static size_t history_bytes(const LargeGroup& g, int C) {
 }
 
 static void hist_free(LargeGroup& g) {
-  double2* hb[] = {g.h_chain, g.h_X, g.h_L, g.h_dA, g.h_dA2, g.h_dA3, g.h_dH[0], g.h_dH[1], g.h_g};
+  double2* hb[] = {g.h_chain, g.h_X, g.h_L, g.h_dA, g.h_dA2, g.h_dA3, g.h_dH[0], g.h_dH[1], g.h_g, g.h_I};
   for (auto x : hb) cudaFree(x);
-  g.h_chain = g.h_X = g.h_L = g.h_dA = g.h_dA2 = g.h_dA3 = g.h_dH[0] = g.h_dH[1] = g.h_g = nullptr;
+  g.h_chain = g.h_X = g.h_L = g.h_dA = g.h_dA2 = g.h_dA3 = g.h_dH[0] = g.h_dH[1] = g.h_g = g.h_I = nullptr;
   for (auto m : g.hlist_mem) cudaFree(m);
   g.hlist_mem.clear();
   g.hlists.clear();
@@ -676,6 +676,13 @@ static int hist_alloc(LargeGroup& g, int nb, int sq) {
   double2** d5[] = {&g.h_dA, &g.h_dA2, &g.h_dA3, &g.h_dH[0], &g.h_dH[1]};
   for (auto pp : d5) LCHK(cudaMalloc(pp, sq_bytes));
   LCHK(cudaMalloc(&g.h_g, N * g.nblk * g.K * sizeof(double2)));
+  if (g.gate) {  // identity blocks for the chunked prefix / suffix scans
+    std::vector<double2> eye(g.totalr, make_double2(0.0, 0.0));
+    for (int b = 0; b < g.nblk; ++b)
+      for (int r = 0; r < g.blocks[b].d; ++r) eye[g.offr[b] + (size_t)r * g.blocks[b].d + r] = make_double2(1.0, 0.0);
+    LCHK(cudaMalloc(&g.h_I, g.totalr * sizeof(double2)));
+    LCHK(cudaMemcpy(g.h_I, eye.data(), g.totalr * sizeof(double2), cudaMemcpyHostToDevice));
+  }
   g.h_C = C;
   return SQOC_OK;
 }
@@ -751,6 +758,118 @@ static int hgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArgs
   return SQOC_OK;
 }
 
+// Chunked prefix / suffix scans of the X / Lam recurrences (gate): depth ~2 sqrt(N)
+// launches instead of N, each batched over chunks x blocks.  Lc = chunk length.
+//   X: chunk 0 runs exactly from X_0; chunks c >= 1 form local prefixes P_i = U_i ... U_{cLc}
+//      (into h_dA2), the chunk starts X[cLc] = P_{cLc-1} X[(c-1)Lc] are carried sequentially,
+//      and X[i+1] = P_i X[cLc] fixes every slice up in one launch.
+//   Lam: the mirror image with local suffixes Q_i = U_i^dag ... U_{(c+1)Lc-1}^dag (into h_dA3).
+static ListRef scan_list(LargeGroup& g, int op, int idx, int Lc, int C) {
+  auto key = std::make_tuple(op * 1000000 + idx * 4, g.h_nb * 100 + g.h_s, Lc, C);
+  auto it = g.hlists.find(key);
+  if (it != g.hlists.end()) return it->second;
+  const int N = g.N, nb = g.h_nb;
+  std::vector<GemmItem> v;
+  auto U = [&](int i, int b) { return g.h_chain + ((size_t)(3 + nb + g.h_s - 1) * N + i) * g.total + g.off[b]; };
+  auto X = [&](int i, int b) { return g.h_X + (size_t)i * g.totalr + g.offr[b]; };
+  auto L = [&](int i, int b) { return g.h_L + (size_t)i * g.totalr + g.offr[b]; };
+  auto P = [&](int i, int b) { return g.h_dA2 + (size_t)i * g.total + g.off[b]; };
+  auto Q = [&](int i, int b) { return g.h_dA3 + (size_t)i * g.total + g.off[b]; };
+  auto I = [&](int b) { return g.h_I + g.offr[b]; };
+  for (int b = 0; b < g.nblk; ++b) {
+    const int d = g.blocks[b].d;
+    auto add = [&](const double2* A, const double2* B, double2* Cm) {
+      v.push_back(mk(A, B, 0, 0, Cm, 0, 0, d, d, d, 1, d, d, d, 0));
+    };
+    switch (op) {
+      case H_XP1:  // step t = idx of every chunk
+        for (int c = 0; c < C; ++c) {
+          const int i = c * Lc + idx;
+          if (i >= N || idx >= Lc) continue;
+          if (c == 0) add(U(i, b), X(i, b), X(i + 1, b));
+          else add(U(i, b), idx == 0 ? I(b) : P(i - 1, b), P(i, b));
+        }
+        break;
+      case H_XP2:  // carry into chunk idx (>= 2)
+        add(P(idx * Lc - 1, b), X((idx - 1) * Lc, b), X(idx * Lc, b));
+        break;
+      case H_XP3:  // fix-up of chunks >= 1
+        for (int c = 1; c < C; ++c)
+          for (int i = c * Lc; i < std::min((c + 1) * Lc, N); ++i) add(P(i, b), X(c * Lc, b), X(i + 1, b));
+        break;
+      case H_LP1:  // step t = idx from each chunk's end
+        for (int c = 0; c < C; ++c) {
+          const int end = std::min((c + 1) * Lc, N);
+          const int i = end - 1 - idx;
+          if (i < c * Lc) continue;
+          if (c == C - 1) v.push_back(mk(U(i, b), L(i + 1, b), 0, 0, L(i, b), 0, 0, d, d, d, 1, d, d, d, 0));
+          else v.push_back(mk(U(i, b), idx == 0 ? I(b) : Q(i + 1, b), 0, 0, Q(i, b), 0, 0, d, d, d, 1, d, d, d, 0));
+        }
+        break;
+      case H_LP2:  // carry: Lam at the start of chunk idx (<= C-2)
+        add(Q(idx * Lc, b), L((idx + 1) * Lc, b), L(idx * Lc, b));
+        break;
+      case H_LP3:  // fix-up of chunks <= C-2
+        for (int c = 0; c < C - 1; ++c)
+          for (int i = c * Lc + 1; i < (c + 1) * Lc; ++i) add(Q(i, b), L((c + 1) * Lc, b), L(i, b));
+        break;
+    }
+  }
+  int t = 0;
+  for (auto& x : v) {
+    x.tile_start = t;
+    t += tiles_of(x.m, x.n);
+  }
+  ListRef ref;
+  if (v.empty()) {
+    g.hlists[key] = ref;
+    return ref;
+  }
+  if (cudaMalloc(&ref.dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return ListRef{};
+  cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
+  ref.n = (int)v.size();
+  ref.tiles = t;
+  g.hlist_mem.push_back(ref.dev);
+  g.hlists[key] = ref;
+  return ref;
+}
+
+static int scan_gemm(LargeGroup& g, int op, int idx, int Lc, int C, cudaStream_t st) {
+  ListRef l = scan_list(g, op, idx, Lc, C);
+  if (!l.n) return SQOC_OK;
+  const GemmArgs one{1.0, 0.0, 0.0, 0.0};
+  cudaError_t e = (op == H_LP1) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, one, st)
+                                : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, one, st);
+  if (e != cudaSuccess) {
+    g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
+    return SQOC_ERR_CUDA;
+  }
+  g.launches++;
+  return SQOC_OK;
+}
+
+static int history_scans(LargeGroup& g, bool do_x, bool do_l, cudaStream_t st) {
+  const int N = g.N;
+  const int Lc = std::max(1, (int)std::ceil(std::sqrt((double)N)));
+  const int C = (N + Lc - 1) / Lc;
+  int rc;
+  if (do_x) {
+    for (int t = 0; t < Lc; ++t)
+      if ((rc = scan_gemm(g, H_XP1, t, Lc, C, st))) return rc;
+    for (int c = 2; c < C; ++c)
+      if ((rc = scan_gemm(g, H_XP2, c, Lc, C, st))) return rc;
+    if ((rc = scan_gemm(g, H_XP3, 0, Lc, C, st))) return rc;
+  }
+  if (do_l) {
+    for (int t = 0; t < Lc; ++t)
+      if ((rc = scan_gemm(g, H_LP1, t, Lc, C, st))) return rc;
+    for (int c = C - 2; c >= 0; --c)
+      if ((rc = scan_gemm(g, H_LP2, c, Lc, C, st))) return rc;
+    if ((rc = scan_gemm(g, H_LP3, 0, Lc, C, st))) return rc;
+  }
+  return SQOC_OK;
+}
+
 static int large_eval_history(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, int nb, int sq,
                               cudaStream_t st) {
   const int K = g.K, N = g.N, nblk = g.nblk;
@@ -788,13 +907,22 @@ static int large_eval_history(LargeGroup& g, const LargeArgs& a, int s_idx, cons
   // ---- forward / backward recurrences (sequential over slices, batched over blocks) ----
   const dim3 ew_grid(ew_x, nblk);
   if ((rc = bc_init(g, g.h_X, g.h_L + (size_t)N * g.totalr, ew_grid, st))) return rc;
-  for (int i = 0; i < N; ++i)
-    if ((rc = hgemm(g, H_X, 0, 0, i, i + 1, one, st))) return rc;
+  const bool chunked = g.gate && N >= 64 && g.h_I != nullptr;  // chunked scans (gate: d x d recurrences)
+  if (chunked) {
+    if ((rc = history_scans(g, true, false, st))) return rc;
+  } else {
+    for (int i = 0; i < N; ++i)
+      if ((rc = hgemm(g, H_X, 0, 0, i, i + 1, one, st))) return rc;
+  }
   bool done = false;
   if ((rc = bc_tau(g, g.h_X + (size_t)N * g.totalr, a, s_idx, st, &done))) return rc;
   if (done) return SQOC_OK;
-  for (int i = N - 1; i >= 0; --i)
-    if ((rc = hgemm(g, H_L, 0, 0, i, i + 1, one, st))) return rc;
+  if (chunked) {
+    if ((rc = history_scans(g, false, true, st))) return rc;
+  } else {
+    for (int i = N - 1; i >= 0; --i)
+      if ((rc = hgemm(g, H_L, 0, 0, i, i + 1, one, st))) return rc;
+  }
   // ---- Frechet derivatives of every slice: L_R(A_i, X_i Lam_{i+1}^dag), derivative-only chain ----
   if ((rc = hgemm(g, H_B, 0, 0, 0, N, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
   if ((rc = hgemm(g, H_DA2, 0, 0, 0, N, one, st))) return rc;

@@ -85,6 +85,7 @@ struct LargeGroup {
   double2* h_L = nullptr;           // [N+1][totalr]
   double2 *h_dA = nullptr, *h_dA2 = nullptr, *h_dA3 = nullptr, *h_dH[2] = {nullptr, nullptr};  // [N][total]
   double2* h_g = nullptr;           // [N][nblk][K] traces
+  double2* h_I = nullptr;           // [totalr] identity per block (chunked scans)
   const double2** gent_dev = nullptr;  // per block a_k^T (K d*d), for the slice traces
   std::vector<void*> gent_mem;
   std::map<std::tuple<int, int, int, int>, ListRef> hlists;

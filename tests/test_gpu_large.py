@@ -150,3 +150,15 @@ def test_complex_gemm_algorithms_against_oracle(mults):
             assert rel(g, go) <= G_TOL
     finally:
         lib.sqoc_set_complex_gemm(3)
+
+
+def test_history_chunked_scans_against_oracle():
+    """N >= 64 switches the history schedule's X / Lam recurrences to chunked scans."""
+    s = systems.config(2, n_slices=70)
+    eng = GrapeEngine(s, max_batch=1)
+    eng.set_schedule("history")
+    u = s.controls(21)
+    F, g = eng.objective(u)
+    Fo, go, _ = O.objective(s, u)
+    assert abs(F - Fo) <= F_TOL
+    assert rel(g, go) <= G_TOL
