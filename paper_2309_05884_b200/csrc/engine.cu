@@ -128,7 +128,7 @@ static int launch_tiny(int d, const TinyParams& tp, int grid, int nwarps, size_t
 }
 
 static int choose_nwarps(int d, int K, int batch) {
-  const int pg = 32 / kTinyLanes;
+  const int pg = 32 / tiny_lanes(d);
   const int need = (batch + pg - 1) / pg;
   int nw = kTinyMaxWarps;
   while (nw > 1 && tiny_smem_bytes(d, K, nw) > kMaxSmem) --nw;
@@ -250,7 +250,7 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
     chk(cudaEventCreate(&bp.t1), "event");
     if (bp.tiny) {
       const int R = objective == SQOC_OBJ_GATE ? d : 1;
-      const int pg = 32 / kTinyLanes;
+      const int pg = 32 / tiny_lanes(d);
       bp.nwarps = choose_nwarps(d, n_controls, max_batch);
       const int per_cta = pg * bp.nwarps;
       bp.park_slots = (size_t)((max_batch + per_cta - 1) / per_cta) * per_cta;
@@ -356,7 +356,7 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
       tp.tau_stride = p->nblocks;
       tp.grad_out = gout;
       tp.park = bp.park;
-      const int pg = 32 / kTinyLanes;
+      const int pg = 32 / tiny_lanes(bp.d);
       int nw = std::max(1, std::min(bp.nwarps, (batch + pg - 1) / pg));
       tp.nwarps = nw;
       const int grid = (batch + pg * nw - 1) / (pg * nw);

@@ -32,9 +32,12 @@ namespace sqoc {
 constexpr int kTinyMaxDim = 16;
 constexpr int kTinyBuffers = 8;   // d x d matrices per problem in shared memory
 constexpr int kMaxControls = 4;
-constexpr int kTinyLanes = 32;    // lanes per problem (one warp)
-constexpr int kLaneRows = 4;      // lane grid: 4 tile rows x 8 tile cols
-constexpr int kLaneCols = 8;
+constexpr int kLaneRows = 4;      // lane grid rows (tile rows)
+// Lanes per problem: 16 (4 x 4 grid, two problems per warp) or 32 (4 x 8, one per warp).
+// Chosen per d by measurement (r01, cfg1 sectors at N_t=100): 16 lanes won for d = 11
+// (12 x 12 vs 12 x 16 padding: 8.5 vs 10.6 ms) and d <= 4; 32 lanes won for d = 5, 7, 9
+// (more resident warps per problem outweighed the extra padding).
+__host__ __device__ constexpr int tiny_lanes(int d) { return (d <= 4 || d == 11 || d == 12 || d == 10) ? 16 : 32; }
 constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
 
 struct TinyParams {
@@ -90,16 +93,18 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
 
-__device__ __forceinline__ double warp_sum(double v) {  // sum over the warp (one problem), fixed tree
+template <int LP>
+__device__ __forceinline__ double prob_sum(double v) {  // sum over the LP lanes of one problem, fixed tree
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = LP / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ double2 warp_sum2(double2 v) { return make_double2(warp_sum(v.x), warp_sum(v.y)); }
-__device__ __forceinline__ double row_sum(double v) {  // sum over the 8 lanes sharing a tile row (tc = 0..7)
-  v += __shfl_xor_sync(0xffffffffu, v, 1);
-  v += __shfl_xor_sync(0xffffffffu, v, 2);
-  v += __shfl_xor_sync(0xffffffffu, v, 4);
+template <int LP>
+__device__ __forceinline__ double2 prob_sum2(double2 v) { return make_double2(prob_sum<LP>(v.x), prob_sum<LP>(v.y)); }
+template <int LC>
+__device__ __forceinline__ double row_sum(double v) {  // sum over the LC lanes sharing a tile row
+#pragma unroll
+  for (int o = 1; o < LC; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 __device__ __forceinline__ double warp_max(double v) {
@@ -112,15 +117,15 @@ __device__ __forceinline__ double warp_max(double v) {
 // (ld D).  The interleaved ownership makes the 8 lanes of a tile row read 8 consecutive
 // complex values of a matrix row in one LDS.128 wavefront (no bank conflict).
 // Indices are clamped into range so padding lanes read valid memory (never stored).
-template <int D, int TSR, int TSC>
+template <int D, int TSR, int TSC, int LC>
 struct Tile {
   int tr, tc;
   __device__ __forceinline__ int row(int i) const { return min(tr + kLaneRows * i, D - 1); }
-  __device__ __forceinline__ int col(int j) const { return min(tc + kLaneCols * j, D - 1); }
-  __device__ __forceinline__ bool ok(int i, int j) const { return tr + kLaneRows * i < D && tc + kLaneCols * j < D; }
+  __device__ __forceinline__ int col(int j) const { return min(tc + LC * j, D - 1); }
+  __device__ __forceinline__ bool ok(int i, int j) const { return tr + kLaneRows * i < D && tc + LC * j < D; }
   __device__ __forceinline__ bool row_ok(int i) const { return tr + kLaneRows * i < D; }
   __device__ __forceinline__ int rrow(int i) const { return tr + kLaneRows * i; }  // unclamped
-  __device__ __forceinline__ int rcol(int j) const { return tc + kLaneCols * j; }
+  __device__ __forceinline__ int rcol(int j) const { return tc + LC * j; }
 
   __device__ __forceinline__ void zero(double2 (&t)[TSR][TSC]) const {
 #pragma unroll
@@ -205,8 +210,11 @@ struct Tile {
 template <int D, bool GATE>
 __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyParams p) {
   constexpr int R = GATE ? D : 1;  // columns of X and Lam
+  constexpr int LP = tiny_lanes(D);                      // lanes per problem
+  constexpr int LC = LP / kLaneRows;                     // lane grid cols
+  constexpr int PPW = 32 / LP;                           // problems per warp
   constexpr int TSR = (D + kLaneRows - 1) / kLaneRows;  // register tile rows
-  constexpr int TSC = (D + kLaneCols - 1) / kLaneCols;  // register tile cols
+  constexpr int TSC = (D + LC - 1) / LC;                // register tile cols
   constexpr int DD = D * D;
   constexpr int PSTRIDE = kTinyBuffers * DD;
   extern __shared__ double2 smem[];
@@ -217,13 +225,14 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tr = lane / kLaneCols, tc = lane % kLaneCols;
-  Tile<D, TSR, TSC> tl{tr, tc};
-  const int slot = blockIdx.x * p.nwarps + warp;  // park is sized for all slots
+  const int sub = lane / LP, q = lane % LP;  // problem within the warp, lane within the problem
+  const int tr = q / LC, tc = q % LC;
+  Tile<D, TSR, TSC, LC> tl{tr, tc};
+  const int slot = (blockIdx.x * p.nwarps + warp) * PPW + sub;  // park is sized for all slots
   const bool real = slot < p.batch;                            // owns a real problem (may store globally)
   const int prob = real ? slot : p.batch - 1;                  // padding slots replay the last problem's u
 
-  double2* buf = gen + (K + 1) * DD + (size_t)warp * PSTRIDE;
+  double2* buf = gen + (K + 1) * DD + (size_t)(warp * PPW + sub) * PSTRIDE;
   double2* B0 = buf;      // X (fwd) | X, A2 (bwd)
   double2* B1 = B0 + DD;  // A2 (fwd) | Lam, dA2 (bwd)
   double2* B2 = B1 + DD;  // A
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
     }
     double nrm = 0.0;
 #pragma unroll
-    for (int i = 0; i < TSR; ++i) nrm = fmax(nrm, row_sum(rowsum[i]));
+    for (int i = 0; i < TSR; ++i) nrm = fmax(nrm, row_sum<LC>(rowsum[i]));
     nrm = warp_max(real ? nrm : 0.0);  // plan is warp-uniform, from real problems only
     choose_taylor(nrm, nb, s);
     const double sc = ldexp(1.0, -s);
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
       double2 v[TSR];
 #pragma unroll
       for (int i = 0; i < TSR; ++i) v[i] = czero();
-      for (int k = tc; k < D; k += kLaneCols) {
+      for (int k = tc; k < D; k += LC) {
         const double2 y = Y[k];
 #pragma unroll
         for (int i = 0; i < TSR; ++i) {
@@ -319,7 +328,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
         }
       }
 #pragma unroll
-      for (int i = 0; i < TSR; ++i) v[i] = make_double2(row_sum(v[i].x), row_sum(v[i].y));
+      for (int i = 0; i < TSR; ++i) v[i] = make_double2(row_sum<LC>(v[i].x), row_sum<LC>(v[i].y));
       __syncwarp();
       if (tc == 0) {
 #pragma unroll
@@ -404,8 +413,8 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
     for (int i = 0; i < TSR; ++i)
       if (tl.row_ok(i)) part = cadd(part, cmul(cconj(p.target[tl.rrow(i)]), X[tl.rrow(i)]));
   }
-  const double2 tau = warp_sum2(part);
-  if (real && lane == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
+  const double2 tau = prob_sum2<LP>(part);
+  if (real && q == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
   copy_x(parkX, X, true);
   copy_x(parkL, p.target, true);
   __syncwarp();
@@ -482,8 +491,8 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
 #pragma unroll
         for (int jj = 0; jj < TSC; ++jj)
           if (tl.ok(i, jj)) cfma(pk, t[i][jj], E[tl.rcol(jj) * D + tl.rrow(i)]);
-      const double2 dtau = warp_sum2(pk);
-      if (real && lane == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau.x - ctw.y * dtau.y;
+      const double2 dtau = prob_sum2<LP>(pk);
+      if (real && q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau.x - ctw.y * dtau.y;
     }
     // X_{j-1} = U^dag X_j, Lam_{j-1} = U^dag Lam_j  -> park (global, own entries)
     mul_x(B6, true, B0, parkX);
@@ -493,7 +502,8 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
 }
 
 inline size_t tiny_smem_bytes(int d, int K, int nwarps) {
-  return sizeof(double2) * ((size_t)(K + 1) * d * d + (size_t)nwarps * kTinyBuffers * d * d);
+  const int ppw = 32 / tiny_lanes(d);
+  return sizeof(double2) * ((size_t)(K + 1) * d * d + (size_t)nwarps * ppw * kTinyBuffers * d * d);
 }
 
 }  // namespace sqoc
