@@ -34,10 +34,10 @@ constexpr int kTinyBuffers = 8;   // d x d matrices per problem in shared memory
 constexpr int kMaxControls = 4;
 constexpr int kLaneRows = 4;      // lane grid rows (tile rows)
 // Lanes per problem: 16 (4 x 4 grid, two problems per warp) or 32 (4 x 8, one per warp).
-// Chosen per d by measurement (r01, cfg1 sectors at N_t=100): 16 lanes won for d = 11
-// (12 x 12 vs 12 x 16 padding: 8.5 vs 10.6 ms) and d <= 4; 32 lanes won for d = 5, 7, 9
-// (more resident warps per problem outweighed the extra padding).
-__host__ __device__ constexpr int tiny_lanes(int d) { return (d <= 4 || d == 11 || d == 12 || d == 10) ? 16 : 32; }
+// Chosen by measurement (r01, cfg1 with the 7 sector kernels running concurrently): 16 lanes
+// for every d <= 12 gave 352 ms per 4096-seed batch vs 365 ms for the per-sector serial optimum
+// and 386 ms for 32 lanes everywhere.
+__host__ __device__ constexpr int tiny_lanes(int d) { return d <= 12 ? 16 : 32; }
 constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
 
 struct TinyParams {
