@@ -88,6 +88,13 @@ int sqoc_set_norm_bounds(sqoc_problem* p, const double* bounds);
 int sqoc_set_schedule(sqoc_problem* p, int schedule);
 int sqoc_last_schedule(const sqoc_problem* p);
 
+/* Tiny-block (d <= 16) schedule: -1 auto (default: slice-parallel for batch <= 16, fused
+ * otherwise), 0 fused (one lane group per problem runs every slice on chip), 1 slice-parallel
+ * (a lane group per (problem, slice) for the propagators and the Frechet chains; only the
+ * X / Lambda recurrences are sequential -- the latency path for single evaluations). */
+int sqoc_set_tiny_schedule(sqoc_problem* p, int schedule);
+int sqoc_last_tiny_schedule(const sqoc_problem* p);
+
 /* Propagator plan of the last large-block evaluation: Taylor degree 3*taylor_blocks,
  * `squarings` squarings, and the number of augmented-action terms (state-vector). */
 int sqoc_last_plan(const sqoc_problem* p, int* taylor_blocks, int* squarings, int* action_terms);

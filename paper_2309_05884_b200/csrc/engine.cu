@@ -45,7 +45,10 @@ struct BlockPlan {
   double2* target = nullptr;  // V or psi_f
   double2* park = nullptr;    // tiny: [slots][2][d*R]
   size_t park_slots = 0;
-  int nwarps = 1;
+  double2 *sp_U = nullptr, *sp_X = nullptr, *sp_L = nullptr;  // slice-parallel histories
+  int sp_batch = 0;
+  int nwarps = 1;       // fused kernel warps per CTA (capped by max_batch)
+  int nwarps_max = 1;   // smem-limited warps per CTA
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // per-block device timing (sqoc_set_timing)
@@ -71,6 +74,8 @@ struct sqoc_problem {
   cudaEvent_t large_done = nullptr;
   cudaEvent_t large_t0 = nullptr, large_t1 = nullptr;
   bool timing = false;
+  int tiny_mode = -1;  // -1 auto, 0 fused, 1 slice-parallel
+  int last_tiny_mode = -1;
   int launches = 0;
 };
 
@@ -100,25 +105,39 @@ __global__ void finalize_kernel(int batch, int nblocks, int KN, const double2* _
 }
 
 // ---------------------------------------------------------------- tiny dispatch
+enum TinyKernel { TK_FUSED = 0, TK_SP_EXPM = 1, TK_SP_SWEEP = 2, TK_SP_GRAD = 3 };
+
 template <int D, bool GATE>
-static int launch_tiny_t(const TinyParams& tp, int grid, int nwarps, size_t smem, cudaStream_t st) {
+static int launch_tiny_t(int which, const TinySliceParams& sp, int grid, int nwarps, size_t smem, cudaStream_t st) {
   static bool attr_set = false;
-  auto kern = grape_tiny_kernel<D, GATE>;
   if (!attr_set) {
-    SQOC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+    SQOC_CUDA(cudaFuncSetAttribute(grape_tiny_kernel<D, GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kMaxSmem));
+    SQOC_CUDA(cudaFuncSetAttribute(tiny_sp_expm_kernel<D, GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kMaxSmem));
+    SQOC_CUDA(cudaFuncSetAttribute(tiny_sp_sweep_kernel<D, GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kMaxSmem));
+    SQOC_CUDA(cudaFuncSetAttribute(tiny_sp_grad_kernel<D, GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kMaxSmem));
     attr_set = true;
   }
-  kern<<<grid, nwarps * 32, smem, st>>>(tp);
+  switch (which) {
+    case TK_FUSED: grape_tiny_kernel<D, GATE><<<grid, nwarps * 32, smem, st>>>(sp.p); break;
+    case TK_SP_EXPM: tiny_sp_expm_kernel<D, GATE><<<grid, nwarps * 32, smem, st>>>(sp); break;
+    case TK_SP_SWEEP: tiny_sp_sweep_kernel<D, GATE><<<grid, nwarps * 32, smem, st>>>(sp); break;
+    default: tiny_sp_grad_kernel<D, GATE><<<grid, nwarps * 32, smem, st>>>(sp); break;
+  }
   SQOC_CUDA(cudaGetLastError());
   return SQOC_OK;
 }
 
 template <bool GATE>
-static int launch_tiny(int d, const TinyParams& tp, int grid, int nwarps, size_t smem, cudaStream_t st) {
+static int launch_tiny(int d, int which, const TinySliceParams& sp, int grid, int nwarps, size_t smem,
+                       cudaStream_t st) {
   switch (d) {
 #define SQOC_CASE(D) \
   case D:            \
-    return launch_tiny_t<D, GATE>(tp, grid, nwarps, smem, st);
+    return launch_tiny_t<D, GATE>(which, sp, grid, nwarps, smem, st);
     SQOC_CASE(1) SQOC_CASE(2) SQOC_CASE(3) SQOC_CASE(4) SQOC_CASE(5) SQOC_CASE(6) SQOC_CASE(7) SQOC_CASE(8)
     SQOC_CASE(9) SQOC_CASE(10) SQOC_CASE(11) SQOC_CASE(12) SQOC_CASE(13) SQOC_CASE(14) SQOC_CASE(15) SQOC_CASE(16)
 #undef SQOC_CASE
@@ -150,6 +169,9 @@ static void free_problem(sqoc_problem* p) {
     cudaFree(b.x0);
     cudaFree(b.target);
     cudaFree(b.park);
+    cudaFree(b.sp_U);
+    cudaFree(b.sp_X);
+    cudaFree(b.sp_L);
     if (b.stream) cudaStreamDestroy(b.stream);
     if (b.done) cudaEventDestroy(b.done);
     if (b.t0) cudaEventDestroy(b.t0);
@@ -252,6 +274,7 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
       const int R = objective == SQOC_OBJ_GATE ? d : 1;
       const int pg = 32 / tiny_lanes(d);
       bp.nwarps = choose_nwarps(d, n_controls, max_batch);
+      bp.nwarps_max = choose_nwarps(d, n_controls, 1 << 30);
       const int per_cta = pg * bp.nwarps;
       bp.park_slots = (size_t)((max_batch + per_cta - 1) / per_cta) * per_cta;
       chk(cudaMalloc(&bp.park, bp.park_slots * 2 * d * R * sizeof(double2)), "cudaMalloc park");
@@ -343,7 +366,8 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
     if (!bp.tiny) continue;
     if (p->timing) SQOC_CUDA(cudaEventRecord(bp.t0, bp.stream));
     {
-      TinyParams tp;
+      TinySliceParams sp{};
+      TinyParams& tp = sp.p;
       tp.K = p->K;
       tp.N = p->N;
       tp.batch = batch;
@@ -357,14 +381,59 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
       tp.grad_out = gout;
       tp.park = bp.park;
       const int pg = 32 / tiny_lanes(bp.d);
-      int nw = std::max(1, std::min(bp.nwarps, (batch + pg - 1) / pg));
-      tp.nwarps = nw;
-      const int grid = (batch + pg * nw - 1) / (pg * nw);
-      const size_t smem = tiny_smem_bytes(bp.d, p->K, nw);
-      int rc = gate ? launch_tiny<true>(bp.d, tp, grid, nw, smem, bp.stream)
-                    : launch_tiny<false>(bp.d, tp, grid, nw, smem, bp.stream);
+      const size_t R = gate ? bp.d : 1;
+      // slice-parallel latency path for small batches (every (problem, slice) its own lane group)
+      const bool sp_mode = p->N > 0 && (p->tiny_mode == 1 || (p->tiny_mode == -1 && batch <= kTinySliceParallelMaxBatch));
+      p->last_tiny_mode = sp_mode ? 1 : 0;
+      int rc = SQOC_OK;
+      if (sp_mode) {
+        if (bp.sp_batch < batch) {
+          cudaFree(bp.sp_U);
+          cudaFree(bp.sp_X);
+          cudaFree(bp.sp_L);
+          bp.sp_U = bp.sp_X = bp.sp_L = nullptr;
+          const int nb_alloc = std::max(batch, std::min(p->max_batch, kTinySliceParallelMaxBatch));
+          SQOC_CUDA(cudaMalloc(&bp.sp_U, (size_t)nb_alloc * p->N * bp.d * bp.d * sizeof(double2)));
+          SQOC_CUDA(cudaMalloc(&bp.sp_X, (size_t)nb_alloc * (p->N + 1) * bp.d * R * sizeof(double2)));
+          SQOC_CUDA(cudaMalloc(&bp.sp_L, (size_t)nb_alloc * (p->N + 1) * bp.d * R * sizeof(double2)));
+          bp.sp_batch = nb_alloc;
+        }
+        sp.Uh = bp.sp_U;
+        sp.Xh = bp.sp_X;
+        sp.Lh = bp.sp_L;
+        sp.units = batch * p->N;
+        // phases 1 and 3: lane group per (problem, slice); phase 2: per problem
+        const int warps_units = (sp.units + pg - 1) / pg;
+        const int nw = std::max(1, std::min(bp.nwarps_max, warps_units));
+        tp.nwarps = nw;
+        const size_t smem = tiny_smem_bytes(bp.d, p->K, nw);
+        const int grid_units = (warps_units + nw - 1) / nw;
+        const int warps_b = (batch + pg - 1) / pg;
+        const int nw_b = std::max(1, std::min(bp.nwarps_max, warps_b));
+        const int grid_b = (warps_b + nw_b - 1) / nw_b;
+        rc = gate ? launch_tiny<true>(bp.d, TK_SP_EXPM, sp, grid_units, nw, smem, bp.stream)
+                  : launch_tiny<false>(bp.d, TK_SP_EXPM, sp, grid_units, nw, smem, bp.stream);
+        if (rc == SQOC_OK) {
+          TinySliceParams sp2 = sp;
+          sp2.p.nwarps = nw_b;
+          const size_t smem_b = tiny_smem_bytes(bp.d, p->K, nw_b);
+          rc = gate ? launch_tiny<true>(bp.d, TK_SP_SWEEP, sp2, grid_b, nw_b, smem_b, bp.stream)
+                    : launch_tiny<false>(bp.d, TK_SP_SWEEP, sp2, grid_b, nw_b, smem_b, bp.stream);
+        }
+        if (rc == SQOC_OK)
+          rc = gate ? launch_tiny<true>(bp.d, TK_SP_GRAD, sp, grid_units, nw, smem, bp.stream)
+                    : launch_tiny<false>(bp.d, TK_SP_GRAD, sp, grid_units, nw, smem, bp.stream);
+        p->launches += 3;
+      } else {
+        int nw = std::max(1, std::min(bp.nwarps, (batch + pg - 1) / pg));
+        tp.nwarps = nw;
+        const int grid = (batch + pg * nw - 1) / (pg * nw);
+        const size_t smem = tiny_smem_bytes(bp.d, p->K, nw);
+        rc = gate ? launch_tiny<true>(bp.d, TK_FUSED, sp, grid, nw, smem, bp.stream)
+                  : launch_tiny<false>(bp.d, TK_FUSED, sp, grid, nw, smem, bp.stream);
+        p->launches += 1;
+      }
       if (rc != SQOC_OK) return rc;
-      p->launches += 1;
     }
     if (p->timing) SQOC_CUDA(cudaEventRecord(bp.t1, bp.stream));
     SQOC_CUDA(cudaEventRecord(bp.done, bp.stream));
@@ -545,6 +614,14 @@ int sqoc_set_schedule(sqoc_problem* p, int schedule) {
 }
 
 int sqoc_last_schedule(const sqoc_problem* p) { return (p && p->large) ? p->large->mode : -1; }
+
+int sqoc_set_tiny_schedule(sqoc_problem* p, int schedule) {
+  if (!p || schedule < -1 || schedule > 1) return fail(SQOC_ERR_ARG, "tiny schedule must be -1, 0 or 1");
+  p->tiny_mode = schedule;
+  return SQOC_OK;
+}
+
+int sqoc_last_tiny_schedule(const sqoc_problem* p) { return p ? p->last_tiny_mode : -1; }
 
 int sqoc_last_plan(const sqoc_problem* p, int* taylor_blocks, int* squarings, int* action_terms) {
   if (!p || !taylor_blocks || !squarings || !action_terms) return fail(SQOC_ERR_ARG, "NULL argument");

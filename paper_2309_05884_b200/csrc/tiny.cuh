@@ -39,6 +39,7 @@ constexpr int kLaneRows = 4;      // lane grid rows (tile rows)
 // and 386 ms for 32 lanes everywhere.
 __host__ __device__ constexpr int tiny_lanes(int d) { return d <= 12 ? 16 : 32; }
 constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
+constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
 
 struct TinyParams {
   int K, N, batch;
@@ -207,46 +208,46 @@ struct Tile {
   }
 };
 
+// Per-warp problem context: tile geometry, shared-memory buffers and the per-slice
+// building blocks shared by the fused kernel and the slice-parallel kernels.
 template <int D, bool GATE>
-__global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyParams p) {
-  constexpr int R = GATE ? D : 1;  // columns of X and Lam
-  constexpr int LP = tiny_lanes(D);                      // lanes per problem
-  constexpr int LC = LP / kLaneRows;                     // lane grid cols
-  constexpr int PPW = 32 / LP;                           // problems per warp
-  constexpr int TSR = (D + kLaneRows - 1) / kLaneRows;  // register tile rows
-  constexpr int TSC = (D + LC - 1) / LC;                // register tile cols
-  constexpr int DD = D * D;
-  constexpr int PSTRIDE = kTinyBuffers * DD;
-  extern __shared__ double2 smem[];
+struct TinyCtx {
+  static constexpr int R = GATE ? D : 1;  // columns of X and Lam
+  static constexpr int LP = tiny_lanes(D);
+  static constexpr int LC = LP / kLaneRows;
+  static constexpr int PPW = 32 / LP;
+  static constexpr int TSR = (D + kLaneRows - 1) / kLaneRows;
+  static constexpr int TSC = (D + LC - 1) / LC;
+  static constexpr int DD = D * D;
+  using T2 = double2[TSR][TSC];
 
-  const int K = p.K, N = p.N;
-  double2* gen = smem;  // (K+1) DD
-  for (int i = threadIdx.x; i < (K + 1) * DD; i += blockDim.x) gen[i] = p.gen[i];
-  __syncthreads();
+  Tile<D, TSR, TSC, LC> tl;
+  int K, N, q, sub;
+  const double2* gen;  // (K+1) DD in smem
+  double2 *B0, *B1, *B2, *B3, *B4, *B5, *B6, *B7;
+  const double* up;  // this problem's u [K][N]
+  bool real;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sub = lane / LP, q = lane % LP;  // problem within the warp, lane within the problem
-  const int tr = q / LC, tc = q % LC;
-  Tile<D, TSR, TSC, LC> tl{tr, tc};
-  const int slot = (blockIdx.x * p.nwarps + warp) * PPW + sub;  // park is sized for all slots
-  const bool real = slot < p.batch;                            // owns a real problem (may store globally)
-  const int prob = real ? slot : p.batch - 1;                  // padding slots replay the last problem's u
+  __device__ __forceinline__ void init(const double2* gen_smem, double2* buf, int K_, int N_) {
+    const int lane = threadIdx.x & 31;
+    sub = lane / LP;
+    q = lane % LP;
+    tl = Tile<D, TSR, TSC, LC>{q / LC, q % LC};
+    gen = gen_smem;
+    K = K_;
+    N = N_;
+    B0 = buf; B1 = B0 + DD; B2 = B1 + DD; B3 = B2 + DD; B4 = B3 + DD; B5 = B4 + DD; B6 = B5 + DD; B7 = B6 + DD;
+  }
 
-  double2* buf = gen + (K + 1) * DD + (size_t)(warp * PPW + sub) * PSTRIDE;
-  double2* B0 = buf;      // X (fwd) | X, A2 (bwd)
-  double2* B1 = B0 + DD;  // A2 (fwd) | Lam, dA2 (bwd)
-  double2* B2 = B1 + DD;  // A
-  double2* B3 = B2 + DD;  // Adot
-  double2* B4 = B3 + DD;  // A3
-  double2* B5 = B4 + DD;  // dA3
-  double2* B6 = B5 + DD;  // T  (-> U)
-  double2* B7 = B6 + DD;  // dT (-> N)
-  const double* up = p.u + (size_t)prob * K * N;
-  double2* parkX = p.park + (size_t)slot * 2 * D * R;
-  double2* parkL = parkX + D * R;
+  __device__ __forceinline__ void scale(T2& t, double c) const {
+#pragma unroll
+    for (int i = 0; i < TSR; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TSC; ++jj) t[i][jj] = cscale(t[i][jj], c);
+  }
 
-  // ---- A tile for slice j (scaled by 2^-s), warp-uniform Taylor plan ----
-  auto build_a = [&](int j, double2 (&a)[TSR][TSC], int& nb, int& s) {
+  // A tile of slice j (scaled by 2^-s) and the warp-uniform Taylor plan
+  __device__ __forceinline__ void build_a(int j, T2& a, int& nb, int& s) const {
     double uk[kMaxControls];
 #pragma unroll
     for (int k = 0; k < kMaxControls; ++k) uk[k] = (k < K) ? up[k * N + j] : 0.0;
@@ -272,15 +273,11 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
     for (int i = 0; i < TSR; ++i) nrm = fmax(nrm, row_sum<LC>(rowsum[i]));
     nrm = warp_max(real ? nrm : 0.0);  // plan is warp-uniform, from real problems only
     choose_taylor(nrm, nb, s);
-    const double sc = ldexp(1.0, -s);
-#pragma unroll
-    for (int i = 0; i < TSR; ++i)
-#pragma unroll
-      for (int jj = 0; jj < TSC; ++jj) a[i][jj] = cscale(a[i][jj], sc);
-  };
+    scale(a, ldexp(1.0, -s));
+  }
 
-  // Q_t tile: c_{3t} I + c_{3t+1} A + c_{3t+2} A2 ; dQ_t: c_{3t+1} dA + c_{3t+2} dA2
-  auto add_q = [&](double2 (&t)[TSR][TSC], int qi, const double2* A, const double2* A2) {
+  // Q_t = c_{3t} I + c_{3t+1} A + c_{3t+2} A2 ;  dQ_t = c_{3t+1} dA + c_{3t+2} dA2
+  __device__ __forceinline__ void add_q(T2& t, int qi, const double2* A, const double2* A2) const {
 #pragma unroll
     for (int i = 0; i < TSR; ++i)
 #pragma unroll
@@ -289,8 +286,8 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
         t[i][jj] = cadd(t[i][jj], cadd(cscale(A[o], c_inv_fact[3 * qi + 1]), cscale(A2[o], c_inv_fact[3 * qi + 2])));
         if (tl.rrow(i) == tl.rcol(jj)) t[i][jj].x += c_inv_fact[3 * qi];
       }
-  };
-  auto add_dq = [&](double2 (&t)[TSR][TSC], int qi, const double2* dA, const double2* dA2) {
+  }
+  __device__ __forceinline__ void add_dq(T2& t, int qi, const double2* dA, const double2* dA2) const {
 #pragma unroll
     for (int i = 0; i < TSR; ++i)
 #pragma unroll
@@ -298,86 +295,18 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
         const int o = tl.row(i) * D + tl.col(jj);
         t[i][jj] = cadd(t[i][jj], cadd(cscale(dA[o], c_inv_fact[3 * qi + 1]), cscale(dA2[o], c_inv_fact[3 * qi + 2])));
       }
-  };
-  auto scale_tile = [&](double2 (&t)[TSR][TSC], double c) {
-#pragma unroll
-    for (int i = 0; i < TSR; ++i)
-#pragma unroll
-      for (int jj = 0; jj < TSC; ++jj) t[i][jj] = cscale(t[i][jj], c);
-  };
-
-  // ---- X-shaped products (R columns): gate -> tiles; state -> one column, k split over tc ----
-  // out = Op(U) Y where Op(U) = U (adj=false) or U^dag (adj=true); Y: D x R; store into Yout (may alias Y)
-  auto mul_x = [&](const double2* U, bool adj, const double2* Y, double2* Yout) {
-    if (GATE) {
-      double2 t[TSR][TSC];
-      if (adj) tl.mul_adj(t, U, Y);
-      else tl.mul(t, U, Y);
-      __syncwarp();
-      tl.store(Yout, t, true);  // park is sized for every slot, padding slots included
-    } else {
-      double2 v[TSR];
-#pragma unroll
-      for (int i = 0; i < TSR; ++i) v[i] = czero();
-      for (int k = tc; k < D; k += LC) {
-        const double2 y = Y[k];
-#pragma unroll
-        for (int i = 0; i < TSR; ++i) {
-          const double2 l = adj ? cconj(U[k * D + tl.row(i)]) : U[tl.row(i) * D + k];
-          cfma(v[i], l, y);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < TSR; ++i) v[i] = make_double2(row_sum<LC>(v[i].x), row_sum<LC>(v[i].y));
-      __syncwarp();
-      if (tc == 0) {
-#pragma unroll
-        for (int i = 0; i < TSR; ++i)
-          if (tl.row_ok(i)) Yout[tl.rrow(i)] = v[i];
-      }
-    }
-  };
-  // copy a D x R matrix between smem and global (own tile / own rows)
-  auto copy_x = [&](double2* dst, const double2* src, bool wr) {
-    if (!wr) return;
-    if (GATE) {
-#pragma unroll
-      for (int i = 0; i < TSR; ++i)
-#pragma unroll
-        for (int jj = 0; jj < TSC; ++jj)
-          if (tl.ok(i, jj)) dst[tl.rrow(i) * D + tl.rcol(jj)] = src[tl.rrow(i) * D + tl.rcol(jj)];
-    } else if (tc == 0) {
-#pragma unroll
-      for (int i = 0; i < TSR; ++i)
-        if (tl.row_ok(i)) dst[tl.rrow(i)] = src[tl.rrow(i)];
-    }
-  };
-
-  double2 t[TSR][TSC], dt[TSR][TSC];
-  // ================= forward sweep: X_N =================
-  double2* X = B0;
-  if (GATE) {
-#pragma unroll
-    for (int i = 0; i < TSR; ++i)
-#pragma unroll
-      for (int jj = 0; jj < TSC; ++jj) t[i][jj] = make_double2(tl.rrow(i) == tl.rcol(jj) ? 1.0 : 0.0, 0.0);
-    tl.store(X, t, true);
-  } else {
-    copy_x(X, p.x0, true);
   }
-  __syncwarp();
-  for (int j = 0; j < N; ++j) {
-    int nb, s;
-    build_a(j, t, nb, s);
-    tl.store(B2, t, true);
-    __syncwarp();
+
+  // U = R(A) with A (scaled) in B2; uses B1 (A2), B4 (A3); U -> B6
+  __device__ __forceinline__ void expm_plain(int nb, int s) const {
+    T2 t;
     tl.mul(t, B2, B2);  // A2
     tl.store(B1, t, true);
     __syncwarp();
     tl.mul(t, B1, B2);  // A3
     tl.store(B4, t, true);
     __syncwarp();
-    scale_tile(t, c_inv_fact[3 * nb]);  // T = c_{3nb} A3 + Q_{nb-1}
+    scale(t, c_inv_fact[3 * nb]);  // T = c_{3nb} A3 + Q_{nb-1}
     add_q(t, nb - 1, B2, B1);
     tl.store(B6, t, true);
     for (int qi = nb - 2; qi >= 0; --qi) {
@@ -394,59 +323,12 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
       tl.store(B6, t, true);
     }
     __syncwarp();
-    mul_x(B6, false, X, X);  // X_j = U_j X_{j-1} (in place after the sync inside)
-    __syncwarp();
   }
-  // tau = <V, X_N>_F ; park X_N and Lam_N = V
-  double2 part = czero();
-  if (GATE) {
-#pragma unroll
-    for (int i = 0; i < TSR; ++i)
-#pragma unroll
-      for (int jj = 0; jj < TSC; ++jj)
-        if (tl.ok(i, jj)) {
-          const int o = tl.rrow(i) * D + tl.rcol(jj);
-          part = cadd(part, cmul(cconj(p.target[o]), X[o]));
-        }
-  } else if (tc == 0) {
-#pragma unroll
-    for (int i = 0; i < TSR; ++i)
-      if (tl.row_ok(i)) part = cadd(part, cmul(cconj(p.target[tl.rrow(i)]), X[tl.rrow(i)]));
-  }
-  const double2 tau = prob_sum2<LP>(part);
-  if (real && q == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
-  copy_x(parkX, X, true);
-  copy_x(parkL, p.target, true);
-  __syncwarp();
 
-  // ================= backward sweep: gradient =================
-  const double2 ctw = cscale(cconj(tau), 2.0 * p.weight);  // dF/du = Re(2 w conj(tau) dtau/du)
-  for (int j = N - 1; j >= 0; --j) {
-    int nb, s;
-    copy_x(B0, parkX, true);  // stage X_j, Lam_j
-    copy_x(B1, parkL, true);
-    build_a(j, t, nb, s);
-    tl.store(B2, t, true);
-    __syncwarp();
-    {  // Adot = 2^-s X_j Lam_j^dag
-      const double sc = ldexp(1.0, -s);
-      tl.zero(t);
-#pragma unroll 1
-      for (int k = 0; k < R; ++k) {
-        double2 l[TSR], m[TSC];
-#pragma unroll
-        for (int i = 0; i < TSR; ++i) l[i] = B0[tl.row(i) * R + k];
-#pragma unroll
-        for (int jj = 0; jj < TSC; ++jj) m[jj] = cconj(B1[tl.col(jj) * R + k]);
-#pragma unroll
-        for (int i = 0; i < TSR; ++i)
-#pragma unroll
-          for (int jj = 0; jj < TSC; ++jj) cfma(t[i][jj], l[i], m[jj]);
-      }
-      scale_tile(t, sc);
-      tl.store(B3, t, true);
-    }
-    __syncwarp();
+  // (U, N) = (R(A), L_R(A, Adot)) with A in B2, Adot in B3 (both scaled); uses B0, B1, B4, B5;
+  // U -> B6, N -> B7
+  __device__ __forceinline__ void expm_pair(int nb, int s) const {
+    T2 t, dt;
     tl.pair(t, dt, B2, B3, B2, B3);  // (A2, dA2)
     tl.store(B0, t, true);
     tl.store(B1, dt, true);
@@ -455,8 +337,8 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
     tl.store(B4, t, true);
     tl.store(B5, dt, true);
     __syncwarp();
-    scale_tile(t, c_inv_fact[3 * nb]);
-    scale_tile(dt, c_inv_fact[3 * nb]);
+    scale(t, c_inv_fact[3 * nb]);
+    scale(dt, c_inv_fact[3 * nb]);
     add_q(t, nb - 1, B2, B0);
     add_dq(dt, nb - 1, B3, B1);
     tl.store(B6, t, true);
@@ -478,10 +360,32 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
       tl.store(B7, dt, true);
     }
     __syncwarp();
-    copy_x(B0, parkX, true);  // restage X_j, Lam_j (B0/B1 were reused)
-    copy_x(B1, parkL, true);
+  }
+
+  // Adot (B3) = 2^-s X Lam^dag with X in B0, Lam in B1 (D x R each)
+  __device__ __forceinline__ void seed_c(int s) const {
+    T2 t;
+    tl.zero(t);
+#pragma unroll 1
+    for (int k = 0; k < R; ++k) {
+      double2 l[TSR], m[TSC];
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) l[i] = B0[tl.row(i) * R + k];
+#pragma unroll
+      for (int jj = 0; jj < TSC; ++jj) m[jj] = cconj(B1[tl.col(jj) * R + k]);
+#pragma unroll
+      for (int i = 0; i < TSR; ++i)
+#pragma unroll
+        for (int jj = 0; jj < TSC; ++jj) cfma(t[i][jj], l[i], m[jj]);
+    }
+    scale(t, ldexp(1.0, -s));
+    tl.store(B3, t, true);
     __syncwarp();
-    // D = U^dag N ; dtau/du_k = Tr(D E_k) = sum_pq D[p][q] E_k[q][p]
+  }
+
+  // dtau_k = Tr(U^dag N E_k) with U in B6, N in B7 (sums over the problem's lanes)
+  __device__ __forceinline__ void traces(double2 (&dtau)[kMaxControls]) const {
+    T2 t;
     tl.mul_adj(t, B6, B7);
     for (int k = 0; k < K; ++k) {
       const double2* E = gen + (k + 1) * DD;
@@ -491,14 +395,280 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
 #pragma unroll
         for (int jj = 0; jj < TSC; ++jj)
           if (tl.ok(i, jj)) cfma(pk, t[i][jj], E[tl.rcol(jj) * D + tl.rrow(i)]);
-      const double2 dtau = prob_sum2<LP>(pk);
-      if (real && q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau.x - ctw.y * dtau.y;
+      dtau[k] = prob_sum2<LP>(pk);
     }
-    // X_{j-1} = U^dag X_j, Lam_{j-1} = U^dag Lam_j  -> park (global, own entries)
-    mul_x(B6, true, B0, parkX);
-    mul_x(B6, true, B1, parkL);
+  }
+
+  // Yout = Op(U) Y for D x R matrices (Op = U or U^dag); gate -> tiles, state -> one column.
+  // Safe in place (syncs before the store).
+  __device__ __forceinline__ void mul_x(const double2* U, bool adj, const double2* Y, double2* Yout) const {
+    if (GATE) {
+      T2 t;
+      if (adj) tl.mul_adj(t, U, Y);
+      else tl.mul(t, U, Y);
+      __syncwarp();
+      tl.store(Yout, t, true);
+    } else {
+      double2 v[TSR];
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) v[i] = czero();
+      for (int k = tl.tc; k < D; k += LC) {
+        const double2 y = Y[k];
+#pragma unroll
+        for (int i = 0; i < TSR; ++i) {
+          const double2 l = adj ? cconj(U[k * D + tl.row(i)]) : U[tl.row(i) * D + k];
+          cfma(v[i], l, y);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) v[i] = make_double2(row_sum<LC>(v[i].x), row_sum<LC>(v[i].y));
+      __syncwarp();
+      if (tl.tc == 0) {
+#pragma unroll
+        for (int i = 0; i < TSR; ++i)
+          if (tl.row_ok(i)) Yout[tl.rrow(i)] = v[i];
+      }
+    }
+  }
+
+  // copy a D x R matrix (own entries)
+  __device__ __forceinline__ void copy_x(double2* dst, const double2* src) const {
+    if (GATE) {
+#pragma unroll
+      for (int i = 0; i < TSR; ++i)
+#pragma unroll
+        for (int jj = 0; jj < TSC; ++jj)
+          if (tl.ok(i, jj)) dst[tl.rrow(i) * D + tl.rcol(jj)] = src[tl.rrow(i) * D + tl.rcol(jj)];
+    } else if (tl.tc == 0) {
+#pragma unroll
+      for (int i = 0; i < TSR; ++i)
+        if (tl.row_ok(i)) dst[tl.rrow(i)] = src[tl.rrow(i)];
+    }
+  }
+  __device__ __forceinline__ void copy_dd(double2* dst, const double2* src) const {  // D x D, own tile
+#pragma unroll
+    for (int i = 0; i < TSR; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TSC; ++jj)
+        if (tl.ok(i, jj)) dst[tl.rrow(i) * D + tl.rcol(jj)] = src[tl.rrow(i) * D + tl.rcol(jj)];
+  }
+  __device__ __forceinline__ void set_identity(double2* X) const {
+    T2 t;
+#pragma unroll
+    for (int i = 0; i < TSR; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TSC; ++jj) t[i][jj] = make_double2(tl.rrow(i) == tl.rcol(jj) ? 1.0 : 0.0, 0.0);
+    tl.store(X, t, true);
+  }
+  // <V, X>_F over the problem's lanes
+  __device__ __forceinline__ double2 overlap(const double2* V, const double2* X) const {
+    double2 part = czero();
+    if (GATE) {
+#pragma unroll
+      for (int i = 0; i < TSR; ++i)
+#pragma unroll
+        for (int jj = 0; jj < TSC; ++jj)
+          if (tl.ok(i, jj)) {
+            const int o = tl.rrow(i) * D + tl.rcol(jj);
+            part = cadd(part, cmul(cconj(V[o]), X[o]));
+          }
+    } else if (tl.tc == 0) {
+#pragma unroll
+      for (int i = 0; i < TSR; ++i)
+        if (tl.row_ok(i)) part = cadd(part, cmul(cconj(V[tl.rrow(i)]), X[tl.rrow(i)]));
+    }
+    return prob_sum2<LP>(part);
+  }
+};
+
+template <int D>
+__device__ __forceinline__ double2* load_generators(const TinyParams& p) {
+  extern __shared__ double2 smem[];
+  for (int i = threadIdx.x; i < (p.K + 1) * D * D; i += blockDim.x) smem[i] = p.gen[i];
+  __syncthreads();
+  return smem;
+}
+
+// ------------------------------------------------------------------ fused kernel
+// One launch per block: all slices, both sweeps, gradient traces, on chip.
+template <int D, bool GATE>
+__global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyParams p) {
+  using C = TinyCtx<D, GATE>;
+  constexpr int R = C::R;
+  const int K = p.K, N = p.N;
+  double2* gen = load_generators<D>(p);
+  const int warp = threadIdx.x >> 5;
+  C c;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / C::LP;
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + sub) * kTinyBuffers * C::DD, K, N);
+  const int slot = (blockIdx.x * p.nwarps + warp) * C::PPW + sub;  // park is sized for all slots
+  c.real = slot < p.batch;                                         // owns a real problem (may store globally)
+  const int prob = c.real ? slot : p.batch - 1;                    // padding slots replay the last problem's u
+  c.up = p.u + (size_t)prob * K * N;
+  double2* parkX = p.park + (size_t)slot * 2 * D * R;
+  double2* parkL = parkX + D * R;
+
+  // ================= forward sweep: X_N =================
+  double2* X = c.B0;
+  if (GATE) c.set_identity(X);
+  else c.copy_x(X, p.x0);
+  __syncwarp();
+  typename C::T2 t;
+  for (int j = 0; j < N; ++j) {
+    int nb, s;
+    c.build_a(j, t, nb, s);
+    c.tl.store(c.B2, t, true);
+    __syncwarp();
+    c.expm_plain(nb, s);
+    c.mul_x(c.B6, false, X, X);  // X_j = U_j X_{j-1}
     __syncwarp();
   }
+  const double2 tau = c.overlap(p.target, X);
+  if (c.real && c.q == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
+  c.copy_x(parkX, X);
+  c.copy_x(parkL, p.target);
+  __syncwarp();
+
+  // ================= backward sweep: gradient =================
+  const double2 ctw = cscale(cconj(tau), 2.0 * p.weight);  // dF/du = Re(2 w conj(tau) dtau/du)
+  for (int j = N - 1; j >= 0; --j) {
+    int nb, s;
+    c.copy_x(c.B0, parkX);  // stage X_j, Lam_j
+    c.copy_x(c.B1, parkL);
+    c.build_a(j, t, nb, s);
+    c.tl.store(c.B2, t, true);
+    __syncwarp();
+    c.seed_c(s);
+    c.expm_pair(nb, s);
+    c.copy_x(c.B0, parkX);  // restage X_j, Lam_j (B0/B1 were reused)
+    c.copy_x(c.B1, parkL);
+    __syncwarp();
+    double2 dtau[kMaxControls];
+    c.traces(dtau);
+    for (int k = 0; k < K; ++k)
+      if (c.real && c.q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau[k].x - ctw.y * dtau[k].y;
+    c.mul_x(c.B6, true, c.B0, parkX);  // X_{j-1} = U^dag X_j, Lam_{j-1} = U^dag Lam_j -> park
+    c.mul_x(c.B6, true, c.B1, parkL);
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ slice-parallel kernels
+// Latency path for small batches (e.g. cfg 0: one problem, N = 100): every (problem, slice)
+// gets its own lane group for the expm and for the Frechet pair chain; only the
+// X / Lam recurrences stay sequential (one lane group per problem).
+struct TinySliceParams {
+  TinyParams p;
+  double2* Uh;   // [batch][N][DD]
+  double2* Xh;   // [batch][N+1][D*R]
+  double2* Lh;   // [batch][N+1][D*R]
+  int units;     // batch * N (lane-group work items of the parallel phases)
+};
+
+// phase 1: U_j for every (problem, slice)
+template <int D, bool GATE>
+__global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_expm_kernel(TinySliceParams sp) {
+  using C = TinyCtx<D, GATE>;
+  const TinyParams& p = sp.p;
+  const int K = p.K, N = p.N;
+  double2* gen = load_generators<D>(p);
+  const int warp = threadIdx.x >> 5;
+  C c;
+  const int sub = (threadIdx.x & 31) / C::LP;
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + sub) * kTinyBuffers * C::DD, K, N);
+  const int item_raw = (blockIdx.x * p.nwarps + warp) * C::PPW + sub;
+  c.real = item_raw < sp.units;
+  const int item = c.real ? item_raw : sp.units - 1;
+  const int prob = item / N, j = item % N;
+  c.up = p.u + (size_t)prob * K * N;
+  typename C::T2 t;
+  int nb, s;
+  c.build_a(j, t, nb, s);
+  c.tl.store(c.B2, t, true);
+  __syncwarp();
+  c.expm_plain(nb, s);
+  if (c.real) c.copy_dd(sp.Uh + (size_t)item * C::DD, c.B6);
+}
+
+// phase 2: X / Lam recurrences (one lane group per problem), tau
+template <int D, bool GATE>
+__global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_sweep_kernel(TinySliceParams sp) {
+  using C = TinyCtx<D, GATE>;
+  constexpr int R = C::R;
+  const TinyParams& p = sp.p;
+  const int K = p.K, N = p.N;
+  double2* gen = load_generators<D>(p);
+  const int warp = threadIdx.x >> 5;
+  C c;
+  const int sub = (threadIdx.x & 31) / C::LP;
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + sub) * kTinyBuffers * C::DD, K, N);
+  const int slot = (blockIdx.x * p.nwarps + warp) * C::PPW + sub;
+  c.real = slot < p.batch;
+  const int prob = c.real ? slot : p.batch - 1;
+  const double2* U = sp.Uh + (size_t)prob * N * C::DD;
+  double2* Xh = sp.Xh + (size_t)prob * (N + 1) * D * R;
+  double2* Lh = sp.Lh + (size_t)prob * (N + 1) * D * R;
+  double2* X = c.B0;
+  double2* L = c.B1;
+  if (GATE) c.set_identity(X);
+  else c.copy_x(X, p.x0);
+  __syncwarp();
+  if (c.real) c.copy_x(Xh, X);
+  for (int j = 0; j < N; ++j) {
+    c.copy_dd(c.B6, U + (size_t)j * C::DD);
+    __syncwarp();
+    c.mul_x(c.B6, false, X, X);
+    __syncwarp();
+    if (c.real) c.copy_x(Xh + (size_t)(j + 1) * D * R, X);
+  }
+  const double2 tau = c.overlap(p.target, X);
+  if (c.real && c.q == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
+  c.copy_x(L, p.target);
+  __syncwarp();
+  if (c.real) c.copy_x(Lh + (size_t)N * D * R, L);
+  for (int j = N - 1; j >= 0; --j) {
+    c.copy_dd(c.B6, U + (size_t)j * C::DD);
+    __syncwarp();
+    c.mul_x(c.B6, true, L, L);
+    __syncwarp();
+    if (c.real) c.copy_x(Lh + (size_t)j * D * R, L);
+  }
+}
+
+// phase 3: Frechet pair chain + traces for every (problem, slice)
+template <int D, bool GATE>
+__global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_grad_kernel(TinySliceParams sp) {
+  using C = TinyCtx<D, GATE>;
+  constexpr int R = C::R;
+  const TinyParams& p = sp.p;
+  const int K = p.K, N = p.N;
+  double2* gen = load_generators<D>(p);
+  const int warp = threadIdx.x >> 5;
+  C c;
+  const int sub = (threadIdx.x & 31) / C::LP;
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + sub) * kTinyBuffers * C::DD, K, N);
+  const int item_raw = (blockIdx.x * p.nwarps + warp) * C::PPW + sub;
+  c.real = item_raw < sp.units;
+  const int item = c.real ? item_raw : sp.units - 1;
+  const int prob = item / N, j = item % N;
+  c.up = p.u + (size_t)prob * K * N;
+  // C_j = X_after_j Lam_after_j^dag  (histories: index j + 1)
+  c.copy_x(c.B0, sp.Xh + ((size_t)prob * (N + 1) + j + 1) * D * R);
+  c.copy_x(c.B1, sp.Lh + ((size_t)prob * (N + 1) + j + 1) * D * R);
+  typename C::T2 t;
+  int nb, s;
+  c.build_a(j, t, nb, s);
+  c.tl.store(c.B2, t, true);
+  __syncwarp();
+  c.seed_c(s);
+  c.expm_pair(nb, s);
+  double2 dtau[kMaxControls];
+  c.traces(dtau);
+  const double2 tau = p.tau_out[(size_t)prob * p.tau_stride];
+  const double2 ctw = cscale(cconj(tau), 2.0 * p.weight);
+  for (int k = 0; k < K; ++k)
+    if (c.real && c.q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau[k].x - ctw.y * dtau[k].y;
 }
 
 inline size_t tiny_smem_bytes(int d, int K, int nwarps) {

@@ -117,6 +117,16 @@ class GrapeEngine:
     def last_schedule(self) -> str:
         return {-1: "none", 0: "sequential", 1: "history", 2: "state-vector"}[self.lib.sqoc_last_schedule(self.handle)]
 
+    TINY_SCHEDULES = {"auto": -1, "fused": 0, "slice-parallel": 1}
+
+    def set_tiny_schedule(self, name: str) -> None:
+        """Tiny blocks: 'auto', 'fused' (throughput) or 'slice-parallel' (latency)."""
+        _lib.check(self.lib.sqoc_set_tiny_schedule(self.handle, self.TINY_SCHEDULES[name]), "sqoc_set_tiny_schedule")
+
+    @property
+    def last_tiny_schedule(self) -> str:
+        return {-1: "none", 0: "fused", 1: "slice-parallel"}[self.lib.sqoc_last_tiny_schedule(self.handle)]
+
     @property
     def last_plan(self) -> dict:
         nb, s, m = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()

@@ -136,3 +136,25 @@ def test_lbfgs_driver_improves_cfg0():
     f0, _ = eng.objective(u0)
     res = qoc.optimize_lbfgs(eng, u0, maxiter=50)
     assert res.trace[-1] > f0
+
+
+@pytest.mark.parametrize("schedule", ["fused", "slice-parallel"])
+@pytest.mark.parametrize("cfg,kw,batch", [(0, {}, 3), (1, {"n_slices": 120}, 5), (2, {"n": 6, "n_slices": 30}, 2)])
+def test_tiny_schedules_against_oracle(schedule, cfg, kw, batch):
+    s = systems.config(cfg, **kw)
+    eng = GrapeEngine(s, max_batch=batch)
+    eng.set_tiny_schedule(schedule)
+    u = s.controls(8, batch=batch)
+    F, g = eng.objective(u)
+    assert eng.last_tiny_schedule == schedule
+    for b in range(batch):
+        Fo, go, _ = O.objective(s, u[b])
+        assert abs(F[b] - Fo) <= F_TOL
+        assert rel(g[b], go) <= G_TOL
+
+
+def test_slice_parallel_is_the_default_for_single_evaluations():
+    s = systems.config(0)
+    eng = GrapeEngine(s, max_batch=1)
+    eng.objective(s.controls(0))
+    assert eng.last_tiny_schedule == "slice-parallel"
