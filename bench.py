@@ -134,7 +134,7 @@ def _truncate(s, slices):
     return s2
 
 
-def cpu_reference(cfg: int, seconds_budget: float = 12.0, cores: int | None = None):
+def cpu_reference(cfg: int, seconds_budget: float | None = None, cores: int | None = None):
     """Time the oracle port on the host: returns (evals/s, cores, sample description).
 
     cfg 0/1: rounds of `cores` independent seeds (one process per core, 1 BLAS
@@ -144,6 +144,8 @@ def cpu_reference(cfg: int, seconds_budget: float = 12.0, cores: int | None = No
     """
     import multiprocessing as mp
 
+    if seconds_budget is None:
+        seconds_budget = float(os.environ.get("SQOC_CPU_BUDGET_S", "12"))
     cores = cores or len(os.sched_getaffinity(0))
     s = build_system_cached(cfg)
     if cfg in (2, 3, 4):

@@ -96,7 +96,8 @@ class GrapeSystem:
 
     @property
     def dt(self) -> float:
-        return self.T / self.n_slices
+        # an empty grid has no slices to scale; any positive dt is equivalent (TimeGrid, propagate.py:36-38)
+        return self.T / self.n_slices if self.n_slices else 1.0
 
     @property
     def n_controls(self) -> int:

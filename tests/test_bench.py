@@ -1,0 +1,49 @@
+"""bench.py contract pieces that run without a GPU: the reference arm and its JSON line."""
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    env = dict(os.environ, SQOC_CPU_BUDGET_S="0.5")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "0",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, env=env, timeout=600,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "config", "impl", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_cpu_reference_sampled_slices():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    v, cores, sample = bench.cpu_reference(2, seconds_budget=0.1)
+    assert v > 0 and cores == 1 and "10 of 500 slices" in sample
+
+
+def test_clock_sampler_parses_nvidia_smi_lines():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    class FakeProc:
+        def terminate(self):
+            pass
+
+        def communicate(self, timeout=None):
+            return ("1965, 1965, Not Active, Not Active, Not Active, Active\n"
+                    "1950, 1965, Not Active, Not Active, Not Active, Not Active\n", "")
+
+    c = bench.ClockSampler(0)
+    c.proc = FakeProc()
+    r = c.stop()
+    assert r["sm_max_mhz"] == 1965 and r["reasons"] == ["sw_power_cap"] and r["samples"] == 2

@@ -162,3 +162,28 @@ def test_history_chunked_scans_against_oracle():
     Fo, go, _ = O.objective(s, u)
     assert abs(F - Fo) <= F_TOL
     assert rel(g, go) <= G_TOL
+
+
+def test_empty_grid_large_block():
+    s = systems.state_transfer_ring(6, 1.0, 0, seed=3, full=True)
+    eng = GrapeEngine(s, max_batch=1)
+    F, g = eng.objective(np.zeros((2, 0)))
+    assert g.shape == (2, 0)
+    assert abs(F - abs(np.vdot(s.targets[0], s.initial[0])) ** 2) <= 1e-15
+
+
+def test_batch_over_max_batch_is_a_value_error():
+    s = systems.config(2, n_slices=4)
+    eng = GrapeEngine(s, max_batch=1)
+    with pytest.raises(ValueError):
+        eng.objective(s.controls(0, batch=2))
+
+
+def test_large_batch_of_two_matches_two_singles():
+    s = systems.config(2, n_slices=8)
+    eng = GrapeEngine(s, max_batch=2)
+    u = s.controls(4, batch=2)
+    F, g = eng.objective(u)
+    for b in range(2):
+        Fb, gb = eng.objective(u[b])
+        assert abs(F[b] - Fb) <= 1e-13 and rel(g[b], gb) <= 1e-12
