@@ -83,7 +83,9 @@ int sqoc_set_norm_bounds(sqoc_problem* p, const double* bounds);
 /* Large-block schedule: -1 auto (default), 0 slice-sequential (no history; memory
  * O(sum d_b^2)), 1 history (all slices resident, slice-batched GEMMs; memory
  * O(N sum d_b^2)), 2 state-vector (state objective only: U_j history, psi/chi
- * sweeps and an augmented Taylor action for the gradient; memory O(N sum d_b^2)).
+ * sweeps and an augmented Taylor action for the gradient; memory O(N sum d_b^2)),
+ * 3 matrix-free (state objective only, opt-in: psi/chi sweeps by Taylor actions of A_j,
+ * no propagator is formed; memory O(N sum d_b)).
  * sqoc_last_schedule reports what the last sqoc_eval used (-1 = no large blocks). */
 int sqoc_set_schedule(sqoc_problem* p, int schedule);
 int sqoc_last_schedule(const sqoc_problem* p);

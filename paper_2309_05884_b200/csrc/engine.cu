@@ -608,7 +608,8 @@ int sqoc_set_norm_bounds(sqoc_problem* p, const double* bounds) {
 }
 
 int sqoc_set_schedule(sqoc_problem* p, int schedule) {
-  if (!p || schedule < -1 || schedule > 2) return fail(SQOC_ERR_ARG, "schedule must be -1 (auto), 0, 1 or 2");
+  if (!p || schedule < -1 || schedule > 3) return fail(SQOC_ERR_ARG, "schedule must be -1 (auto), 0, 1, 2 or 3");
+  if (schedule == 3 && p->objective != SQOC_OBJ_STATE) return fail(SQOC_ERR_ARG, "matrix-free needs the state objective");
   if (p->large) p->large->force_mode = schedule;
   return SQOC_OK;
 }

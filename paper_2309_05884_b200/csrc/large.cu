@@ -600,7 +600,7 @@ void large_free(LargeGroup& g) {
   for (auto m : g.gentall_mem) cudaFree(m);
   g.gentall_mem.clear();
   cudaFree(g.gentall_dev);
-  double2* sv[] = {g.sv_U, g.sv_chunk, g.sv_psi, g.sv_chi, g.sv_V, g.sv_W, g.sv_acc, g.sv_g};
+  double2* sv[] = {g.sv_U, g.sv_chunk, g.sv_psi, g.sv_chi, g.sv_V, g.sv_W, g.sv_acc, g.sv_g, g.mf_t};
   for (auto x : sv) cudaFree(x);
   cudaFree(g.gent_dev);
   for (auto m : g.hlist_mem) cudaFree(m);
@@ -963,16 +963,19 @@ static size_t sv_fixed_bytes(const LargeGroup& g) {
                             K * N * g.totalr + N * g.nblk * K);
 }
 
-static int sv_alloc(LargeGroup& g) {
-  if (g.sv_U) return SQOC_OK;
+static int sv_alloc(LargeGroup& g, bool with_u) {
   const size_t N = g.N, K = g.K;
+  if (!g.sv_psi) {  // vector histories + augmented-action buffers (shared by modes 2 and 3)
+    LCHK(cudaMalloc(&g.sv_psi, (N + 1) * g.totalr * sizeof(double2)));
+    LCHK(cudaMalloc(&g.sv_chi, (N + 1) * g.totalr * sizeof(double2)));
+    LCHK(cudaMalloc(&g.sv_V, (K + 1) * N * g.totalr * sizeof(double2)));
+    LCHK(cudaMalloc(&g.sv_W, (K + 1) * (K + 1) * N * g.totalr * sizeof(double2)));
+    LCHK(cudaMalloc(&g.sv_acc, K * N * g.totalr * sizeof(double2)));
+    LCHK(cudaMalloc(&g.sv_g, N * g.nblk * K * sizeof(double2)));
+    LCHK(cudaMalloc(&g.mf_t, 3 * g.totalr * sizeof(double2)));
+  }
+  if (!with_u || g.sv_U) return SQOC_OK;
   LCHK(cudaMalloc(&g.sv_U, N * g.total * sizeof(double2)));
-  LCHK(cudaMalloc(&g.sv_psi, (N + 1) * g.totalr * sizeof(double2)));
-  LCHK(cudaMalloc(&g.sv_chi, (N + 1) * g.totalr * sizeof(double2)));
-  LCHK(cudaMalloc(&g.sv_V, (K + 1) * N * g.totalr * sizeof(double2)));
-  LCHK(cudaMalloc(&g.sv_W, (K + 1) * (K + 1) * N * g.totalr * sizeof(double2)));
-  LCHK(cudaMalloc(&g.sv_acc, K * N * g.totalr * sizeof(double2)));
-  LCHK(cudaMalloc(&g.sv_g, N * g.nblk * K * sizeof(double2)));
   size_t free_b = 0, total_b = 0;
   LCHK(cudaMemGetInfo(&free_b, &total_b));
   const size_t per_slice = 5 * g.total * sizeof(double2);
@@ -1060,6 +1063,8 @@ static int taylor_terms(double beta) {
   return 200;
 }
 
+static int sv_gradient(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, double bound, cudaStream_t st);
+
 static int large_eval_state_vector(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, int nb, int sq,
                                    double bound, cudaStream_t st) {
   const int K = g.K, N = g.N, nblk = g.nblk;
@@ -1111,7 +1116,18 @@ static int large_eval_state_vector(LargeGroup& g, const LargeArgs& a, int s_idx,
   if (done) return SQOC_OK;
   for (int i = N - 1; i >= 0; --i)
     if ((rc = svgemm(g, SV_CHI, 0, 0, i, i + 1, one, st))) return rc;
-  // ---- dtau/du_k,i = <chi_{i+1}| L(A_i, a_k) |psi_i> by the augmented Taylor action ----
+  return sv_gradient(g, a, s_idx, u, bound, st);
+}
+
+// dtau/du_k,i = <chi_{i+1}| L(A_i, a_k) |psi_i> for every slice by the augmented Taylor action
+// exp([[A, a_k],[0, A]]) [0; psi] (top block = L(A, a_k) psi), batched over slices as GEMMs
+// W_k = V a_k^T; needs the psi / chi histories in sv_psi / sv_chi.
+static int sv_gradient(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, double bound, cudaStream_t st) {
+  const int K = g.K, N = g.N, nblk = g.nblk;
+  int maxd = 0;
+  for (auto& b : g.blocks) maxd = std::max(maxd, b.d);
+  int rc;
+  GemmArgs one{1.0, 0.0, 0.0, 0.0};
   double emax = 0.0;
   for (auto& b : g.blocks)
     for (int k = 1; k <= K; ++k) emax = std::max(emax, b.gen_norm[k]);
@@ -1138,6 +1154,107 @@ static int large_eval_state_vector(LargeGroup& g, const LargeArgs& a, int s_idx,
   return SQOC_OK;
 }
 
+// ------------------------------------------------------------------ matrix-free state schedule
+// y = sgn A t for every block (one warp per row, coalesced rows of the dense A); t_out = y * scale;
+// acc += t_out.  HBM-bound: one read of A per Taylor term.
+__global__ void mv_taylor_kernel(int nblk, const int* __restrict__ dims, const size_t* __restrict__ off,
+                                 const size_t* __restrict__ offr, const double2* __restrict__ A,
+                                 const double2* __restrict__ tin, double2* __restrict__ tout,
+                                 double2* __restrict__ acc, double scale) {
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.y;
+  const int d = dims[b];
+  const double2* Ab = A + off[b];
+  const double2* t = tin + offr[b];
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < d; row += gridDim.x * warps) {
+    const double2* ar = Ab + (size_t)row * d;
+    double sx = 0.0, sy = 0.0;
+    for (int c = lane; c < d; c += 32) {
+      const double2 x = __ldg(ar + c), v = __ldg(t + c);
+      sx = fma(x.x, v.x, sx);
+      sx = fma(-x.y, v.y, sx);
+      sy = fma(x.x, v.y, sy);
+      sy = fma(x.y, v.x, sy);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sx += __shfl_xor_sync(0xffffffffu, sx, o);
+      sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    }
+    if (lane == 0) {
+      const double2 y = make_double2(sx * scale, sy * scale);
+      tout[offr[b] + row] = y;
+      double2 z = acc[offr[b] + row];
+      acc[offr[b] + row] = make_double2(z.x + y.x, z.y + y.y);
+    }
+  }
+}
+
+__global__ void vcopy_kernel(size_t n, const double2* __restrict__ a, double2* __restrict__ b, double2* __restrict__ c) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    b[i] = a[i];
+    if (c) c[i] = a[i];
+  }
+}
+
+// exp(sgn A) applied to `in` -> `out` by sigma substeps of a degree-m Taylor action (A in g.A)
+static int mf_action(LargeGroup& g, double sgn, int m, int sigma, const double2* in, double2* out, cudaStream_t st) {
+  int maxd = 0;
+  for (auto& b : g.blocks) maxd = std::max(maxd, b.d);
+  double2 *t0 = g.mf_t, *t1 = g.mf_t + g.totalr;
+  const unsigned vg = (unsigned)std::min<size_t>((g.totalr + 255) / 256, 1024);
+  vcopy_kernel<<<vg, 256, 0, st>>>(g.totalr, in, out, t0);  // acc = t = in
+  LCHK(cudaGetLastError());
+  g.launches++;
+  const dim3 grid((unsigned)std::max(1, std::min((maxd + 7) / 8, 1184)), g.nblk);
+  for (int sub = 0; sub < sigma; ++sub) {
+    if (sub > 0) {
+      vcopy_kernel<<<vg, 256, 0, st>>>(g.totalr, out, t0, nullptr);
+      LCHK(cudaGetLastError());
+      g.launches++;
+    }
+    for (int l = 1; l <= m; ++l) {
+      mv_taylor_kernel<<<grid, 256, 0, st>>>(g.nblk, g.d_dev, g.off_dev, g.offr_dev, g.A, t0, t1, out,
+                                             sgn / (sigma * (double)l));
+      LCHK(cudaGetLastError());
+      g.launches++;
+      std::swap(t0, t1);
+    }
+  }
+  return SQOC_OK;
+}
+
+static int large_eval_matrix_free(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, double bound,
+                                  cudaStream_t st) {
+  const int K = g.K, N = g.N, nblk = g.nblk;
+  int maxd = 0;
+  for (auto& b : g.blocks) maxd = std::max(maxd, b.d);
+  const dim3 ew_grid((unsigned)std::min<size_t>(((size_t)maxd * maxd + 255) / 256, 4096), nblk);
+  int sigma = std::max(1, (int)std::ceil(bound / 3.0));
+  const int m = taylor_terms(bound / sigma);
+  g.last_taylor_terms = m;
+  int rc;
+  if ((rc = bc_init(g, g.sv_psi, g.sv_chi + (size_t)N * g.totalr, dim3(ew_grid.x, nblk), st))) return rc;
+  for (int j = 0; j < N; ++j) {  // psi_{j+1} = exp(A_j) psi_j
+    build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, 1.0, g.A, 0);
+    LCHK(cudaGetLastError());
+    g.launches++;
+    if ((rc = mf_action(g, 1.0, m, sigma, g.sv_psi + (size_t)j * g.totalr, g.sv_psi + (size_t)(j + 1) * g.totalr, st)))
+      return rc;
+  }
+  bool done = false;
+  if ((rc = bc_tau(g, g.sv_psi + (size_t)N * g.totalr, a, s_idx, st, &done))) return rc;
+  if (done) return SQOC_OK;
+  for (int j = N - 1; j >= 0; --j) {  // chi_j = exp(A_j)^dag chi_{j+1} = exp(-A_j) chi_{j+1} (A anti-Hermitian)
+    build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, 1.0, g.A, 0);
+    LCHK(cudaGetLastError());
+    g.launches++;
+    if ((rc = mf_action(g, -1.0, m, sigma, g.sv_chi + (size_t)(j + 1) * g.totalr, g.sv_chi + (size_t)j * g.totalr, st)))
+      return rc;
+  }
+  return sv_gradient(g, a, s_idx, u, bound, st);
+}
+
 int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
   const int K = g.K, N = g.N, nblk = g.nblk;
   int maxd = 0;
@@ -1160,6 +1277,14 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
     choose_taylor_host(bound, nb, sq);
     g.last_nb = nb;
     g.last_s = sq;
+    if (!g.gate && N > 0 && g.force_mode == 3) {  // matrix-free state schedule (opt-in)
+      int rc = sv_alloc(g, false);
+      if (rc != SQOC_OK) return rc;
+      g.mode = 3;
+      rc = large_eval_matrix_free(g, a, s, u, bound, st);
+      if (rc != SQOC_OK) return rc;
+      continue;
+    }
     if (!g.gate && N > 0 && g.force_mode != 0 && g.force_mode != 1) {  // state-vector schedule
       bool use_sv = g.force_mode == 2;
       if (!use_sv) {
@@ -1169,7 +1294,7 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
         use_sv = sv_fixed_bytes(g) + 5 * g.total * sizeof(double2) <= (size_t)(0.7 * (double)(free_b + have));
       }
       if (use_sv) {
-        int rc = sv_alloc(g);
+        int rc = sv_alloc(g, true);
         if (rc != SQOC_OK) return rc;
         g.mode = 2;
         rc = large_eval_state_vector(g, a, s, u, nb, sq, bound, st);

@@ -100,6 +100,7 @@ struct LargeGroup {
   double2* sv_W = nullptr;          // [K+1] x same shape as sv_V
   double2* sv_acc = nullptr;        // per block: [K N][d_b]
   double2* sv_g = nullptr;          // [N][nblk][K]
+  double2* mf_t = nullptr;          // matrix-free schedule: Taylor term vectors [3][totalr]
   const double2** gentall_dev = nullptr;  // per block a_k^T for k = 0..K
   std::vector<void*> gentall_mem;
   int last_nb = 0, last_s = 0, last_taylor_terms = 0;
@@ -109,8 +110,8 @@ struct LargeGroup {
   const double2** bc_l_dev = nullptr;     // device array of per-block Lam_end pointers, or null
   const double2* bc_tau = nullptr;        // device [nblk] full-grid tau_b, or null
   std::vector<double2*> fwd_out;          // forward-only: X_N of each block copied here
-  int mode = -1;                    // last schedule used: 0 sequential, 1 history, 2 state-vector
-  int force_mode = -1;              // -1 auto, 0 sequential, 1 history, 2 state-vector
+  int mode = -1;                    // last schedule used: 0 sequential, 1 history, 2 state-vector, 3 matrix-free
+  int force_mode = -1;              // -1 auto, 0 sequential, 1 history, 2 state-vector, 3 matrix-free
   int launches = 0;
   std::string err;
 };

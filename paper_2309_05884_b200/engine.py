@@ -107,7 +107,7 @@ class GrapeEngine:
         tiny_max = self.lib.sqoc_tiny_max_dim()
         return [b for b, d in enumerate(self.dims) if d > tiny_max]
 
-    SCHEDULES = {"auto": -1, "sequential": 0, "history": 1, "state-vector": 2}
+    SCHEDULES = {"auto": -1, "sequential": 0, "history": 1, "state-vector": 2, "matrix-free": 3}
 
     def set_schedule(self, name: str) -> None:
         """Large-block schedule: 'auto', 'sequential' (O(sum d^2) memory) or 'history' (slice-batched)."""
@@ -115,7 +115,8 @@ class GrapeEngine:
 
     @property
     def last_schedule(self) -> str:
-        return {-1: "none", 0: "sequential", 1: "history", 2: "state-vector"}[self.lib.sqoc_last_schedule(self.handle)]
+        return {-1: "none", 0: "sequential", 1: "history", 2: "state-vector", 3: "matrix-free"}[
+            self.lib.sqoc_last_schedule(self.handle)]
 
     TINY_SCHEDULES = {"auto": -1, "fused": 0, "slice-parallel": 1}
 

@@ -76,7 +76,7 @@ def test_cfg2_full_grid_fidelity_and_fd_gradient():
         assert abs(fd - g[k, j]) / max(abs(fd), abs(g[k, j]), rms) < 1e-6
 
 
-@pytest.mark.parametrize("schedule", SCHEDULES + ["state-vector"])
+@pytest.mark.parametrize("schedule", SCHEDULES + ["state-vector", "matrix-free"])
 def test_state_transfer_full_space_d64_against_oracle(schedule):
     s = systems.state_transfer_ring(6, 10.0, 40, seed=3, full=True)  # 64 x 64 dense
     eng = GrapeEngine(s, max_batch=1)
@@ -116,6 +116,11 @@ def test_cfg4_short_grid_schedules_agree():
     F2, g2 = eng.objective(u)
     assert abs(F1 - F2) <= F_TOL
     assert rel(g1, g2) <= G_TOL
+    eng.set_schedule("matrix-free")
+    F3, g3 = eng.objective(u)
+    assert eng.last_schedule == "matrix-free"
+    assert abs(F1 - F3) <= F_TOL
+    assert rel(g1, g3) <= G_TOL
 
 
 @pytest.mark.parametrize("world", [2, 3])

@@ -12,6 +12,8 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 kw = {"n_slices": int(sys.argv[4])} if len(sys.argv) > 4 else {}
 s = systems.config(cfg, **kw)
 eng = GrapeEngine(s, max_batch=batch)
+if len(sys.argv) > 5:
+    eng.set_schedule(sys.argv[5])
 u = torch.from_numpy(s.controls(0, batch=batch)).cuda()
 F = torch.empty(batch, dtype=torch.float64, device="cuda")
 g = torch.empty_like(u)
