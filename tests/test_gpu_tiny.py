@@ -158,3 +158,20 @@ def test_slice_parallel_is_the_default_for_single_evaluations():
     eng = GrapeEngine(s, max_batch=1)
     eng.objective(s.controls(0))
     assert eng.last_tiny_schedule == "slice-parallel"
+
+
+def test_integration_md_ctypes_stub_runs(golden):
+    """The reference-side binding shown in INTEGRATION.md works as written."""
+    import os
+    import re
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "INTEGRATION.md")).read()
+    code = re.search(r"## 2\..*?```python\n(.*?)```", text, re.S).group(1)
+    code = code.replace("/path/to/libsymqoc_b200.so", os.path.join(root, "paper_2309_05884_b200", "libsymqoc_b200.so"))
+    ns = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    g = lambda k: golden[f"cfg0_{k}"]  # noqa: E731
+    gx, gy, p = ns["gradient"](g("psi0"), g("psif"), g("u")[0], g("u")[1], Duck(g("h0"), g("hx"), g("hy")), 0.1)
+    assert abs(p - float(g("P"))) <= F_TOL
+    assert rel(np.concatenate([gx, gy]), np.concatenate([g("gx"), g("gy")])) <= G_TOL
