@@ -192,3 +192,25 @@ def test_large_batch_of_two_matches_two_singles():
     for b in range(2):
         Fb, gb = eng.objective(u[b])
         assert abs(F[b] - Fb) <= 1e-13 and rel(g[b], gb) <= 1e-12
+
+
+def test_gradient_finite_difference_100_probes_mixed_blocks():
+    """Acceptance-criterion-5 style (test_acceptance.py:119-156): >= 100 central-difference probes,
+    worst relative error <= 1e-6 (denominator floored by the gradient RMS), on a gate system whose
+    blocks go through both the tiny kernel (d = 6, 13) and the DMMA path (d = 21 .. 33)."""
+    s = systems.gate_ring(8, 10.0 * 60 / 500, 60, seed=9)
+    eng = GrapeEngine(s, max_batch=1)
+    u = s.controls(5)
+    F, g = eng.objective(u)
+    rms = np.sqrt(np.mean(g**2))
+    h = 1e-6
+    worst, probes = 0.0, 0
+    for j in range(0, 60, 1):
+        for k in range(2):
+            up, um = u.copy(), u.copy()
+            up[k, j] += h
+            um[k, j] -= h
+            fd = (eng.objective(up)[0] - eng.objective(um)[0]) / (2 * h)
+            worst = max(worst, abs(fd - g[k, j]) / max(abs(fd), abs(g[k, j]), rms))
+            probes += 1
+    assert probes >= 100 and worst <= 1e-6, worst
