@@ -32,12 +32,16 @@ namespace sqoc {
 constexpr int kTinyMaxDim = 16;
 constexpr int kTinyBuffers = 8;   // d x d matrices per problem in shared memory
 constexpr int kMaxControls = 4;
-constexpr int kLaneRows = 4;      // lane grid rows (tile rows)
-// Lanes per problem: 16 (4 x 4 grid, two problems per warp) or 32 (4 x 8, one per warp).
-// Chosen by measurement (r01, cfg1 with the 7 sector kernels running concurrently): 16 lanes
-// for every d <= 12 gave 352 ms per 4096-seed batch vs 365 ms for the per-sector serial optimum
-// and 386 ms for 32 lanes everywhere.
-__host__ __device__ constexpr int tiny_lanes(int d) { return d <= 12 ? 16 : 32; }
+// Lane grid per problem: LR x LC lanes, each owning a TSR x TSC register tile (rows tr + LR i,
+// cols tc + LC j).  Chosen to minimise padded work per warp: square 3 x 3 grids (three problems
+// per warp) make d = 3, 6, 9 exact and d = 5 nearly so; 4 x 4 grids (two per warp) fit d = 4, 7,
+// 8, 10..12; d >= 13 uses one warp per problem as 4 x 8.  (r01 measurements: 16 lanes for all
+// d <= 12 ran cfg1 in 352 ms vs 386 ms with 32 lanes everywhere.)
+__host__ __device__ constexpr int tiny_lr(int d) {
+  return d == 1 ? 1 : d == 2 ? 2 : (d == 3 || d == 5 || d == 6 || d == 9) ? 3 : 4;
+}
+__host__ __device__ constexpr int tiny_lc(int d) { return d >= 13 ? 8 : tiny_lr(d); }
+__host__ __device__ constexpr int tiny_lanes(int d) { return tiny_lr(d) * tiny_lc(d); }
 constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
 
@@ -94,19 +98,38 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
 
+__host__ __device__ constexpr bool is_pow2(int x) { return (x & (x - 1)) == 0; }
+
+// Sum over the LP lanes of one problem (lanes base .. base+LP-1); every lane of the group gets
+// the same value, accumulated in a fixed order (deterministic).
 template <int LP>
-__device__ __forceinline__ double prob_sum(double v) {  // sum over the LP lanes of one problem, fixed tree
+__device__ __forceinline__ double prob_sum(double v) {
+  if (is_pow2(LP)) {
 #pragma unroll
-  for (int o = LP / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+    for (int o = LP / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  }
+  const int base = ((threadIdx.x & 31) / LP) * LP;
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < LP; ++i) s += __shfl_sync(0xffffffffu, v, (base + i) & 31);
+  return s;
 }
 template <int LP>
 __device__ __forceinline__ double2 prob_sum2(double2 v) { return make_double2(prob_sum<LP>(v.x), prob_sum<LP>(v.y)); }
+// Sum over the LC lanes sharing a tile row (lanes base .. base+LC-1 with base a multiple of LC)
 template <int LC>
-__device__ __forceinline__ double row_sum(double v) {  // sum over the LC lanes sharing a tile row
+__device__ __forceinline__ double row_sum(double v) {
+  if (is_pow2(LC)) {
 #pragma unroll
-  for (int o = 1; o < LC; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+    for (int o = 1; o < LC; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  }
+  const int base = ((threadIdx.x & 31) / LC) * LC;
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < LC; ++i) s += __shfl_sync(0xffffffffu, v, (base + i) & 31);
+  return s;
 }
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
@@ -118,14 +141,14 @@ __device__ __forceinline__ double warp_max(double v) {
 // (ld D).  The interleaved ownership makes the 8 lanes of a tile row read 8 consecutive
 // complex values of a matrix row in one LDS.128 wavefront (no bank conflict).
 // Indices are clamped into range so padding lanes read valid memory (never stored).
-template <int D, int TSR, int TSC, int LC>
+template <int D, int TSR, int TSC, int LR, int LC>
 struct Tile {
   int tr, tc;
-  __device__ __forceinline__ int row(int i) const { return min(tr + kLaneRows * i, D - 1); }
+  __device__ __forceinline__ int row(int i) const { return min(tr + LR * i, D - 1); }
   __device__ __forceinline__ int col(int j) const { return min(tc + LC * j, D - 1); }
-  __device__ __forceinline__ bool ok(int i, int j) const { return tr + kLaneRows * i < D && tc + LC * j < D; }
-  __device__ __forceinline__ bool row_ok(int i) const { return tr + kLaneRows * i < D; }
-  __device__ __forceinline__ int rrow(int i) const { return tr + kLaneRows * i; }  // unclamped
+  __device__ __forceinline__ bool ok(int i, int j) const { return tr + LR * i < D && tc + LC * j < D; }
+  __device__ __forceinline__ bool row_ok(int i) const { return tr + LR * i < D; }
+  __device__ __forceinline__ int rrow(int i) const { return tr + LR * i; }  // unclamped
   __device__ __forceinline__ int rcol(int j) const { return tc + LC * j; }
 
   __device__ __forceinline__ void zero(double2 (&t)[TSR][TSC]) const {
@@ -213,16 +236,18 @@ struct Tile {
 template <int D, bool GATE>
 struct TinyCtx {
   static constexpr int R = GATE ? D : 1;  // columns of X and Lam
-  static constexpr int LP = tiny_lanes(D);
-  static constexpr int LC = LP / kLaneRows;
+  static constexpr int LR = tiny_lr(D);
+  static constexpr int LC = tiny_lc(D);
+  static constexpr int LP = LR * LC;
   static constexpr int PPW = 32 / LP;
-  static constexpr int TSR = (D + kLaneRows - 1) / kLaneRows;
+  static constexpr int TSR = (D + LR - 1) / LR;
   static constexpr int TSC = (D + LC - 1) / LC;
   static constexpr int DD = D * D;
   using T2 = double2[TSR][TSC];
 
-  Tile<D, TSR, TSC, LC> tl;
+  Tile<D, TSR, TSC, LR, LC> tl;
   int K, N, q, sub;
+  bool act;  // lane belongs to a problem group (lanes past PPW * LP idle and never store)
   const double2* gen;  // (K+1) DD in smem
   double2 *B0, *B1, *B2, *B3, *B4, *B5, *B6, *B7;
   const double* up;  // this problem's u [K][N]
@@ -230,9 +255,10 @@ struct TinyCtx {
 
   __device__ __forceinline__ void init(const double2* gen_smem, double2* buf, int K_, int N_) {
     const int lane = threadIdx.x & 31;
-    sub = lane / LP;
-    q = lane % LP;
-    tl = Tile<D, TSR, TSC, LC>{q / LC, q % LC};
+    act = lane < PPW * LP;
+    sub = act ? lane / LP : 0;
+    q = act ? lane % LP : 0;
+    tl = Tile<D, TSR, TSC, LR, LC>{q / LC, q % LC};
     gen = gen_smem;
     K = K_;
     N = N_;
@@ -301,26 +327,26 @@ struct TinyCtx {
   __device__ __forceinline__ void expm_plain(int nb, int s) const {
     T2 t;
     tl.mul(t, B2, B2);  // A2
-    tl.store(B1, t, true);
+    tl.store(B1, t, act);
     __syncwarp();
     tl.mul(t, B1, B2);  // A3
-    tl.store(B4, t, true);
+    tl.store(B4, t, act);
     __syncwarp();
     scale(t, c_inv_fact[3 * nb]);  // T = c_{3nb} A3 + Q_{nb-1}
     add_q(t, nb - 1, B2, B1);
-    tl.store(B6, t, true);
+    tl.store(B6, t, act);
     for (int qi = nb - 2; qi >= 0; --qi) {
       __syncwarp();
       tl.mul(t, B6, B4);
       add_q(t, qi, B2, B1);
       __syncwarp();
-      tl.store(B6, t, true);
+      tl.store(B6, t, act);
     }
     for (int r = 0; r < s; ++r) {
       __syncwarp();
       tl.mul(t, B6, B6);
       __syncwarp();
-      tl.store(B6, t, true);
+      tl.store(B6, t, act);
     }
     __syncwarp();
   }
@@ -330,34 +356,34 @@ struct TinyCtx {
   __device__ __forceinline__ void expm_pair(int nb, int s) const {
     T2 t, dt;
     tl.pair(t, dt, B2, B3, B2, B3);  // (A2, dA2)
-    tl.store(B0, t, true);
-    tl.store(B1, dt, true);
+    tl.store(B0, t, act);
+    tl.store(B1, dt, act);
     __syncwarp();
     tl.pair(t, dt, B0, B1, B2, B3);  // (A3, dA3)
-    tl.store(B4, t, true);
-    tl.store(B5, dt, true);
+    tl.store(B4, t, act);
+    tl.store(B5, dt, act);
     __syncwarp();
     scale(t, c_inv_fact[3 * nb]);
     scale(dt, c_inv_fact[3 * nb]);
     add_q(t, nb - 1, B2, B0);
     add_dq(dt, nb - 1, B3, B1);
-    tl.store(B6, t, true);
-    tl.store(B7, dt, true);
+    tl.store(B6, t, act);
+    tl.store(B7, dt, act);
     for (int qi = nb - 2; qi >= 0; --qi) {
       __syncwarp();
       tl.pair(t, dt, B6, B7, B4, B5);
       add_q(t, qi, B2, B0);
       add_dq(dt, qi, B3, B1);
       __syncwarp();
-      tl.store(B6, t, true);
-      tl.store(B7, dt, true);
+      tl.store(B6, t, act);
+      tl.store(B7, dt, act);
     }
     for (int r = 0; r < s; ++r) {
       __syncwarp();
       tl.pair(t, dt, B6, B7, B6, B7);
       __syncwarp();
-      tl.store(B6, t, true);
-      tl.store(B7, dt, true);
+      tl.store(B6, t, act);
+      tl.store(B7, dt, act);
     }
     __syncwarp();
   }
@@ -379,7 +405,7 @@ struct TinyCtx {
         for (int jj = 0; jj < TSC; ++jj) cfma(t[i][jj], l[i], m[jj]);
     }
     scale(t, ldexp(1.0, -s));
-    tl.store(B3, t, true);
+    tl.store(B3, t, act);
     __syncwarp();
   }
 
@@ -407,7 +433,7 @@ struct TinyCtx {
       if (adj) tl.mul_adj(t, U, Y);
       else tl.mul(t, U, Y);
       __syncwarp();
-      tl.store(Yout, t, true);
+      tl.store(Yout, t, act);
     } else {
       double2 v[TSR];
 #pragma unroll
@@ -423,7 +449,7 @@ struct TinyCtx {
 #pragma unroll
       for (int i = 0; i < TSR; ++i) v[i] = make_double2(row_sum<LC>(v[i].x), row_sum<LC>(v[i].y));
       __syncwarp();
-      if (tl.tc == 0) {
+      if (act && tl.tc == 0) {
 #pragma unroll
         for (int i = 0; i < TSR; ++i)
           if (tl.row_ok(i)) Yout[tl.rrow(i)] = v[i];
@@ -433,6 +459,7 @@ struct TinyCtx {
 
   // copy a D x R matrix (own entries)
   __device__ __forceinline__ void copy_x(double2* dst, const double2* src) const {
+    if (!act) return;
     if (GATE) {
 #pragma unroll
       for (int i = 0; i < TSR; ++i)
@@ -446,6 +473,7 @@ struct TinyCtx {
     }
   }
   __device__ __forceinline__ void copy_dd(double2* dst, const double2* src) const {  // D x D, own tile
+    if (!act) return;
 #pragma unroll
     for (int i = 0; i < TSR; ++i)
 #pragma unroll
@@ -458,7 +486,7 @@ struct TinyCtx {
     for (int i = 0; i < TSR; ++i)
 #pragma unroll
       for (int jj = 0; jj < TSC; ++jj) t[i][jj] = make_double2(tl.rrow(i) == tl.rcol(jj) ? 1.0 : 0.0, 0.0);
-    tl.store(X, t, true);
+    tl.store(X, t, act);
   }
   // <V, X>_F over the problem's lanes
   __device__ __forceinline__ double2 overlap(const double2* V, const double2* X) const {
@@ -499,11 +527,10 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   double2* gen = load_generators<D>(p);
   const int warp = threadIdx.x >> 5;
   C c;
-  const int lane = threadIdx.x & 31;
-  const int sub = lane / C::LP;
-  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + sub) * kTinyBuffers * C::DD, K, N);
-  const int slot = (blockIdx.x * p.nwarps + warp) * C::PPW + sub;  // park is sized for all slots
-  c.real = slot < p.batch;                                         // owns a real problem (may store globally)
+  c.init(gen, nullptr, K, N);
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * kTinyBuffers * C::DD, K, N);
+  const int slot = (blockIdx.x * p.nwarps + warp) * C::PPW + c.sub;  // park is sized for all slots
+  c.real = c.act && slot < p.batch;                                  // owns a real problem (may store globally)
   const int prob = c.real ? slot : p.batch - 1;                    // padding slots replay the last problem's u
   c.up = p.u + (size_t)prob * K * N;
   double2* parkX = p.park + (size_t)slot * 2 * D * R;
@@ -518,7 +545,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   for (int j = 0; j < N; ++j) {
     int nb, s;
     c.build_a(j, t, nb, s);
-    c.tl.store(c.B2, t, true);
+    c.tl.store(c.B2, t, c.act);
     __syncwarp();
     c.expm_plain(nb, s);
     c.mul_x(c.B6, false, X, X);  // X_j = U_j X_{j-1}
@@ -537,7 +564,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
     c.copy_x(c.B0, parkX);  // stage X_j, Lam_j
     c.copy_x(c.B1, parkL);
     c.build_a(j, t, nb, s);
-    c.tl.store(c.B2, t, true);
+    c.tl.store(c.B2, t, c.act);
     __syncwarp();
     c.seed_c(s);
     c.expm_pair(nb, s);
@@ -575,17 +602,17 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_expm_kernel(TinySl
   double2* gen = load_generators<D>(p);
   const int warp = threadIdx.x >> 5;
   C c;
-  const int sub = (threadIdx.x & 31) / C::LP;
-  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + sub) * kTinyBuffers * C::DD, K, N);
-  const int item_raw = (blockIdx.x * p.nwarps + warp) * C::PPW + sub;
-  c.real = item_raw < sp.units;
+  c.init(gen, nullptr, K, N);
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * kTinyBuffers * C::DD, K, N);
+  const int item_raw = (blockIdx.x * p.nwarps + warp) * C::PPW + c.sub;
+  c.real = c.act && item_raw < sp.units;
   const int item = c.real ? item_raw : sp.units - 1;
   const int prob = item / N, j = item % N;
   c.up = p.u + (size_t)prob * K * N;
   typename C::T2 t;
   int nb, s;
   c.build_a(j, t, nb, s);
-  c.tl.store(c.B2, t, true);
+  c.tl.store(c.B2, t, c.act);
   __syncwarp();
   c.expm_plain(nb, s);
   if (c.real) c.copy_dd(sp.Uh + (size_t)item * C::DD, c.B6);
@@ -601,10 +628,10 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_sweep_kernel(TinyS
   double2* gen = load_generators<D>(p);
   const int warp = threadIdx.x >> 5;
   C c;
-  const int sub = (threadIdx.x & 31) / C::LP;
-  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + sub) * kTinyBuffers * C::DD, K, N);
-  const int slot = (blockIdx.x * p.nwarps + warp) * C::PPW + sub;
-  c.real = slot < p.batch;
+  c.init(gen, nullptr, K, N);
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * kTinyBuffers * C::DD, K, N);
+  const int slot = (blockIdx.x * p.nwarps + warp) * C::PPW + c.sub;
+  c.real = c.act && slot < p.batch;
   const int prob = c.real ? slot : p.batch - 1;
   const double2* U = sp.Uh + (size_t)prob * N * C::DD;
   double2* Xh = sp.Xh + (size_t)prob * (N + 1) * D * R;
@@ -646,10 +673,10 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_grad_kernel(TinySl
   double2* gen = load_generators<D>(p);
   const int warp = threadIdx.x >> 5;
   C c;
-  const int sub = (threadIdx.x & 31) / C::LP;
-  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + sub) * kTinyBuffers * C::DD, K, N);
-  const int item_raw = (blockIdx.x * p.nwarps + warp) * C::PPW + sub;
-  c.real = item_raw < sp.units;
+  c.init(gen, nullptr, K, N);
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * kTinyBuffers * C::DD, K, N);
+  const int item_raw = (blockIdx.x * p.nwarps + warp) * C::PPW + c.sub;
+  c.real = c.act && item_raw < sp.units;
   const int item = c.real ? item_raw : sp.units - 1;
   const int prob = item / N, j = item % N;
   c.up = p.u + (size_t)prob * K * N;
@@ -659,7 +686,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_grad_kernel(TinySl
   typename C::T2 t;
   int nb, s;
   c.build_a(j, t, nb, s);
-  c.tl.store(c.B2, t, true);
+  c.tl.store(c.B2, t, c.act);
   __syncwarp();
   c.seed_c(s);
   c.expm_pair(nb, s);
