@@ -33,13 +33,12 @@ constexpr int kTinyMaxDim = 16;
 constexpr int kTinyBuffers = 8;   // d x d matrices per problem in shared memory
 constexpr int kMaxControls = 4;
 // Lane grid per problem: LR x LC lanes, each owning a TSR x TSC register tile (rows tr + LR i,
-// cols tc + LC j).  Chosen to minimise padded work per warp: square 3 x 3 grids (three problems
-// per warp) make d = 3, 6, 9 exact and d = 5 nearly so; 4 x 4 grids (two per warp) fit d = 4, 7,
-// 8, 10..12; d >= 13 uses one warp per problem as 4 x 8.  (r01 measurements: 16 lanes for all
-// d <= 12 ran cfg1 in 352 ms vs 386 ms with 32 lanes everywhere.)
-__host__ __device__ constexpr int tiny_lr(int d) {
-  return d == 1 ? 1 : d == 2 ? 2 : (d == 3 || d == 5 || d == 6 || d == 9) ? 3 : 4;
-}
+// cols tc + LC j).  Measured per sector (r01, cfg1 at N_t=100, serialised): 3 x 3 grids (three
+// problems per warp) win for d = 5 (2.17 vs 3.0 ms) and tie for d = 3, but lose for d = 9 (9.5 vs
+// 9.2 ms: LC = 3 row loads conflict and 5 lanes idle) and d = 1; 4 x 4 (two per warp) elsewhere
+// up to d = 12; d >= 13 uses one warp per problem as 4 x 8 (all-16-lane layout: 352 ms per cfg1
+// batch vs 386 ms with 32 lanes everywhere).
+__host__ __device__ constexpr int tiny_lr(int d) { return d == 2 ? 2 : (d == 3 || d == 5 || d == 6) ? 3 : 4; }
 __host__ __device__ constexpr int tiny_lc(int d) { return d >= 13 ? 8 : tiny_lr(d); }
 __host__ __device__ constexpr int tiny_lanes(int d) { return tiny_lr(d) * tiny_lc(d); }
 constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
