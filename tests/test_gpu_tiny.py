@@ -175,3 +175,19 @@ def test_integration_md_ctypes_stub_runs(golden):
     gx, gy, p = ns["gradient"](g("psi0"), g("psif"), g("u")[0], g("u")[1], Duck(g("h0"), g("hx"), g("hy")), 0.1)
     assert abs(p - float(g("P"))) <= F_TOL
     assert rel(np.concatenate([gx, gy]), np.concatenate([g("gx"), g("gy")])) <= G_TOL
+
+
+def test_batched_device_lbfgs_improves_every_seed():
+    import torch
+
+    from paper_2309_05884_b200 import optim
+
+    s = systems.config(1, n_slices=100)
+    eng = GrapeEngine(s, max_batch=64)
+    u0 = torch.from_numpy(s.controls(1, batch=64)).cuda()
+    fun = optim.DeviceObjective(eng)
+    F0, _ = fun(u0)
+    res = optim.lbfgs_maximize(fun, u0, iterations=10)
+    assert bool(torch.all(res.F >= F0))
+    assert res.history[-1] > res.history[0] + 1e-3
+    assert all(b >= a - 1e-12 for a, b in zip(res.history, res.history[1:]))
