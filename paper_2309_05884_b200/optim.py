@@ -43,8 +43,12 @@ class DeviceObjective:
 
 
 def lbfgs_maximize(fun, u0: torch.Tensor, iterations: int = 50, history: int = 10, c1: float = 1e-4,
-                   shrink: float = 0.5, max_backtracks: int = 20) -> BatchedResult:
-    """Maximise fun(u) -> (F (B,), grad (B, ...)) independently for every batch row."""
+                   shrink: float = 0.5, max_backtracks: int = 12, indexed: bool = False) -> BatchedResult:
+    """Maximise fun(u) -> (F (B,), grad (B, ...)) independently for every batch row.
+
+    Line-search trials are evaluated on compacted sub-batches; when the objective differs per
+    row (``indexed=True``) it is called as fun(u_sub, rows) with the original row indices.
+    """
     B = u0.shape[0]
     shape = u0.shape
     u = u0.clone().reshape(B, -1)
@@ -88,21 +92,26 @@ def lbfgs_maximize(fun, u0: torch.Tensor, iterations: int = 50, history: int = 1
             step = 1.0 / g.norm(dim=1).clamp_min(1e-300)
         else:
             step = torch.ones(B, dtype=dt, device=dev)
-        # batched Armijo backtracking: every seed keeps shrinking until it is accepted
+        # batched Armijo backtracking: trial points are evaluated only for the seeds that have
+        # not accepted yet (compacted sub-batch), so a few stubborn seeds cost little
         accepted = torch.zeros(B, dtype=torch.bool, device=dev)
         u_new, f_new, g_new = u.clone(), fval.clone(), g.clone()
         for _ in range(max_backtracks):
-            trial = u + step[:, None] * d
-            ft, gt = f(trial)
-            evals += 1
-            ok = (~accepted) & (ft <= fval + c1 * step * slope)
-            u_new = torch.where(ok[:, None], trial, u_new)
-            f_new = torch.where(ok, ft, f_new)
-            g_new = torch.where(ok[:, None], gt, g_new)
-            accepted |= ok
-            if bool(accepted.all()):
+            idx = torch.nonzero(~accepted).squeeze(1)
+            if idx.numel() == 0:
                 break
-            step = torch.where(accepted, step, step * shrink)
+            trial = u[idx] + step[idx, None] * d[idx]
+            sub = trial.reshape((idx.numel(),) + tuple(shape[1:]))
+            Ft, Gt = fun(sub, idx) if indexed else fun(sub)
+            ft, gt = -Ft, -Gt.reshape(idx.numel(), -1)
+            evals += 1
+            ok = ft <= fval[idx] + c1 * step[idx] * slope[idx]
+            acc_idx = idx[ok]
+            u_new[acc_idx] = trial[ok]
+            f_new[acc_idx] = ft[ok]
+            g_new[acc_idx] = gt[ok]
+            accepted[acc_idx] = True
+            step[idx[~ok]] *= shrink
         s = u_new - u
         y = g_new - g
         sy = (s * y).sum(1)

@@ -84,3 +84,17 @@ def test_cfg4_full_size_matrix_free_equals_dense_state_vector():
     F2, g2 = eng.objective(u)
     assert abs(F1 - F2) <= 1e-10
     assert np.abs(g1 - g2).max() <= 1e-8 * np.abs(g2).max()
+
+
+def test_cfg4_symmetric_equals_conventional_at_full_size():
+    """The paper's central claim at the BASELINE size: n=12, N=200 state transfer in the full
+    4096-dim space (matrix-free schedule) equals the same evaluation in the 224-dim A1 block."""
+    full = systems.config(4)
+    blk = systems.config(4, full=False)
+    u = full.controls(2)
+    ef = GrapeEngine(full, max_batch=1)
+    ef.set_schedule("matrix-free")
+    Ff, gf = ef.objective(u)
+    Fb, gb = GrapeEngine(blk, max_batch=1).objective(u)
+    assert abs(Ff - Fb) <= 1e-10
+    assert np.abs(gf - gb).max() <= 1e-8 * np.abs(gb).max()

@@ -14,11 +14,12 @@ def test_batched_lbfgs_solves_independent_quadratics():
     A = A @ A.transpose(1, 2) + n * torch.eye(n, dtype=torch.float64)
     c = torch.randn(B, n, dtype=torch.float64)
 
-    def fun(u):  # maximise F = -(1/2 u^T A u - c^T u)
-        Au = torch.einsum("bij,bj->bi", A, u)
-        return -(0.5 * (u * Au).sum(1) - (c * u).sum(1)), -(Au - c)
+    def fun(u, rows=None):  # maximise F = -(1/2 u^T A u - c^T u), a different quadratic per row
+        rows = torch.arange(u.shape[0]) if rows is None else rows
+        Au = torch.einsum("bij,bj->bi", A[rows], u)
+        return -(0.5 * (u * Au).sum(1) - (c[rows] * u).sum(1)), -(Au - c[rows])
 
-    res = optim.lbfgs_maximize(fun, torch.zeros(B, n, dtype=torch.float64), iterations=60)
+    res = optim.lbfgs_maximize(fun, torch.zeros(B, n, dtype=torch.float64), iterations=60, indexed=True)
     ustar = torch.linalg.solve(A, c)
     assert torch.allclose(res.u, ustar, atol=1e-6)
     assert all(b >= a - 1e-12 for a, b in zip(res.history, res.history[1:]))
