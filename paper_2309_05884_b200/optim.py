@@ -94,7 +94,8 @@ def lbfgs_maximize(fun, u0: torch.Tensor, iterations: int = 50, history: int = 1
             step = torch.ones(B, dtype=dt, device=dev)
         # batched Armijo backtracking: trial points are evaluated only for the seeds that have
         # not accepted yet (compacted sub-batch), so a few stubborn seeds cost little
-        accepted = torch.zeros(B, dtype=torch.bool, device=dev)
+        # seeds whose predicted decrease is below rounding are converged: they stay put
+        accepted = slope.abs() <= 1e-13 * fval.abs().clamp_min(1.0)
         u_new, f_new, g_new = u.clone(), fval.clone(), g.clone()
         for _ in range(max_backtracks):
             idx = torch.nonzero(~accepted).squeeze(1)
