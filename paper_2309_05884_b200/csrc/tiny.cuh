@@ -38,8 +38,8 @@ constexpr int kMaxControls = 4;
 // 9.2 ms: LC = 3 row loads conflict and 5 lanes idle) and d = 1; 4 x 4 (two per warp) elsewhere
 // up to d = 12; d >= 13 uses one warp per problem as 4 x 8 (all-16-lane layout: 352 ms per cfg1
 // batch vs 386 ms with 32 lanes everywhere).
-__host__ __device__ constexpr int tiny_lr(int d) { return d == 2 ? 2 : (d == 3 || d == 5 || d == 6) ? 3 : 4; }
-__host__ __device__ constexpr int tiny_lc(int d) { return d >= 13 ? 8 : tiny_lr(d); }
+__host__ __device__ constexpr int tiny_lr(int d) { return d >= 13 ? 8 : d == 2 ? 2 : (d == 3 || d == 5 || d == 6) ? 3 : 4; }
+__host__ __device__ constexpr int tiny_lc(int d) { return d >= 13 ? 4 : tiny_lr(d); }
 __host__ __device__ constexpr int tiny_lanes(int d) { return tiny_lr(d) * tiny_lc(d); }
 constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
@@ -230,6 +230,147 @@ struct Tile {
   }
 };
 
+__device__ __forceinline__ void tdmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// FP64 tensor-core tile for 13 <= D <= 16: one warp computes the full (padded 16 x 16) product
+// with mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) in the 3M (Gauss) form -- three real DMMAs per
+// complex k-step instead of 4 x 4 DFMA lanes.  Lane l owns the DMMA C fragments: rows
+// l/4 + 8i (i < 2), cols 2(l%4) + v + 8t (v, t < 2) -- a 2 x 4 register tile, 4 lanes per row.
+// Operand fragments are loaded from the exact D x D shared-memory matrices with zero padding
+// (no 16 x 16 storage), so the resident-problem count per SM is unchanged.
+template <int D>
+struct MmaTile {
+  static constexpr int TSR = 2, TSC = 4;
+  int tr, tc;  // lane / 4, lane % 4
+  __device__ __forceinline__ int rrow(int i) const { return tr + 8 * i; }
+  __device__ __forceinline__ int rcol(int j) const { return 2 * tc + (j & 1) + 8 * (j >> 1); }
+  __device__ __forceinline__ int row(int i) const { return min(rrow(i), D - 1); }
+  __device__ __forceinline__ int col(int j) const { return min(rcol(j), D - 1); }
+  __device__ __forceinline__ bool ok(int i, int j) const { return rrow(i) < D && rcol(j) < D; }
+  __device__ __forceinline__ bool row_ok(int i) const { return rrow(i) < D; }
+
+  __device__ __forceinline__ void zero(double2 (&t)[TSR][TSC]) const {
+#pragma unroll
+    for (int i = 0; i < TSR; ++i)
+#pragma unroll
+      for (int j = 0; j < TSC; ++j) t[i][j] = czero();
+  }
+  __device__ __forceinline__ void store(double2* M, const double2 (&t)[TSR][TSC], bool wr) const {
+    if (!wr) return;
+#pragma unroll
+    for (int i = 0; i < TSR; ++i)
+#pragma unroll
+      for (int j = 0; j < TSC; ++j)
+        if (ok(i, j)) M[rrow(i) * D + rcol(j)] = t[i][j];
+  }
+  // A fragment (m = mt*8 + tr, k = k0 + tc) of op(L) (L or L^dag), zero outside D
+  __device__ __forceinline__ double2 frag_a(const double2* L, int mt, int k0, bool adj) const {
+    const int m = mt * 8 + tr, k = k0 + tc;
+    if (m >= D || k >= D) return czero();
+    return adj ? cconj(L[k * D + m]) : L[m * D + k];
+  }
+  // B fragment (k = k0 + tc, n = nt*8 + tr) of M, zero outside D
+  __device__ __forceinline__ double2 frag_b(const double2* M, int nt, int k0) const {
+    const int k = k0 + tc, n = nt * 8 + tr;
+    if (k >= D || n >= D) return czero();
+    return M[k * D + n];
+  }
+  // acc[mt][nt][T1, T2, T3][c0, c1] += 3M product of one k-step
+  __device__ __forceinline__ static void acc3(double (&acc)[2][2][3][2], const double2 (&a)[2],
+                                              const double2 (&b)[2]) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        tdmma(acc[mt][nt][0][0], acc[mt][nt][0][1], a[mt].x, b[nt].x);
+        tdmma(acc[mt][nt][1][0], acc[mt][nt][1][1], a[mt].y, b[nt].y);
+        tdmma(acc[mt][nt][2][0], acc[mt][nt][2][1], a[mt].x + a[mt].y, b[nt].x + b[nt].y);
+      }
+  }
+  __device__ __forceinline__ static void clear(double (&acc)[2][2][3][2]) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) acc[mt][nt][q][0] = acc[mt][nt][q][1] = 0.0;
+  }
+  __device__ __forceinline__ static void finish(double2 (&t)[TSR][TSC], const double (&acc)[2][2][3][2]) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const double t1 = acc[mt][nt][0][v], t2 = acc[mt][nt][1][v], t3 = acc[mt][nt][2][v];
+          t[mt][nt * 2 + v] = make_double2(t1 - t2, t3 - t1 - t2);
+        }
+  }
+  __device__ __forceinline__ void mul_op(double2 (&t)[TSR][TSC], const double2* L, const double2* M, bool adj) const {
+    double acc[2][2][3][2];
+    clear(acc);
+#pragma unroll 1
+    for (int k0 = 0; k0 < D; k0 += 4) {
+      double2 a[2], b[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) a[mt] = frag_a(L, mt, k0, adj);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) b[nt] = frag_b(M, nt, k0);
+      acc3(acc, a, b);
+    }
+    finish(t, acc);
+  }
+  __device__ __forceinline__ void mul(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
+    mul_op(t, L, M, false);
+  }
+  __device__ __forceinline__ void mul_adj(double2 (&t)[TSR][TSC], const double2* U, const double2* M) const {
+    mul_op(t, U, M, true);
+  }
+  // (t, dt) = (L M, L dM + dL M)
+  __device__ __forceinline__ void pair(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const double2* L,
+                                       const double2* dL, const double2* M, const double2* dM) const {
+    double acc[2][2][3][2], dacc[2][2][3][2];
+    clear(acc);
+    clear(dacc);
+#pragma unroll 1
+    for (int k0 = 0; k0 < D; k0 += 4) {
+      double2 a[2], da[2], b[2], db[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        a[mt] = frag_a(L, mt, k0, false);
+        da[mt] = frag_a(dL, mt, k0, false);
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        b[nt] = frag_b(M, nt, k0);
+        db[nt] = frag_b(dM, nt, k0);
+      }
+      acc3(acc, a, b);
+      acc3(dacc, a, db);
+      acc3(dacc, da, b);
+    }
+    finish(t, acc);
+    finish(dt, dacc);
+  }
+};
+
+template <int D, int TSR, int TSC, int LR, int LC>
+struct TileSel {
+  using type = Tile<D, TSR, TSC, LR, LC>;
+};
+template <int TSR, int TSC, int LR, int LC>
+struct TileSel<13, TSR, TSC, LR, LC> { using type = MmaTile<13>; };
+template <int TSR, int TSC, int LR, int LC>
+struct TileSel<14, TSR, TSC, LR, LC> { using type = MmaTile<14>; };
+template <int TSR, int TSC, int LR, int LC>
+struct TileSel<15, TSR, TSC, LR, LC> { using type = MmaTile<15>; };
+template <int TSR, int TSC, int LR, int LC>
+struct TileSel<16, TSR, TSC, LR, LC> { using type = MmaTile<16>; };
+
 // Per-warp problem context: tile geometry, shared-memory buffers and the per-slice
 // building blocks shared by the fused kernel and the slice-parallel kernels.
 template <int D, bool GATE>
@@ -244,7 +385,8 @@ struct TinyCtx {
   static constexpr int DD = D * D;
   using T2 = double2[TSR][TSC];
 
-  Tile<D, TSR, TSC, LR, LC> tl;
+  using TileT = typename TileSel<D, TSR, TSC, LR, LC>::type;
+  TileT tl;
   int K, N, q, sub;
   bool act;  // lane belongs to a problem group (lanes past PPW * LP idle and never store)
   const double2* gen;  // (K+1) DD in smem
@@ -257,7 +399,7 @@ struct TinyCtx {
     act = lane < PPW * LP;
     sub = act ? lane / LP : 0;
     q = act ? lane % LP : 0;
-    tl = Tile<D, TSR, TSC, LR, LC>{q / LC, q % LC};
+    tl = TileT{q / LC, q % LC};
     gen = gen_smem;
     K = K_;
     N = N_;
