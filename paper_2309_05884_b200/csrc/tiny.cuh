@@ -279,6 +279,12 @@ struct MmaTile {
     if (k >= D || n >= D) return czero();
     return M[k * D + n];
   }
+  // B fragment of M^dag: (k, n) -> conj(M[n][k])
+  __device__ __forceinline__ double2 frag_b_adj(const double2* M, int nt, int k0) const {
+    const int k = k0 + tc, n = nt * 8 + tr;
+    if (k >= D || n >= D) return czero();
+    return cconj(M[n * D + k]);
+  }
   // acc[mt][nt][T1, T2, T3][c0, c1] += 3M product of one k-step
   __device__ __forceinline__ static void acc3(double (&acc)[2][2][3][2], const double2 (&a)[2],
                                               const double2 (&b)[2]) {
@@ -326,6 +332,21 @@ struct MmaTile {
   }
   __device__ __forceinline__ void mul(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
     mul_op(t, L, M, false);
+  }
+  // t = L M^dag
+  __device__ __forceinline__ void mul_bt(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
+    double acc[2][2][3][2];
+    clear(acc);
+#pragma unroll 1
+    for (int k0 = 0; k0 < D; k0 += 4) {
+      double2 a[2], b[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) a[mt] = frag_a(L, mt, k0, false);
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) b[nt] = frag_b_adj(M, nt, k0);
+      acc3(acc, a, b);
+    }
+    finish(t, acc);
   }
   __device__ __forceinline__ void mul_adj(double2 (&t)[TSR][TSC], const double2* U, const double2* M) const {
     mul_op(t, U, M, true);
@@ -532,18 +553,22 @@ struct TinyCtx {
   // Adot (B3) = 2^-s X Lam^dag with X in B0, Lam in B1 (D x R each)
   __device__ __forceinline__ void seed_c(int s) const {
     T2 t;
-    tl.zero(t);
+    if constexpr (GATE && D >= 13) {
+      tl.mul_bt(t, B0, B1);
+    } else {
+      tl.zero(t);
 #pragma unroll 1
-    for (int k = 0; k < R; ++k) {
-      double2 l[TSR], m[TSC];
+      for (int k = 0; k < R; ++k) {
+        double2 l[TSR], m[TSC];
 #pragma unroll
-      for (int i = 0; i < TSR; ++i) l[i] = B0[tl.row(i) * R + k];
+        for (int i = 0; i < TSR; ++i) l[i] = B0[tl.row(i) * R + k];
 #pragma unroll
-      for (int jj = 0; jj < TSC; ++jj) m[jj] = cconj(B1[tl.col(jj) * R + k]);
+        for (int jj = 0; jj < TSC; ++jj) m[jj] = cconj(B1[tl.col(jj) * R + k]);
 #pragma unroll
-      for (int i = 0; i < TSR; ++i)
+        for (int i = 0; i < TSR; ++i)
 #pragma unroll
-        for (int jj = 0; jj < TSC; ++jj) cfma(t[i][jj], l[i], m[jj]);
+          for (int jj = 0; jj < TSC; ++jj) cfma(t[i][jj], l[i], m[jj]);
+      }
     }
     scale(t, ldexp(1.0, -s));
     tl.store(B3, t, act);
