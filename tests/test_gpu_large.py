@@ -214,3 +214,26 @@ def test_gradient_finite_difference_100_probes_mixed_blocks():
             worst = max(worst, abs(fd - g[k, j]) / max(abs(fd), abs(g[k, j]), rms))
             probes += 1
     assert probes >= 100 and worst <= 1e-6, worst
+
+
+@pytest.mark.parametrize("K", [1, 3])
+def test_other_control_counts(K):
+    """K = 1 and K = 3 controls (H_3 = sum Z_i as an extra control) through tiny and DMMA paths."""
+    from paper_2309_05884_b200 import pauli, symmetry
+
+    n = 8
+    bases = symmetry.dn_full_basis(n)
+    h0 = pauli.realize(systems.ring_heisenberg(n))
+    hx, hy = [pauli.realize(h) for h in systems.global_controls(n)]
+    hz = pauli.realize(pauli.PauliTermSum(n, [pauli.single_site(n, i, "Z") for i in range(1, n + 1)]))
+    ctrl = [hx, hy, hz][:K] if K == 3 else [hx]
+    blocks = [systems.Block(b.label, systems.hermitian_part(b.compress(h0)),
+                            [systems.hermitian_part(b.compress(h)) for h in ctrl], b) for b in bases]
+    rng = np.random.default_rng(3)
+    targets = [systems.haar_unitary(rng, b.dim) for b in blocks]
+    s = systems.GrapeSystem("k-test", n, blocks, "gate", 10.0 * 20 / 500, 20, targets)
+    u = np.random.default_rng(4).uniform(-1, 1, (K, 20))
+    F, g = GrapeEngine(s, max_batch=1).objective(u)
+    Fo, go, _ = O.objective(s, u)
+    assert abs(F - Fo) <= F_TOL
+    assert rel(g, go) <= G_TOL
