@@ -38,8 +38,9 @@ constexpr int kMaxControls = 4;
 // 9.2 ms: LC = 3 row loads conflict and 5 lanes idle) and d = 1; 4 x 4 (two per warp) elsewhere
 // up to d = 12; d >= 13 uses one warp per problem as 4 x 8 (all-16-lane layout: 352 ms per cfg1
 // batch vs 386 ms with 32 lanes everywhere).
-__host__ __device__ constexpr int tiny_lr(int d) { return d >= 13 ? 8 : d == 2 ? 2 : (d == 3 || d == 5 || d == 6) ? 3 : 4; }
-__host__ __device__ constexpr int tiny_lc(int d) { return d >= 13 ? 4 : tiny_lr(d); }
+__host__ __device__ constexpr int tiny_lr(int d) { return (d >= 13 || d == 7 || d == 8) ? 8 : d == 2 ? 2 : (d == 3 || d == 5 || d == 6) ? 3 : 4; }
+__host__ __device__ constexpr bool tiny_mma(int d) { return d >= 13 || d == 7 || d == 8; }
+__host__ __device__ constexpr int tiny_lc(int d) { return tiny_mma(d) ? 4 : tiny_lr(d); }
 __host__ __device__ constexpr int tiny_lanes(int d) { return tiny_lr(d) * tiny_lc(d); }
 constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
@@ -242,9 +243,9 @@ __device__ __forceinline__ void tdmma(double& c0, double& c1, double a, double b
 // l/4 + 8i (i < 2), cols 2(l%4) + v + 8t (v, t < 2) -- a 2 x 4 register tile, 4 lanes per row.
 // Operand fragments are loaded from the exact D x D shared-memory matrices with zero padding
 // (no 16 x 16 storage), so the resident-problem count per SM is unchanged.
-template <int D>
+template <int D, int MT = (D + 7) / 8>
 struct MmaTile {
-  static constexpr int TSR = 2, TSC = 4;
+  static constexpr int TSR = MT, TSC = 2 * MT;  // MT = number of 8-row DMMA tiles (1 or 2)
   int tr, tc;  // lane / 4, lane % 4
   __device__ __forceinline__ int rrow(int i) const { return tr + 8 * i; }
   __device__ __forceinline__ int rcol(int j) const { return 2 * tc + (j & 1) + 8 * (j >> 1); }
@@ -286,30 +287,30 @@ struct MmaTile {
     return cconj(M[n * D + k]);
   }
   // acc[mt][nt][T1, T2, T3][c0, c1] += 3M product of one k-step
-  __device__ __forceinline__ static void acc3(double (&acc)[2][2][3][2], const double2 (&a)[2],
-                                              const double2 (&b)[2]) {
+  __device__ __forceinline__ static void acc3(double (&acc)[MT][MT][3][2], const double2 (&a)[MT],
+                                              const double2 (&b)[MT]) {
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
+      for (int nt = 0; nt < MT; ++nt) {
         tdmma(acc[mt][nt][0][0], acc[mt][nt][0][1], a[mt].x, b[nt].x);
         tdmma(acc[mt][nt][1][0], acc[mt][nt][1][1], a[mt].y, b[nt].y);
         tdmma(acc[mt][nt][2][0], acc[mt][nt][2][1], a[mt].x + a[mt].y, b[nt].x + b[nt].y);
       }
   }
-  __device__ __forceinline__ static void clear(double (&acc)[2][2][3][2]) {
+  __device__ __forceinline__ static void clear(double (&acc)[MT][MT][3][2]) {
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < MT; ++nt)
 #pragma unroll
         for (int q = 0; q < 3; ++q) acc[mt][nt][q][0] = acc[mt][nt][q][1] = 0.0;
   }
-  __device__ __forceinline__ static void finish(double2 (&t)[TSR][TSC], const double (&acc)[2][2][3][2]) {
+  __device__ __forceinline__ static void finish(double2 (&t)[TSR][TSC], const double (&acc)[MT][MT][3][2]) {
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < MT; ++nt)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const double t1 = acc[mt][nt][0][v], t2 = acc[mt][nt][1][v], t3 = acc[mt][nt][2][v];
@@ -317,15 +318,15 @@ struct MmaTile {
         }
   }
   __device__ __forceinline__ void mul_op(double2 (&t)[TSR][TSC], const double2* L, const double2* M, bool adj) const {
-    double acc[2][2][3][2];
+    double acc[MT][MT][3][2];
     clear(acc);
 #pragma unroll 1
     for (int k0 = 0; k0 < D; k0 += 4) {
-      double2 a[2], b[2];
+      double2 a[MT], b[MT];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) a[mt] = frag_a(L, mt, k0, adj);
+      for (int mt = 0; mt < MT; ++mt) a[mt] = frag_a(L, mt, k0, adj);
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) b[nt] = frag_b(M, nt, k0);
+      for (int nt = 0; nt < MT; ++nt) b[nt] = frag_b(M, nt, k0);
       acc3(acc, a, b);
     }
     finish(t, acc);
@@ -335,15 +336,15 @@ struct MmaTile {
   }
   // t = L M^dag
   __device__ __forceinline__ void mul_bt(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
-    double acc[2][2][3][2];
+    double acc[MT][MT][3][2];
     clear(acc);
 #pragma unroll 1
     for (int k0 = 0; k0 < D; k0 += 4) {
-      double2 a[2], b[2];
+      double2 a[MT], b[MT];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) a[mt] = frag_a(L, mt, k0, false);
+      for (int mt = 0; mt < MT; ++mt) a[mt] = frag_a(L, mt, k0, false);
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) b[nt] = frag_b_adj(M, nt, k0);
+      for (int nt = 0; nt < MT; ++nt) b[nt] = frag_b_adj(M, nt, k0);
       acc3(acc, a, b);
     }
     finish(t, acc);
@@ -354,19 +355,19 @@ struct MmaTile {
   // (t, dt) = (L M, L dM + dL M)
   __device__ __forceinline__ void pair(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const double2* L,
                                        const double2* dL, const double2* M, const double2* dM) const {
-    double acc[2][2][3][2], dacc[2][2][3][2];
+    double acc[MT][MT][3][2], dacc[MT][MT][3][2];
     clear(acc);
     clear(dacc);
 #pragma unroll 1
     for (int k0 = 0; k0 < D; k0 += 4) {
-      double2 a[2], da[2], b[2], db[2];
+      double2 a[MT], da[MT], b[MT], db[MT];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
+      for (int mt = 0; mt < MT; ++mt) {
         a[mt] = frag_a(L, mt, k0, false);
         da[mt] = frag_a(dL, mt, k0, false);
       }
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
+      for (int nt = 0; nt < MT; ++nt) {
         b[nt] = frag_b(M, nt, k0);
         db[nt] = frag_b(dM, nt, k0);
       }
@@ -383,6 +384,10 @@ template <int D, int TSR, int TSC, int LR, int LC>
 struct TileSel {
   using type = Tile<D, TSR, TSC, LR, LC>;
 };
+template <int TSR, int TSC, int LR, int LC>
+struct TileSel<7, TSR, TSC, LR, LC> { using type = MmaTile<7>; };
+template <int TSR, int TSC, int LR, int LC>
+struct TileSel<8, TSR, TSC, LR, LC> { using type = MmaTile<8>; };
 template <int TSR, int TSC, int LR, int LC>
 struct TileSel<13, TSR, TSC, LR, LC> { using type = MmaTile<13>; };
 template <int TSR, int TSC, int LR, int LC>
@@ -553,7 +558,7 @@ struct TinyCtx {
   // Adot (B3) = 2^-s X Lam^dag with X in B0, Lam in B1 (D x R each)
   __device__ __forceinline__ void seed_c(int s) const {
     T2 t;
-    if constexpr (GATE && D >= 13) {
+    if constexpr (GATE && tiny_mma(D)) {
       tl.mul_bt(t, B0, B1);
     } else {
       tl.zero(t);
