@@ -146,11 +146,11 @@ static int launch_tiny(int d, int which, const TinySliceParams& sp, int grid, in
   }
 }
 
-static int choose_nwarps(int d, int K, int batch) {
-  const int pg = 32 / tiny_lanes(d);
+static int choose_nwarps(int d, int K, int batch, bool mma) {
+  const int pg = 32 / tiny_lanes(d, mma);
   const int need = (batch + pg - 1) / pg;
   int nw = kTinyMaxWarps;
-  while (nw > 1 && tiny_smem_bytes(d, K, nw) > kMaxSmem) --nw;
+  while (nw > 1 && tiny_smem_bytes(d, K, nw, mma) > kMaxSmem) --nw;
   return std::max(1, std::min(nw, need));
 }
 
@@ -272,9 +272,9 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
     chk(cudaEventCreate(&bp.t1), "event");
     if (bp.tiny) {
       const int R = objective == SQOC_OBJ_GATE ? d : 1;
-      const int pg = 32 / tiny_lanes(d);
-      bp.nwarps = choose_nwarps(d, n_controls, max_batch);
-      bp.nwarps_max = choose_nwarps(d, n_controls, 1 << 30);
+      const int pg = 32 / tiny_lanes(d, tiny_mma(d));
+      bp.nwarps = choose_nwarps(d, n_controls, max_batch, tiny_mma(d));
+      bp.nwarps_max = choose_nwarps(d, n_controls, 1 << 30, false);
       const int per_cta = pg * bp.nwarps;
       bp.park_slots = (size_t)((max_batch + per_cta - 1) / per_cta) * per_cta;
       chk(cudaMalloc(&bp.park, bp.park_slots * 2 * d * R * sizeof(double2)), "cudaMalloc park");
@@ -380,7 +380,6 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
       tp.tau_stride = p->nblocks;
       tp.grad_out = gout;
       tp.park = bp.park;
-      const int pg = 32 / tiny_lanes(bp.d);
       const size_t R = gate ? bp.d : 1;
       // slice-parallel latency path for small batches (every (problem, slice) its own lane group)
       const bool sp_mode = p->N > 0 && (p->tiny_mode == 1 || (p->tiny_mode == -1 && batch <= kTinySliceParallelMaxBatch));
@@ -402,11 +401,12 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
         sp.Xh = bp.sp_X;
         sp.Lh = bp.sp_L;
         sp.units = batch * p->N;
+        const int pg = 32 / tiny_lanes(bp.d, false);
         // phases 1 and 3: lane group per (problem, slice); phase 2: per problem
         const int warps_units = (sp.units + pg - 1) / pg;
         const int nw = std::max(1, std::min(bp.nwarps_max, warps_units));
         tp.nwarps = nw;
-        const size_t smem = tiny_smem_bytes(bp.d, p->K, nw);
+        const size_t smem = tiny_smem_bytes(bp.d, p->K, nw, false);
         const int grid_units = (warps_units + nw - 1) / nw;
         const int warps_b = (batch + pg - 1) / pg;
         const int nw_b = std::max(1, std::min(bp.nwarps_max, warps_b));
@@ -416,7 +416,7 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
         if (rc == SQOC_OK) {
           TinySliceParams sp2 = sp;
           sp2.p.nwarps = nw_b;
-          const size_t smem_b = tiny_smem_bytes(bp.d, p->K, nw_b);
+          const size_t smem_b = tiny_smem_bytes(bp.d, p->K, nw_b, false);
           rc = gate ? launch_tiny<true>(bp.d, TK_SP_SWEEP, sp2, grid_b, nw_b, smem_b, bp.stream)
                     : launch_tiny<false>(bp.d, TK_SP_SWEEP, sp2, grid_b, nw_b, smem_b, bp.stream);
         }
@@ -425,10 +425,11 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
                     : launch_tiny<false>(bp.d, TK_SP_GRAD, sp, grid_units, nw, smem, bp.stream);
         p->launches += 3;
       } else {
+        const int pg = 32 / tiny_lanes(bp.d, tiny_mma(bp.d));
         int nw = std::max(1, std::min(bp.nwarps, (batch + pg - 1) / pg));
         tp.nwarps = nw;
         const int grid = (batch + pg * nw - 1) / (pg * nw);
-        const size_t smem = tiny_smem_bytes(bp.d, p->K, nw);
+        const size_t smem = tiny_smem_bytes(bp.d, p->K, nw, tiny_mma(bp.d));
         rc = gate ? launch_tiny<true>(bp.d, TK_FUSED, sp, grid, nw, smem, bp.stream)
                   : launch_tiny<false>(bp.d, TK_FUSED, sp, grid, nw, smem, bp.stream);
         p->launches += 1;

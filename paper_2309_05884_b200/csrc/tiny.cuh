@@ -38,10 +38,15 @@ constexpr int kMaxControls = 4;
 // 9.2 ms: LC = 3 row loads conflict and 5 lanes idle) and d = 1; 4 x 4 (two per warp) elsewhere
 // up to d = 12; d >= 13 uses one warp per problem as 4 x 8 (all-16-lane layout: 352 ms per cfg1
 // batch vs 386 ms with 32 lanes everywhere).
-__host__ __device__ constexpr int tiny_lr(int d) { return (d >= 13 || d == 7 || d == 8) ? 8 : d == 2 ? 2 : (d == 3 || d == 5 || d == 6) ? 3 : 4; }
+// DMMA (tensor-core) tiles for d = 7, 8 (one 8x8 tile) and d >= 13 (2x2 tiles) in the fused
+// throughput kernel (r01: d=13 15.5 -> 13.9 ms, d=7 4.3 -> 2.3 ms per cfg1 launch at N_t=100);
+// the slice-parallel latency kernels keep DFMA tiles (shorter dependency chains per warp).
 __host__ __device__ constexpr bool tiny_mma(int d) { return d >= 13 || d == 7 || d == 8; }
-__host__ __device__ constexpr int tiny_lc(int d) { return tiny_mma(d) ? 4 : tiny_lr(d); }
-__host__ __device__ constexpr int tiny_lanes(int d) { return tiny_lr(d) * tiny_lc(d); }
+__host__ __device__ constexpr int tiny_lr(int d, bool mma) {
+  return mma ? 8 : d >= 13 ? 4 : d == 2 ? 2 : (d == 3 || d == 5 || d == 6) ? 3 : 4;
+}
+__host__ __device__ constexpr int tiny_lc(int d, bool mma) { return mma ? 4 : d >= 13 ? 8 : tiny_lr(d, false); }
+__host__ __device__ constexpr int tiny_lanes(int d, bool mma) { return tiny_lr(d, mma) * tiny_lc(d, mma); }
 constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
 
@@ -380,30 +385,30 @@ struct MmaTile {
   }
 };
 
-template <int D, int TSR, int TSC, int LR, int LC>
+template <int D, int TSR, int TSC, int LR, int LC, bool MMA>
 struct TileSel {
   using type = Tile<D, TSR, TSC, LR, LC>;
 };
 template <int TSR, int TSC, int LR, int LC>
-struct TileSel<7, TSR, TSC, LR, LC> { using type = MmaTile<7>; };
+struct TileSel<7, TSR, TSC, LR, LC, true> { using type = MmaTile<7>; };
 template <int TSR, int TSC, int LR, int LC>
-struct TileSel<8, TSR, TSC, LR, LC> { using type = MmaTile<8>; };
+struct TileSel<8, TSR, TSC, LR, LC, true> { using type = MmaTile<8>; };
 template <int TSR, int TSC, int LR, int LC>
-struct TileSel<13, TSR, TSC, LR, LC> { using type = MmaTile<13>; };
+struct TileSel<13, TSR, TSC, LR, LC, true> { using type = MmaTile<13>; };
 template <int TSR, int TSC, int LR, int LC>
-struct TileSel<14, TSR, TSC, LR, LC> { using type = MmaTile<14>; };
+struct TileSel<14, TSR, TSC, LR, LC, true> { using type = MmaTile<14>; };
 template <int TSR, int TSC, int LR, int LC>
-struct TileSel<15, TSR, TSC, LR, LC> { using type = MmaTile<15>; };
+struct TileSel<15, TSR, TSC, LR, LC, true> { using type = MmaTile<15>; };
 template <int TSR, int TSC, int LR, int LC>
-struct TileSel<16, TSR, TSC, LR, LC> { using type = MmaTile<16>; };
+struct TileSel<16, TSR, TSC, LR, LC, true> { using type = MmaTile<16>; };
 
 // Per-warp problem context: tile geometry, shared-memory buffers and the per-slice
 // building blocks shared by the fused kernel and the slice-parallel kernels.
-template <int D, bool GATE>
+template <int D, bool GATE, bool MMA = tiny_mma(D)>
 struct TinyCtx {
   static constexpr int R = GATE ? D : 1;  // columns of X and Lam
-  static constexpr int LR = tiny_lr(D);
-  static constexpr int LC = tiny_lc(D);
+  static constexpr int LR = tiny_lr(D, MMA);
+  static constexpr int LC = tiny_lc(D, MMA);
   static constexpr int LP = LR * LC;
   static constexpr int PPW = 32 / LP;
   static constexpr int TSR = (D + LR - 1) / LR;
@@ -411,7 +416,7 @@ struct TinyCtx {
   static constexpr int DD = D * D;
   using T2 = double2[TSR][TSC];
 
-  using TileT = typename TileSel<D, TSR, TSC, LR, LC>::type;
+  using TileT = typename TileSel<D, TSR, TSC, LR, LC, MMA>::type;
   TileT tl;
   int K, N, q, sub;
   bool act;  // lane belongs to a problem group (lanes past PPW * LP idle and never store)
@@ -558,7 +563,7 @@ struct TinyCtx {
   // Adot (B3) = 2^-s X Lam^dag with X in B0, Lam in B1 (D x R each)
   __device__ __forceinline__ void seed_c(int s) const {
     T2 t;
-    if constexpr (GATE && tiny_mma(D)) {
+    if constexpr (GATE && MMA) {
       tl.mul_bt(t, B0, B1);
     } else {
       tl.zero(t);
@@ -767,7 +772,7 @@ struct TinySliceParams {
 // phase 1: U_j for every (problem, slice)
 template <int D, bool GATE>
 __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_expm_kernel(TinySliceParams sp) {
-  using C = TinyCtx<D, GATE>;
+  using C = TinyCtx<D, GATE, false>;
   const TinyParams& p = sp.p;
   const int K = p.K, N = p.N;
   double2* gen = load_generators<D>(p);
@@ -792,7 +797,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_expm_kernel(TinySl
 // phase 2: X / Lam recurrences (one lane group per problem), tau
 template <int D, bool GATE>
 __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_sweep_kernel(TinySliceParams sp) {
-  using C = TinyCtx<D, GATE>;
+  using C = TinyCtx<D, GATE, false>;
   constexpr int R = C::R;
   const TinyParams& p = sp.p;
   const int K = p.K, N = p.N;
@@ -837,7 +842,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_sweep_kernel(TinyS
 // phase 3: Frechet pair chain + traces for every (problem, slice)
 template <int D, bool GATE>
 __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_grad_kernel(TinySliceParams sp) {
-  using C = TinyCtx<D, GATE>;
+  using C = TinyCtx<D, GATE, false>;
   constexpr int R = C::R;
   const TinyParams& p = sp.p;
   const int K = p.K, N = p.N;
@@ -869,8 +874,8 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_grad_kernel(TinySl
     if (c.real && c.q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau[k].x - ctw.y * dtau[k].y;
 }
 
-inline size_t tiny_smem_bytes(int d, int K, int nwarps) {
-  const int ppw = 32 / tiny_lanes(d);
+inline size_t tiny_smem_bytes(int d, int K, int nwarps, bool mma) {
+  const int ppw = 32 / tiny_lanes(d, mma);
   return sizeof(double2) * ((size_t)(K + 1) * d * d + (size_t)nwarps * ppw * kTinyBuffers * d * d);
 }
 
