@@ -42,4 +42,6 @@ def test_random_dense_block(d, objective):
         for b in range(3):
             Fo, go, _ = O.objective(s, u[b])
             assert abs(F[b] - Fo) <= 1e-10, (d, objective, sched)
-            assert np.abs(g[b] - go).max() <= 1e-8 * max(np.abs(go).max(), 1e-12), (d, objective, sched)
+            # d = 1 has F = 1 and an exactly-zero gradient: rounding noise ~1e-18 is judged
+            # against an absolute floor of 1e-14 (1e-8 of a unit-scale gradient entry 1e-6)
+            assert np.abs(g[b] - go).max() <= 1e-8 * max(np.abs(go).max(), 1e-6), (d, objective, sched)
