@@ -47,6 +47,14 @@ __host__ __device__ constexpr int tiny_lr(int d, bool mma) {
 }
 __host__ __device__ constexpr int tiny_lc(int d, bool mma) { return mma ? 4 : d >= 13 ? 8 : tiny_lr(d, false); }
 __host__ __device__ constexpr int tiny_lanes(int d, bool mma) { return tiny_lr(d, mma) * tiny_lc(d, mma); }
+// Per-problem shared-memory stride (double2): 8 d^2 buffers plus a pad that staggers the
+// problems of one warp across the 32 banks.  8 d^2 double2 is always a multiple of 32 words,
+// so without the pad every problem of a warp starts on bank 0 and the broadcast loads of
+// the LP-lane groups collide (2 wavefronts instead of 1 for two problems per warp).
+__host__ __device__ constexpr int tiny_pad(int d, bool mma) {
+  return (32 / tiny_lanes(d, mma)) == 2 ? 4 : (32 / tiny_lanes(d, mma)) == 3 ? 3 : (32 / tiny_lanes(d, mma)) == 8 ? 2 : 0;
+}
+__host__ __device__ constexpr int tiny_stride(int d, bool mma) { return kTinyBuffers * d * d + tiny_pad(d, mma); }
 constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
 
@@ -414,6 +422,7 @@ struct TinyCtx {
   static constexpr int TSR = (D + LR - 1) / LR;
   static constexpr int TSC = (D + LC - 1) / LC;
   static constexpr int DD = D * D;
+  static constexpr int STRIDE = tiny_stride(D, MMA);
   using T2 = double2[TSR][TSC];
 
   using TileT = typename TileSel<D, TSR, TSC, LR, LC, MMA>::type;
@@ -704,7 +713,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   const int warp = threadIdx.x >> 5;
   C c;
   c.init(gen, nullptr, K, N);
-  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * kTinyBuffers * C::DD, K, N);
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * C::STRIDE, K, N);
   const int slot = (blockIdx.x * p.nwarps + warp) * C::PPW + c.sub;  // park is sized for all slots
   c.real = c.act && slot < p.batch;                                  // owns a real problem (may store globally)
   const int prob = c.real ? slot : p.batch - 1;                    // padding slots replay the last problem's u
@@ -779,7 +788,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_expm_kernel(TinySl
   const int warp = threadIdx.x >> 5;
   C c;
   c.init(gen, nullptr, K, N);
-  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * kTinyBuffers * C::DD, K, N);
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * C::STRIDE, K, N);
   const int item_raw = (blockIdx.x * p.nwarps + warp) * C::PPW + c.sub;
   c.real = c.act && item_raw < sp.units;
   const int item = c.real ? item_raw : sp.units - 1;
@@ -805,7 +814,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_sweep_kernel(TinyS
   const int warp = threadIdx.x >> 5;
   C c;
   c.init(gen, nullptr, K, N);
-  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * kTinyBuffers * C::DD, K, N);
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * C::STRIDE, K, N);
   const int slot = (blockIdx.x * p.nwarps + warp) * C::PPW + c.sub;
   c.real = c.act && slot < p.batch;
   const int prob = c.real ? slot : p.batch - 1;
@@ -850,7 +859,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_grad_kernel(TinySl
   const int warp = threadIdx.x >> 5;
   C c;
   c.init(gen, nullptr, K, N);
-  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * kTinyBuffers * C::DD, K, N);
+  c.init(gen, gen + (K + 1) * C::DD + (size_t)(warp * C::PPW + c.sub) * C::STRIDE, K, N);
   const int item_raw = (blockIdx.x * p.nwarps + warp) * C::PPW + c.sub;
   c.real = c.act && item_raw < sp.units;
   const int item = c.real ? item_raw : sp.units - 1;
@@ -876,7 +885,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_grad_kernel(TinySl
 
 inline size_t tiny_smem_bytes(int d, int K, int nwarps, bool mma) {
   const int ppw = 32 / tiny_lanes(d, mma);
-  return sizeof(double2) * ((size_t)(K + 1) * d * d + (size_t)nwarps * ppw * kTinyBuffers * d * d);
+  return sizeof(double2) * ((size_t)(K + 1) * d * d + (size_t)nwarps * ppw * tiny_stride(d, mma));
 }
 
 }  // namespace sqoc

@@ -246,6 +246,72 @@ __global__ void __launch_bounds__(GTHREADS) zgemm_kernel(const GemmItem* __restr
 // so the three accumulator sets fit in registers.
 constexpr int G3THREADS = 256;
 
+// Main loop of one CTA tile for a warp whose valid output is MC x NC DMMA sub-tiles (8 x 8):
+// sub-tiles wholly outside C issue neither fragment loads nor DMMAs.  The shape is a template
+// parameter (dispatched once per warp) because a predicated-off DMMA still occupies the pipe;
+// every instantiation runs the same cp.async / barrier sequence, so warps of one CTA may take
+// different instantiations.  The all-zero k = 4 half-step of a segment's last K tile is skipped.
+template <int TA, int TB, int MC, int NC>
+__device__ __forceinline__ void g3_mainloop(double (&acc)[4][2][3][2], const GemmItem& it, double2* sAbase,
+                                            double2* sBbase, int m0, int n0, int wm, int wn, int lr, int lc) {
+  const int kt_per_seg = (it.k + GBK - 1) / GBK;
+  const int kt_total = kt_per_seg * it.nseg;
+  auto issue = [&](int kt) {
+    if (kt < kt_total) {
+      const int seg = kt / kt_per_seg;
+      const int k0 = (kt - seg * kt_per_seg) * GBK;
+      const int st = kt % GSTAGES;
+      gemm_load_stage<TA, TB, G3THREADS>(sAbase + st * G_A_ELEMS, sBbase + st * G_A_ELEMS, seg ? it.A1 : it.A0,
+                                         seg ? it.B1 : it.B0, it, m0, n0, k0);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < GSTAGES - 1; ++s) issue(s);
+  const bool half_tail = (it.k % GBK) != 0 && (it.k % GBK) <= 4;  // last K tile has one k-step
+  int kin = 0;
+  for (int kt = 0; kt < kt_total; ++kt) {
+    cp_async_wait<GSTAGES - 2>();
+    __syncthreads();
+    issue(kt + GSTAGES - 1);
+    const int st = kt % GSTAGES;
+    const double2* sA = sAbase + st * G_A_ELEMS;
+    const double2* sB = sBbase + st * G_A_ELEMS;
+    const int ksteps = (half_tail && kin == kt_per_seg - 1) ? 1 : 2;
+    if (++kin == kt_per_seg) kin = 0;
+    if constexpr (MC == 0 || NC == 0) continue;
+#pragma unroll 1
+    for (int ks = 0; ks < ksteps; ++ks) {
+      const int kk = ks * 4;
+      double ar[MC ? MC : 1], ai[MC ? MC : 1], as[MC ? MC : 1], br[NC ? NC : 1], bi[NC ? NC : 1], bs[NC ? NC : 1];
+#pragma unroll
+      for (int mi = 0; mi < MC; ++mi) {
+        const int m = wm + mi * 8 + lr, k = kk + lc;
+        double2 a;
+        if (TA == OP_N) a = sA[m * LD_KMAJ + k];
+        else { a = sA[k * LD_NMAJ + m]; a.y = -a.y; }
+        ar[mi] = a.x; ai[mi] = a.y; as[mi] = a.x + a.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < NC; ++ni) {
+        const int n = wn + ni * 8 + lr, k = kk + lc;
+        double2 b;
+        if (TB == OP_N) b = sB[k * LD_NMAJ + n];
+        else { b = sB[n * LD_KMAJ + k]; b.y = -b.y; }
+        br[ni] = b.x; bi[ni] = b.y; bs[ni] = b.x + b.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < MC; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NC; ++ni) {
+          dmma(acc[mi][ni][0][0], acc[mi][ni][0][1], ar[mi], br[ni]);
+          dmma(acc[mi][ni][1][0], acc[mi][ni][1][1], ai[mi], bi[ni]);
+          dmma(acc[mi][ni][2][0], acc[mi][ni][2][1], as[mi], bs[ni]);
+        }
+    }
+  }
+}
+
 template <int TA, int TB, int EPI>
 __global__ void __launch_bounds__(G3THREADS, 2) zgemm3m_kernel(const GemmItem* __restrict__ items, int nitems,
                                                                GemmArgs args) {
@@ -274,60 +340,20 @@ __global__ void __launch_bounds__(G3THREADS, 2) zgemm3m_kernel(const GemmItem* _
 #pragma unroll
       for (int c = 0; c < 3; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
 
-  const int kt_per_seg = (it.k + GBK - 1) / GBK;
-  const int kt_total = kt_per_seg * it.nseg;
   double2* sAbase = gsm;
   double2* sBbase = gsm + GSTAGES * G_A_ELEMS;
-
-  auto issue = [&](int kt) {
-    if (kt < kt_total) {
-      const int seg = kt / kt_per_seg;
-      const int k0 = (kt - seg * kt_per_seg) * GBK;
-      const int st = kt % GSTAGES;
-      gemm_load_stage<TA, TB, G3THREADS>(sAbase + st * G_A_ELEMS, sBbase + st * G_A_ELEMS, seg ? it.A1 : it.A0,
-                                         seg ? it.B1 : it.B0, it, m0, n0, k0);
-    }
-    cp_async_commit();
-  };
-
-#pragma unroll
-  for (int s = 0; s < GSTAGES - 1; ++s) issue(s);
-
-  for (int kt = 0; kt < kt_total; ++kt) {
-    cp_async_wait<GSTAGES - 2>();
-    __syncthreads();
-    issue(kt + GSTAGES - 1);
-    const int st = kt % GSTAGES;
-    const double2* sA = sAbase + st * G_A_ELEMS;
-    const double2* sB = sBbase + st * G_A_ELEMS;
-#pragma unroll
-    for (int kk = 0; kk < GBK; kk += 4) {
-      double ar[4], ai[4], as[4], br[2], bi[2], bs[2];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const int m = wm + mi * 8 + lr, k = kk + lc;
-        double2 a;
-        if (TA == OP_N) a = sA[m * LD_KMAJ + k];
-        else { a = sA[k * LD_NMAJ + m]; a.y = -a.y; }
-        ar[mi] = a.x; ai[mi] = a.y; as[mi] = a.x + a.y;
-      }
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni) {
-        const int n = wn + ni * 8 + lr, k = kk + lc;
-        double2 b;
-        if (TB == OP_N) b = sB[k * LD_NMAJ + n];
-        else { b = sB[n * LD_KMAJ + k]; b.y = -b.y; }
-        br[ni] = b.x; bi[ni] = b.y; bs[ni] = b.x + b.y;
-      }
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-          dmma(acc[mi][ni][0][0], acc[mi][ni][0][1], ar[mi], br[ni]);
-          dmma(acc[mi][ni][1][0], acc[mi][ni][1][1], ai[mi], bi[ni]);
-          dmma(acc[mi][ni][2][0], acc[mi][ni][2][1], as[mi], bs[ni]);
-        }
-    }
+  const int mc = max(0, min(4, (it.m - m0 - wm + 7) / 8));
+  const int nc = max(0, min(2, (it.n - n0 - wn + 7) / 8));
+  switch ((mc == 0 || nc == 0) ? -1 : (mc - 1) * 2 + (nc - 1)) {
+    case 7: g3_mainloop<TA, TB, 4, 2>(acc, it, sAbase, sBbase, m0, n0, wm, wn, lr, lc); break;
+    case 6: g3_mainloop<TA, TB, 4, 1>(acc, it, sAbase, sBbase, m0, n0, wm, wn, lr, lc); break;
+    case 5: g3_mainloop<TA, TB, 3, 2>(acc, it, sAbase, sBbase, m0, n0, wm, wn, lr, lc); break;
+    case 4: g3_mainloop<TA, TB, 3, 1>(acc, it, sAbase, sBbase, m0, n0, wm, wn, lr, lc); break;
+    case 3: g3_mainloop<TA, TB, 2, 2>(acc, it, sAbase, sBbase, m0, n0, wm, wn, lr, lc); break;
+    case 2: g3_mainloop<TA, TB, 2, 1>(acc, it, sAbase, sBbase, m0, n0, wm, wn, lr, lc); break;
+    case 1: g3_mainloop<TA, TB, 1, 2>(acc, it, sAbase, sBbase, m0, n0, wm, wn, lr, lc); break;
+    case 0: g3_mainloop<TA, TB, 1, 1>(acc, it, sAbase, sBbase, m0, n0, wm, wn, lr, lc); break;
+    default: g3_mainloop<TA, TB, 0, 0>(acc, it, sAbase, sBbase, m0, n0, wm, wn, lr, lc); break;
   }
   cp_async_wait<0>();
 
