@@ -17,7 +17,7 @@
 // dimensions; here the k dimension stays exact (only output tiles pad).
 //
 // Per slice j (A_j = -i dt (H0 + sum_k u_kj H_k), U_j = R(A_j) with
-// R = Taylor_m(A/2^s)^(2^s), Paterson-Stockmeyer with A^2, A^3):
+// R = y(A/2^s)^(2^s), y = degree-12 Taylor polynomial in 4 products, see c_s4):
 //   forward : X_j = U_j X_{j-1}
 //   backward: C_j = X_j Lam_j^dag,  (U_j, N_j) = (R(A_j), L_R(A_j, C_j)) by
 //             forward-mode pairs,   D_j = U_j^dag N_j = L_R(A_j, X_{j-1} Lam_j^dag),
@@ -72,29 +72,24 @@ struct TinyParams {
   int nwarps;             // warps per CTA
 };
 
-// Taylor coefficients 1/k!, k = 0..21
-__constant__ double c_inv_fact[22] = {
-    1.0, 1.0, 0.5, 1.6666666666666666e-01, 4.1666666666666664e-02, 8.3333333333333332e-03,
-    1.3888888888888889e-03, 1.9841269841269841e-04, 2.4801587301587302e-05,
-    2.7557319223985893e-06, 2.7557319223985888e-07, 2.5052108385441720e-08,
-    2.0876756987868100e-09, 1.6059043836821613e-10, 1.1470745597729725e-11,
-    7.6471637318198164e-13, 4.7794773323873853e-14, 2.8114572543455206e-15,
-    1.5619206968586225e-16, 8.2206352466243295e-18, 4.1103176233121648e-19,
-    1.9572941063391263e-20};
+// Propagator R(A) = y(A / 2^s)^(2^s), y = the degree-12 Taylor polynomial of exp evaluated
+// with 4 products instead of Paterson-Stockmeyer's 5 (tools/derive_expm_schemes.py):
+//   A2 = A A, A3 = A2 A, Z = (x4 A + x5 A2 + x6 A3) A3 + z0 I + z1 A + z2 A2 + z3 A3,
+//   y = (Z + b0 I + b1 A + b2 A2 + b3 A3) Z + c0 I + c1 A + c2 A2 + c3 A3.
+// theta_12 = 0.3352 (sum_{k>12} t^k / k! <= 2^-53); each squaring doubles it, so the s4 scheme
+// with s squarings costs 4 + s products and beats every PS degree at every norm.
+// Layout: z0..z6 (z4..z6 = x4..x6), b0..b3, c0..c3.
+__constant__ double c_s4[15] = {
+    0.0, 2.1763083362520447e-12, 0.11462406647905307, 0.012167782611650191,
+    2.1931723165325633e-3, 2.7414653956657041e-4, 4.5691089927761735e-5,
+    5.5174437753427168, 1.3093238729655877, 4.3247187526118505e-3, 9.6586056829543493e-3,
+    1.0, 0.99999999998799234, -0.13243184210217061, -0.050548416421633109};
+constexpr double kTheta12 = 0.33;
 
-// Degree m = 3 nb, nb = 4..7: largest ||A|| with truncation <= 2^-53.
-__device__ __forceinline__ void choose_taylor(double nrm, int& nb, int& s) {
-  const double theta[4] = {0.33, 0.67, 1.10, 1.65};
-  int best_cost = 1 << 30;
-  nb = 4;
-  s = 0;
-  for (int i = 0; i < 4; ++i) {
-    int si = 0;
-    double x = nrm;
-    while (x > theta[i] && si < 60) { x *= 0.5; ++si; }
-    int cost = (4 + i) + 1 + si;
-    if (cost < best_cost || (cost == best_cost && si < s)) { best_cost = cost; nb = 4 + i; s = si; }
-  }
+__device__ __forceinline__ int choose_squarings(double nrm) {
+  int s = 0;
+  while (nrm > kTheta12 && s < 60) { nrm *= 0.5; ++s; }
+  return s;
 }
 
 __device__ __forceinline__ void cfma(double2& acc, const double2 a, const double2 b) {
@@ -454,7 +449,7 @@ struct TinyCtx {
   }
 
   // A tile of slice j (scaled by 2^-s) and the warp-uniform Taylor plan
-  __device__ __forceinline__ void build_a(int j, T2& a, int& nb, int& s) const {
+  __device__ __forceinline__ void build_a(int j, T2& a, int& s) const {
     double uk[kMaxControls];
 #pragma unroll
     for (int k = 0; k < kMaxControls; ++k) uk[k] = (k < K) ? up[k * N + j] : 0.0;
@@ -479,50 +474,65 @@ struct TinyCtx {
 #pragma unroll
     for (int i = 0; i < TSR; ++i) nrm = fmax(nrm, row_sum<LC>(rowsum[i]));
     nrm = warp_max(real ? nrm : 0.0);  // plan is warp-uniform, from real problems only
-    choose_taylor(nrm, nb, s);
+    s = choose_squarings(nrm);
     scale(a, ldexp(1.0, -s));
   }
 
-  // Q_t = c_{3t} I + c_{3t+1} A + c_{3t+2} A2 ;  dQ_t = c_{3t+1} dA + c_{3t+2} dA2
-  __device__ __forceinline__ void add_q(T2& t, int qi, const double2* A, const double2* A2) const {
+  // own tile entries: t += k0 I + k1 M1 + k2 M2 + k3 M3 (M3 may be null)
+  __device__ __forceinline__ void add_poly(T2& t, double k0, double k1, const double2* M1, double k2,
+                                           const double2* M2, double k3, const double2* M3) const {
 #pragma unroll
     for (int i = 0; i < TSR; ++i)
 #pragma unroll
       for (int jj = 0; jj < TSC; ++jj) {
         const int o = tl.row(i) * D + tl.col(jj);
-        t[i][jj] = cadd(t[i][jj], cadd(cscale(A[o], c_inv_fact[3 * qi + 1]), cscale(A2[o], c_inv_fact[3 * qi + 2])));
-        if (tl.rrow(i) == tl.rcol(jj)) t[i][jj].x += c_inv_fact[3 * qi];
+        double2 v = t[i][jj];
+        const double2 m1 = M1[o], m2 = M2[o];
+        v.x = fma(k1, m1.x, fma(k2, m2.x, v.x));
+        v.y = fma(k1, m1.y, fma(k2, m2.y, v.y));
+        if (M3) {
+          const double2 m3 = M3[o];
+          v.x = fma(k3, m3.x, v.x);
+          v.y = fma(k3, m3.y, v.y);
+        }
+        if (tl.rrow(i) == tl.rcol(jj)) v.x += k0;
+        t[i][jj] = v;
       }
   }
-  __device__ __forceinline__ void add_dq(T2& t, int qi, const double2* dA, const double2* dA2) const {
+  __device__ __forceinline__ void load_own(T2& t, const double2* M) const {
 #pragma unroll
     for (int i = 0; i < TSR; ++i)
 #pragma unroll
-      for (int jj = 0; jj < TSC; ++jj) {
-        const int o = tl.row(i) * D + tl.col(jj);
-        t[i][jj] = cadd(t[i][jj], cadd(cscale(dA[o], c_inv_fact[3 * qi + 1]), cscale(dA2[o], c_inv_fact[3 * qi + 2])));
-      }
+      for (int jj = 0; jj < TSC; ++jj) t[i][jj] = M[tl.row(i) * D + tl.col(jj)];
   }
 
-  // U = R(A) with A (scaled) in B2; uses B1 (A2), B4 (A3); U -> B6
-  __device__ __forceinline__ void expm_plain(int nb, int s) const {
-    T2 t;
+  // U = R(A) with A (scaled) in B2; uses B1 (A2), B4 (A3), B5 (Z); U -> B6
+  __device__ __forceinline__ void expm_plain(int s) const {
+    T2 t, w;
     tl.mul(t, B2, B2);  // A2
     tl.store(B1, t, act);
     __syncwarp();
     tl.mul(t, B1, B2);  // A3
-    tl.store(B4, t, act);
-    __syncwarp();
-    scale(t, c_inv_fact[3 * nb]);  // T = c_{3nb} A3 + Q_{nb-1}
-    add_q(t, nb - 1, B2, B1);
+    tl.store(B4, t, act);  // own entries are read back below without a sync
+    scale(t, c_s4[6]);     // x4 A + x5 A2 + x6 A3
+    add_poly(t, 0.0, c_s4[4], B2, c_s4[5], B1, 0.0, nullptr);
     tl.store(B6, t, act);
-    for (int qi = nb - 2; qi >= 0; --qi) {
-      __syncwarp();
-      tl.mul(t, B6, B4);
-      add_q(t, qi, B2, B1);
-      __syncwarp();
-      tl.store(B6, t, act);
-    }
+    __syncwarp();
+    tl.mul(t, B6, B4);  // Z = (x4 A + x5 A2 + x6 A3) A3 + z(A)
+    add_poly(t, c_s4[0], c_s4[1], B2, c_s4[2], B1, c_s4[3], B4);
+#pragma unroll
+    for (int i = 0; i < TSR; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TSC; ++jj) w[i][jj] = t[i][jj];
+    add_poly(w, c_s4[7], c_s4[8], B2, c_s4[9], B1, c_s4[10], B4);  // W = Z + b(A)
+    __syncwarp();
+    tl.store(B5, t, act);
+    tl.store(B6, w, act);
+    __syncwarp();
+    tl.mul(t, B6, B5);  // y = W Z + c(A)
+    add_poly(t, c_s4[11], c_s4[12], B2, c_s4[13], B1, c_s4[14], B4);
+    __syncwarp();
+    tl.store(B6, t, act);
     for (int r = 0; r < s; ++r) {
       __syncwarp();
       tl.mul(t, B6, B6);
@@ -532,9 +542,9 @@ struct TinyCtx {
     __syncwarp();
   }
 
-  // (U, N) = (R(A), L_R(A, Adot)) with A in B2, Adot in B3 (both scaled); uses B0, B1, B4, B5;
-  // U -> B6, N -> B7
-  __device__ __forceinline__ void expm_pair(int nb, int s) const {
+  // (U, N) = (R(A), L_R(A, Adot)) with A in B2, Adot in B3 (both scaled), forward-mode pairs
+  // through the same 4-product scheme; uses B0, B1, B4, B5; U -> B6, N -> B7
+  __device__ __forceinline__ void expm_pair(int s) const {
     T2 t, dt;
     tl.pair(t, dt, B2, B3, B2, B3);  // (A2, dA2)
     tl.store(B0, t, act);
@@ -543,22 +553,40 @@ struct TinyCtx {
     tl.pair(t, dt, B0, B1, B2, B3);  // (A3, dA3)
     tl.store(B4, t, act);
     tl.store(B5, dt, act);
-    __syncwarp();
-    scale(t, c_inv_fact[3 * nb]);
-    scale(dt, c_inv_fact[3 * nb]);
-    add_q(t, nb - 1, B2, B0);
-    add_dq(dt, nb - 1, B3, B1);
+    scale(t, c_s4[6]);
+    scale(dt, c_s4[6]);
+    add_poly(t, 0.0, c_s4[4], B2, c_s4[5], B0, 0.0, nullptr);
+    add_poly(dt, 0.0, c_s4[4], B3, c_s4[5], B1, 0.0, nullptr);
     tl.store(B6, t, act);
     tl.store(B7, dt, act);
-    for (int qi = nb - 2; qi >= 0; --qi) {
-      __syncwarp();
-      tl.pair(t, dt, B6, B7, B4, B5);
-      add_q(t, qi, B2, B0);
-      add_dq(dt, qi, B3, B1);
-      __syncwarp();
-      tl.store(B6, t, act);
-      tl.store(B7, dt, act);
-    }
+    __syncwarp();
+    tl.pair(t, dt, B6, B7, B4, B5);  // (Z, dZ) before the z(A) terms
+    add_poly(t, c_s4[0], c_s4[1], B2, c_s4[2], B0, c_s4[3], B4);
+    add_poly(dt, 0.0, c_s4[1], B3, c_s4[2], B1, c_s4[3], B5);
+    __syncwarp();
+    tl.store(B6, t, act);  // Z
+    tl.store(B7, dt, act);  // dZ
+    // own entries only from here to the next sync: W = Z + b(A) -> B4, C = c(A) -> B0,
+    // dW = dZ + b(dA) -> B5, dC = c(dA) -> B1 (each lane reads its entries before overwriting)
+    load_own(dt, B6);
+    add_poly(dt, c_s4[7], c_s4[8], B2, c_s4[9], B0, c_s4[10], B4);
+    tl.zero(t);
+    add_poly(t, c_s4[11], c_s4[12], B2, c_s4[13], B0, c_s4[14], B4);
+    tl.store(B4, dt, act);
+    tl.store(B0, t, act);
+    load_own(dt, B7);
+    add_poly(dt, 0.0, c_s4[8], B3, c_s4[9], B1, c_s4[10], B5);
+    tl.zero(t);
+    add_poly(t, 0.0, c_s4[12], B3, c_s4[13], B1, c_s4[14], B5);
+    tl.store(B5, dt, act);
+    tl.store(B1, t, act);
+    __syncwarp();
+    tl.pair(t, dt, B4, B5, B6, B7);  // (W Z, dW Z + W dZ)
+    add_poly(t, 0.0, 1.0, B0, 0.0, B0, 0.0, nullptr);  // + C
+    add_poly(dt, 0.0, 1.0, B1, 0.0, B1, 0.0, nullptr);  // + dC
+    __syncwarp();
+    tl.store(B6, t, act);
+    tl.store(B7, dt, act);
     for (int r = 0; r < s; ++r) {
       __syncwarp();
       tl.pair(t, dt, B6, B7, B6, B7);
@@ -728,11 +756,11 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   __syncwarp();
   typename C::T2 t;
   for (int j = 0; j < N; ++j) {
-    int nb, s;
-    c.build_a(j, t, nb, s);
+    int s;
+    c.build_a(j, t, s);
     c.tl.store(c.B2, t, c.act);
     __syncwarp();
-    c.expm_plain(nb, s);
+    c.expm_plain(s);
     c.mul_x(c.B6, false, X, X);  // X_j = U_j X_{j-1}
     __syncwarp();
   }
@@ -745,14 +773,14 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   // ================= backward sweep: gradient =================
   const double2 ctw = cscale(cconj(tau), 2.0 * p.weight);  // dF/du = Re(2 w conj(tau) dtau/du)
   for (int j = N - 1; j >= 0; --j) {
-    int nb, s;
+    int s;
     c.copy_x(c.B0, parkX);  // stage X_j, Lam_j
     c.copy_x(c.B1, parkL);
-    c.build_a(j, t, nb, s);
+    c.build_a(j, t, s);
     c.tl.store(c.B2, t, c.act);
     __syncwarp();
     c.seed_c(s);
-    c.expm_pair(nb, s);
+    c.expm_pair(s);
     c.copy_x(c.B0, parkX);  // restage X_j, Lam_j (B0/B1 were reused)
     c.copy_x(c.B1, parkL);
     __syncwarp();
@@ -795,11 +823,11 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_expm_kernel(TinySl
   const int prob = item / N, j = item % N;
   c.up = p.u + (size_t)prob * K * N;
   typename C::T2 t;
-  int nb, s;
-  c.build_a(j, t, nb, s);
+  int s;
+  c.build_a(j, t, s);
   c.tl.store(c.B2, t, c.act);
   __syncwarp();
-  c.expm_plain(nb, s);
+  c.expm_plain(s);
   if (c.real) c.copy_dd(sp.Uh + (size_t)item * C::DD, c.B6);
 }
 
@@ -869,12 +897,12 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_grad_kernel(TinySl
   c.copy_x(c.B0, sp.Xh + ((size_t)prob * (N + 1) + j + 1) * D * R);
   c.copy_x(c.B1, sp.Lh + ((size_t)prob * (N + 1) + j + 1) * D * R);
   typename C::T2 t;
-  int nb, s;
-  c.build_a(j, t, nb, s);
+  int s;
+  c.build_a(j, t, s);
   c.tl.store(c.B2, t, c.act);
   __syncwarp();
   c.seed_c(s);
-  c.expm_pair(nb, s);
+  c.expm_pair(s);
   double2 dtau[kMaxControls];
   c.traces(dtau);
   const double2 tau = p.tau_out[(size_t)prob * p.tau_stride];

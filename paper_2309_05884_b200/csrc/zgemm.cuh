@@ -279,11 +279,11 @@ __device__ __forceinline__ void g3_mainloop(double (&acc)[4][2][3][2], const Gem
     const double2* sB = sBbase + st * G_A_ELEMS;
     const int ksteps = (half_tail && kin == kt_per_seg - 1) ? 1 : 2;
     if (++kin == kt_per_seg) kin = 0;
-    if constexpr (MC == 0 || NC == 0) continue;
+    if constexpr (MC > 0 && NC > 0) {
 #pragma unroll 1
     for (int ks = 0; ks < ksteps; ++ks) {
       const int kk = ks * 4;
-      double ar[MC ? MC : 1], ai[MC ? MC : 1], as[MC ? MC : 1], br[NC ? NC : 1], bi[NC ? NC : 1], bs[NC ? NC : 1];
+      double ar[MC], ai[MC], as[MC], br[NC], bi[NC], bs[NC];
 #pragma unroll
       for (int mi = 0; mi < MC; ++mi) {
         const int m = wm + mi * 8 + lr, k = kk + lc;
@@ -308,6 +308,7 @@ __device__ __forceinline__ void g3_mainloop(double (&acc)[4][2][3][2], const Gem
           dmma(acc[mi][ni][1][0], acc[mi][ni][1][1], ai[mi], bi[ni]);
           dmma(acc[mi][ni][2][0], acc[mi][ni][2][1], as[mi], bs[ni]);
         }
+    }
     }
   }
 }
