@@ -97,9 +97,10 @@ int sqoc_last_schedule(const sqoc_problem* p);
 int sqoc_set_tiny_schedule(sqoc_problem* p, int schedule);
 int sqoc_last_tiny_schedule(const sqoc_problem* p);
 
-/* Propagator plan of the last large-block evaluation: Taylor degree 3*taylor_blocks,
- * `squarings` squarings, and the number of augmented-action terms (state-vector). */
-int sqoc_last_plan(const sqoc_problem* p, int* taylor_blocks, int* squarings, int* action_terms);
+/* Propagator plan of the last large-block evaluation: Taylor degree of the product scheme
+ * (12: 4 products, 18: 5 products), `squarings` squarings, and the number of
+ * augmented-action terms (state-vector). */
+int sqoc_last_plan(const sqoc_problem* p, int* taylor_degree, int* squarings, int* action_terms);
 
 /* Slice-chunk sharding (multi-GPU scan carry).  A rank builds
  * the problem for its own contiguous slice range [s, e) (n_slices = e - s, the same

@@ -625,9 +625,9 @@ int sqoc_set_tiny_schedule(sqoc_problem* p, int schedule) {
 
 int sqoc_last_tiny_schedule(const sqoc_problem* p) { return p ? p->last_tiny_mode : -1; }
 
-int sqoc_last_plan(const sqoc_problem* p, int* taylor_blocks, int* squarings, int* action_terms) {
-  if (!p || !taylor_blocks || !squarings || !action_terms) return fail(SQOC_ERR_ARG, "NULL argument");
-  *taylor_blocks = p->large ? p->large->last_nb : 0;
+int sqoc_last_plan(const sqoc_problem* p, int* taylor_degree, int* squarings, int* action_terms) {
+  if (!p || !taylor_degree || !squarings || !action_terms) return fail(SQOC_ERR_ARG, "NULL argument");
+  *taylor_degree = p->large ? p->large->last_degree : 0;
   *squarings = p->large ? p->large->last_s : 0;
   *action_terms = p->large ? p->large->last_taylor_terms : 0;
   return SQOC_OK;

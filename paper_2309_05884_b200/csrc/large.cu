@@ -9,28 +9,93 @@
 
 #include "../../include/symqoc_b200.h"
 #include "large.cuh"
+#include "schemes.h"
 
 namespace sqoc {
 
-static double inv_fact(int k) {
-  double f = 1.0;
-  for (int i = 2; i <= k; ++i) f *= i;
-  return 1.0 / f;
-}
+// ------------------------------------------------------------------ propagator schemes
+// R(A) = y(A / 2^s)^(2^s) with y an exact Taylor polynomial evaluated by an optimized product
+// scheme (coefficients derived in tools/derive_expm_schemes.py; same s4 as tiny.cuh):
+//   s4: degree 12 in 4 products (theta 0.33),  s5: degree 18 in 5 products (theta 1.10)
+// versus 5 and 7 products for Paterson-Stockmeyer at the same degrees.  Every step is one
+// GEMM C = L R whose epilogue writes up to two linear combinations alpha acc + sum_t beta_t
+// E_t + gamma I over the basis slots E = (A, A2, A3, A6) -- so the schemes need no separate
+// elementwise passes.  Slots: 0 A, 1 A2, 2 A3, 3 A6, 4 P, 5 Q, 6 W1, 7 W2, 8 Y (unsquared R).
+struct PolyOut {
+  int slot;
+  double alpha, beta[4], gamma;
+};
+struct PolyStep {
+  int L, R, nout;
+  PolyOut out[2];
+};
+struct PolyScheme {
+  int degree, nsteps;
+  double theta;
+  PolyStep step[5];
+};
+constexpr int kSlots = 9, kSlotY = 8;
 
-// Same plan rule as the tiny kernel's choose_taylor (tiny.cuh).
-static void choose_taylor_host(double nrm, int& nb, int& s) {
-  const double theta[4] = {0.33, 0.67, 1.10, 1.65};
-  int best = 1 << 30;
-  nb = 4;
-  s = 0;
-  for (int i = 0; i < 4; ++i) {
-    int si = 0;
-    double x = nrm;
-    while (x > theta[i] && si < 60) { x *= 0.5; ++si; }
-    const int cost = (4 + i) + 1 + si;
-    if (cost < best || (cost == best && si < s)) { best = cost; nb = 4 + i; s = si; }
+// s4: A2 = A A; A3 = A2 A, P = x6 A3 + x4 A + x5 A2; Z = P A3 + z(A) -> Q, W = Z + b(A) -> W1;
+//     Y = W1 Q + c(A)
+static const PolyScheme kS4 = {
+    12, 4, 0.33,
+    {{0, 0, 1, {{1, 1.0, {0, 0, 0, 0}, 0.0}}},
+     {1, 0, 2, {{2, 1.0, {0, 0, 0, 0}, 0.0}, {4, SQOC_S4_X6, {SQOC_S4_X4, SQOC_S4_X5, 0, 0}, 0.0}}},
+     {4, 2, 2,
+      {{5, 1.0, {SQOC_S4_Z1, SQOC_S4_Z2, SQOC_S4_Z3, 0}, SQOC_S4_Z0},
+       {6, 1.0, {SQOC_S4_Z1 + SQOC_S4_B1, SQOC_S4_Z2 + SQOC_S4_B2, SQOC_S4_Z3 + SQOC_S4_B3, 0},
+        SQOC_S4_Z0 + SQOC_S4_B0}}},
+     {6, 5, 1, {{8, 1.0, {SQOC_S4_C1, SQOC_S4_C2, SQOC_S4_C3, 0}, SQOC_S4_C0}}}}};
+
+// s5: A2 = A A; A3 = A2 A, P = A + be2 A2 + be3 A3; A6 = A3 A3, Q = ga2 A2 + ga3 A3 + ga6 A6;
+//     Z = P Q -> W1 = Z + b(A), W2 = Z + e(A);  Y = W1 W2 + c(A)
+static const PolyScheme kS5 = {
+    18, 5, 1.10,
+    {{0, 0, 1, {{1, 1.0, {0, 0, 0, 0}, 0.0}}},
+     {1, 0, 2, {{2, 1.0, {0, 0, 0, 0}, 0.0}, {4, SQOC_S5_BE3, {1.0, SQOC_S5_BE2, 0, 0}, 0.0}}},
+     {2, 2, 2, {{3, 1.0, {0, 0, 0, 0}, 0.0}, {5, SQOC_S5_GA6, {0, SQOC_S5_GA2, SQOC_S5_GA3, 0}, 0.0}}},
+     {4, 5, 2,
+      {{6, 1.0, {SQOC_S5_B1, SQOC_S5_B2, SQOC_S5_B3, SQOC_S5_B6}, SQOC_S5_B0},
+       {7, 1.0, {SQOC_S5_E1, SQOC_S5_E2, SQOC_S5_E3, SQOC_S5_E6}, SQOC_S5_E0}}},
+     {6, 7, 1, {{8, 1.0, {SQOC_S5_C1, SQOC_S5_C2, SQOC_S5_C3, SQOC_S5_C6}, SQOC_S5_C0}}}}};
+
+static int squarings_for(double nrm, double theta) {
+  int s = 0;
+  while (nrm > theta && s < 60) { nrm *= 0.5; ++s; }
+  return s;
+}
+// Cheapest scheme for the norm bound: products + squarings (ties -> fewer squarings).
+static const PolyScheme* choose_scheme(double nrm, int& s) {
+  const int s4 = squarings_for(nrm, kS4.theta), s5 = squarings_for(nrm, kS5.theta);
+  if (4 + s4 < 5 + s5) {
+    s = s4;
+    return &kS4;
   }
+  s = s5;
+  return &kS5;
+}
+static const PolyScheme& scheme_of(int degree) { return degree == 12 ? kS4 : kS5; }
+
+static GemmArgs step_args(const PolyStep& st) {
+  GemmArgs a{};
+  const PolyOut& o = st.out[0];
+  a.alpha = o.alpha;
+  a.beta0 = o.beta[0];
+  a.beta1 = o.beta[1];
+  a.beta2 = o.beta[2];
+  a.beta3 = o.beta[3];
+  a.gamma = o.gamma;
+  if (st.nout > 1) {
+    const PolyOut& q = st.out[1];
+    a.alpha2 = q.alpha;
+    a.beta2_0 = q.beta[0];
+    a.beta2_1 = q.beta[1];
+    a.beta2_2 = q.beta[2];
+    a.beta2_3 = q.beta[3];
+    a.gamma2 = q.gamma;
+  }
+  return a;
 }
 
 // ------------------------------------------------------------------ kernels
@@ -68,29 +133,6 @@ __global__ void build_a_kernel(int j0, int K, int N, const double* __restrict__ 
       a.y = fma(uk[k], e.y, a.y);
     }
     out[i] = make_double2(a.x * scale, a.y * scale);
-  }
-}
-
-// T = cm A3 + c0 I + c1 A + c2 A2 ;  dT = cm dA3 + c1 Ad + c2 dA2 (when pair); slice batch on blockIdx.z
-__global__ void horner_init_kernel(int pair, const int* __restrict__ dims, const size_t* __restrict__ off, double cm,
-                                   double c0, double c1, double c2, const double2* __restrict__ A,
-                                   const double2* __restrict__ A2, const double2* __restrict__ A3,
-                                   const double2* __restrict__ Ad, const double2* __restrict__ dA2,
-                                   const double2* __restrict__ dA3, double2* __restrict__ T, double2* __restrict__ dT,
-                                   size_t slice_stride) {
-  const int b = blockIdx.y;
-  const int d = dims[b];
-  const size_t dd = (size_t)d * d;
-  const size_t base = blockIdx.z * slice_stride + off[b];
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < dd; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t o = base + i;
-    if (T) {
-      double2 t = make_double2(cm * A3[o].x + c1 * A[o].x + c2 * A2[o].x, cm * A3[o].y + c1 * A[o].y + c2 * A2[o].y);
-      if (i / d == i % d) t.x += c0;
-      T[o] = t;
-    }
-    if (pair)
-      dT[o] = make_double2(cm * dA3[o].x + c1 * Ad[o].x + c2 * dA2[o].x, cm * dA3[o].y + c1 * Ad[o].y + c2 * dA2[o].y);
   }
 }
 
@@ -367,7 +409,7 @@ static cudaError_t launch_gemm(const GemmItem* items, int n, int tiles, GemmArgs
   return cudaGetLastError();
 }
 
-enum Op { F_A2, F_A3, F_H, F_S, F_X, B_C, B_P2, B_P3, B_H, B_S, B_D, B_XL };
+enum Op { F_STEP, F_S, F_X, B_C, B_STEP, B_S, B_D, B_XL };
 
 static int tiles_of(int m, int n) { return ((m + GBM - 1) / GBM) * ((n + GBN - 1) / GBN); }
 
@@ -381,6 +423,36 @@ static GemmItem mk(const double2* A0, const double2* B0, const double2* A1, cons
   return it;
 }
 
+// Work-list item(s) of scheme step k for one d x d block.  slot(c) / dslot(c) give the block's
+// matrix for scheme slot c and its derivative.  fwd: C = L R (+ epilogue combinations over the
+// basis slots); deriv: dC = L dR + dL R (+ the same combinations over the derivative basis,
+// no identity term).
+template <class SF, class DF>
+static void push_step(std::vector<GemmItem>& v, const PolyScheme& sc, int k, int d, SF slot, DF dslot, bool fwd,
+                      bool deriv) {
+  const PolyStep& st = sc.step[k];
+  bool used[4] = {false, false, false, false};
+  for (int o = 0; o < st.nout; ++o)
+    for (int t = 0; t < 4; ++t) used[t] = used[t] || st.out[o].beta[t] != 0.0;
+  auto epi = [&](GemmItem& it, auto S) {
+    const double2** E[4] = {&it.E0, &it.E1, &it.E2, &it.E3};
+    for (int t = 0; t < 4; ++t) *E[t] = used[t] ? S(t) : nullptr;
+    it.C2 = st.nout > 1 ? S(st.out[1].slot) : nullptr;
+  };
+  if (fwd) {
+    GemmItem it = mk(slot(st.L), slot(st.R), 0, 0, slot(st.out[0].slot), 0, 0, d, d, d, 1, d, d, d, 1);
+    epi(it, slot);
+    v.push_back(it);
+  }
+  if (deriv) {
+    GemmItem it = mk(slot(st.L), dslot(st.R), dslot(st.L), slot(st.R), dslot(st.out[0].slot), 0, 0, d, d, d, 2, d, d,
+                     d, 0);
+    epi(it, dslot);
+    v.push_back(it);
+  }
+}
+
+// Sequential schedule lists.  F_STEP / B_STEP: p = step index, q = scheme degree.
 static std::pair<GemmItem*, int> get_list(LargeGroup& g, int op, int p, int q, int r, int* tiles_out) {
   auto key = std::make_tuple(op, p, q, r);
   auto found = g.lists.find(key);
@@ -389,28 +461,33 @@ static std::pair<GemmItem*, int> get_list(LargeGroup& g, int op, int p, int q, i
     for (int b = 0; b < g.nblk; ++b) {
       const int d = g.blocks[b].d, R = g.gate ? d : 1;
       const size_t o = g.off[b], orr = g.offr[b];
-      double2 *A = g.A + o, *Ad = g.Ad + o, *A2 = g.A2 + o, *dA2 = g.dA2 + o, *A3 = g.A3 + o, *dA3 = g.dA3 + o;
+      double2 *Ad = g.Ad + o;
       double2 *Tp = g.T[p] + o, *Tn = g.T[1 - p] + o, *dTp = g.dT[p] + o, *dTn = g.dT[1 - p] + o;
       double2 *Xq = g.X[q] + orr, *Xn = g.X[1 - q] + orr, *Lr = g.L[r] + orr, *Ln = g.L[1 - r] + orr;
+      auto slot = [&](int c) -> double2* {
+        switch (c) {
+          case 0: return g.A + o;
+          case 1: return g.A2 + o;
+          case 2: return g.A3 + o;
+          case kSlotY: return g.T[0] + o;
+          default: return g.xs[c - 3] + o;
+        }
+      };
+      auto dslot = [&](int c) -> double2* {
+        switch (c) {
+          case 0: return g.Ad + o;
+          case 1: return g.dA2 + o;
+          case 2: return g.dA3 + o;
+          case kSlotY: return g.dT[0] + o;
+          default: return g.dxs[c - 3] + o;
+        }
+      };
       switch (op) {
-        case F_A2: v.push_back(mk(A, A, 0, 0, A2, 0, 0, d, d, d, 1, d, d, d, 0)); break;
-        case F_A3: v.push_back(mk(A2, A, 0, 0, A3, 0, 0, d, d, d, 1, d, d, d, 0)); break;
-        case F_H: v.push_back(mk(Tp, A3, 0, 0, Tn, A, A2, d, d, d, 1, d, d, d, 1)); break;
+        case F_STEP: push_step(v, scheme_of(q), p, d, slot, dslot, true, false); break;
+        case B_STEP: push_step(v, scheme_of(q), p, d, slot, dslot, true, true); break;
         case F_S: v.push_back(mk(Tp, Tp, 0, 0, Tn, 0, 0, d, d, d, 1, d, d, d, 0)); break;
         case F_X: v.push_back(mk(Tp, Xq, 0, 0, Xn, 0, 0, d, R, d, 1, d, R, R, 0)); break;
         case B_C: v.push_back(mk(Xq, Lr, 0, 0, Ad, 0, 0, d, d, R, 1, R, R, d, 0)); break;
-        case B_P2:
-          v.push_back(mk(A, A, 0, 0, A2, 0, 0, d, d, d, 1, d, d, d, 0));
-          v.push_back(mk(A, Ad, Ad, A, dA2, 0, 0, d, d, d, 2, d, d, d, 0));
-          break;
-        case B_P3:
-          v.push_back(mk(A2, A, 0, 0, A3, 0, 0, d, d, d, 1, d, d, d, 0));
-          v.push_back(mk(A2, Ad, dA2, A, dA3, 0, 0, d, d, d, 2, d, d, d, 0));
-          break;
-        case B_H:
-          v.push_back(mk(Tp, A3, 0, 0, Tn, A, A2, d, d, d, 1, d, d, d, 1));
-          v.push_back(mk(Tp, dA3, dTp, A3, dTn, Ad, dA2, d, d, d, 2, d, d, d, 0));
-          break;
         case B_S:
           v.push_back(mk(Tp, Tp, 0, 0, Tn, 0, 0, d, d, d, 1, d, d, d, 0));
           v.push_back(mk(Tp, dTp, dTp, Tp, dTn, 0, 0, d, d, d, 2, d, d, d, 0));
@@ -499,6 +576,10 @@ int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, 
   const size_t bytes = g.total * sizeof(double2);
   double2** sq[] = {&g.A, &g.Ad, &g.A2, &g.dA2, &g.A3, &g.dA3, &g.T[0], &g.T[1], &g.dT[0], &g.dT[1]};
   for (auto pp : sq) LCHK(cudaMalloc(pp, bytes));
+  for (int i = 0; i < 5; ++i) {
+    LCHK(cudaMalloc(&g.xs[i], bytes));
+    LCHK(cudaMalloc(&g.dxs[i], bytes));
+  }
   double2** rect[] = {&g.X[0], &g.X[1], &g.L[0], &g.L[1]};
   for (auto pp : rect) LCHK(cudaMalloc(pp, g.totalr * sizeof(double2)));
   LCHK(cudaMalloc(&g.trace_part, (size_t)g.trace_tiles * K * sizeof(double2)));
@@ -582,6 +663,10 @@ void large_free(LargeGroup& g) {
   double2* bufs[] = {g.A, g.Ad, g.A2, g.dA2, g.A3, g.dA3, g.T[0], g.T[1], g.dT[0], g.dT[1],
                      g.X[0], g.X[1], g.L[0], g.L[1], g.trace_part, g.tau_dev};
   for (auto b : bufs) cudaFree(b);
+  for (int i = 0; i < 5; ++i) {
+    cudaFree(g.xs[i]);
+    cudaFree(g.dxs[i]);
+  }
   cudaFree(g.norm_dev);
   cudaFree(g.gnorm_dev);
   cudaFree(g.d_dev);
@@ -593,8 +678,9 @@ void large_free(LargeGroup& g) {
   cudaFree(g.w_dev);
   cudaFree(g.gidx_dev);
   cudaFree(g.tile_off_dev);
-  double2* hb[] = {g.h_chain, g.h_X, g.h_L, g.h_dA, g.h_dA2, g.h_dA3, g.h_dH[0], g.h_dH[1], g.h_g};
+  double2* hb[] = {g.h_chain, g.h_X, g.h_L, g.h_dH[0], g.h_dH[1], g.h_g, g.h_I};
   for (auto x : hb) cudaFree(x);
+  for (auto x : g.h_d) cudaFree(x);
   for (auto m : g.gent_mem) cudaFree(m);
   g.gent_mem.clear();
   for (auto m : g.gentall_mem) cudaFree(m);
@@ -646,35 +732,40 @@ static int bc_tau(LargeGroup& g, const double2* XN, const LargeArgs& a, int s_id
 }
 
 // ------------------------------------------------------------------ history schedule
-enum HOp { H_A2, H_A3, H_H, H_S, H_X, H_L, H_B, H_DA2, H_DA3, H_DH, H_DS, H_XP1, H_XP2, H_XP3, H_LP1, H_LP2, H_LP3 };
+enum HOp { H_STEP, H_S, H_X, H_L, H_B, H_DSTEP, H_DS, H_XP1, H_XP2, H_XP3, H_LP1, H_LP2, H_LP3 };
 
+// h_chain slots 0..8 (scheme), then S_1..S_s; derivative arrays h_d[0..7] + h_dH[2].
 static size_t history_bytes(const LargeGroup& g, int C) {
   const size_t N = g.N;
-  return sizeof(double2) * ((size_t)(C + 5) * N * g.total + 2 * (N + 1) * g.totalr + N * g.nblk * g.K);
+  return sizeof(double2) * ((size_t)(C + 10) * N * g.total + 2 * (N + 1) * g.totalr + N * g.nblk * g.K);
 }
 
 static void hist_free(LargeGroup& g) {
-  double2* hb[] = {g.h_chain, g.h_X, g.h_L, g.h_dA, g.h_dA2, g.h_dA3, g.h_dH[0], g.h_dH[1], g.h_g, g.h_I};
+  double2* hb[] = {g.h_chain, g.h_X, g.h_L, g.h_dH[0], g.h_dH[1], g.h_g, g.h_I};
   for (auto x : hb) cudaFree(x);
-  g.h_chain = g.h_X = g.h_L = g.h_dA = g.h_dA2 = g.h_dA3 = g.h_dH[0] = g.h_dH[1] = g.h_g = g.h_I = nullptr;
+  for (auto& x : g.h_d) {
+    cudaFree(x);
+    x = nullptr;
+  }
+  g.h_chain = g.h_X = g.h_L = g.h_dH[0] = g.h_dH[1] = g.h_g = g.h_I = nullptr;
   for (auto m : g.hlist_mem) cudaFree(m);
   g.hlist_mem.clear();
   g.hlists.clear();
   g.h_C = 0;
 }
 
-static int hist_alloc(LargeGroup& g, int nb, int sq) {
-  const int C = 3 + nb + sq;
-  g.h_nb = nb;
+static int hist_alloc(LargeGroup& g, int degree, int sq) {
+  const int C = kSlots + sq;
+  g.h_deg = degree;
   g.h_s = sq;
-  if (C <= g.h_C) return SQOC_OK;  // buffers large enough; lists depend on (nb, s) via keys
+  if (C <= g.h_C) return SQOC_OK;  // buffers large enough; lists depend on (degree, s) via keys
   hist_free(g);
   const size_t N = g.N, sq_bytes = N * g.total * sizeof(double2);
   LCHK(cudaMalloc(&g.h_chain, (size_t)C * sq_bytes));
   LCHK(cudaMalloc(&g.h_X, (N + 1) * g.totalr * sizeof(double2)));
   LCHK(cudaMalloc(&g.h_L, (N + 1) * g.totalr * sizeof(double2)));
-  double2** d5[] = {&g.h_dA, &g.h_dA2, &g.h_dA3, &g.h_dH[0], &g.h_dH[1]};
-  for (auto pp : d5) LCHK(cudaMalloc(pp, sq_bytes));
+  for (auto& x : g.h_d) LCHK(cudaMalloc(&x, sq_bytes));
+  for (auto& x : g.h_dH) LCHK(cudaMalloc(&x, sq_bytes));
   LCHK(cudaMalloc(&g.h_g, N * g.nblk * g.K * sizeof(double2)));
   if (g.gate) {  // identity blocks for the chunked prefix / suffix scans
     std::vector<double2> eye(g.totalr, make_double2(0.0, 0.0));
@@ -689,37 +780,34 @@ static int hist_alloc(LargeGroup& g, int nb, int sq) {
 
 // Work list for history op `op` (index idx, parity p), over slices [i0, i1) x blocks.
 static ListRef hist_list(LargeGroup& g, int op, int idx, int p, int i0, int i1) {
-  auto key = std::make_tuple(op * 1000000 + idx * 4 + p, g.h_nb * 100 + g.h_s, i0, i1);
+  auto key = std::make_tuple(op * 1000000 + idx * 4 + p, g.h_deg * 100 + g.h_s, i0, i1);
   auto it = g.hlists.find(key);
   if (it != g.hlists.end()) return it->second;
   std::vector<GemmItem> v;
-  const int nb = g.h_nb;
+  const PolyScheme& sc = scheme_of(g.h_deg);
   for (int i = i0; i < i1; ++i)
     for (int b = 0; b < g.nblk; ++b) {
       const int d = g.blocks[b].d, R = g.gate ? d : 1;
       const size_t o = (size_t)i * g.total + g.off[b];
       auto ch = [&](int c) { return g.h_chain + (size_t)c * g.N * g.total + o; };
-      double2 *A = ch(0), *A2 = ch(1), *A3 = ch(2), *U = ch(3 + nb + g.h_s - 1);
-      double2 *dA = g.h_dA + o, *dA2 = g.h_dA2 + o, *dA3 = g.h_dA3 + o;
+      double2* U = ch(kSlotY + g.h_s);
+      double2* dA = g.h_d[0] + o;
       double2 *dHp = g.h_dH[p] + o, *dHn = g.h_dH[1 - p] + o;
       double2* Xi = g.h_X + (size_t)i * g.totalr + g.offr[b];
       double2* Xn = g.h_X + (size_t)(i + 1) * g.totalr + g.offr[b];
       double2* Li = g.h_L + (size_t)i * g.totalr + g.offr[b];
       double2* Ln = g.h_L + (size_t)(i + 1) * g.totalr + g.offr[b];
+      auto dslot = [&](int c) -> double2* { return c == kSlotY ? g.h_dH[0] + o : g.h_d[c] + o; };
       switch (op) {
-        case H_A2: v.push_back(mk(A, A, 0, 0, A2, 0, 0, d, d, d, 1, d, d, d, 0)); break;
-        case H_A3: v.push_back(mk(A2, A, 0, 0, A3, 0, 0, d, d, d, 1, d, d, d, 0)); break;
-        case H_H: v.push_back(mk(ch(3 + idx - 1), A3, 0, 0, ch(3 + idx), A, A2, d, d, d, 1, d, d, d, 1)); break;
-        case H_S: v.push_back(mk(ch(3 + nb - 1 + idx - 1), ch(3 + nb - 1 + idx - 1), 0, 0, ch(3 + nb - 1 + idx), 0, 0,
+        case H_STEP: push_step(v, sc, idx, d, ch, dslot, true, false); break;
+        case H_DSTEP: push_step(v, sc, idx, d, ch, dslot, false, true); break;
+        case H_S: v.push_back(mk(ch(kSlotY + idx - 1), ch(kSlotY + idx - 1), 0, 0, ch(kSlotY + idx), 0, 0,
                                  d, d, d, 1, d, d, d, 0)); break;
         case H_X: v.push_back(mk(U, Xi, 0, 0, Xn, 0, 0, d, R, d, 1, d, R, R, 0)); break;
         case H_L: v.push_back(mk(U, Ln, 0, 0, Li, 0, 0, d, R, d, 1, d, R, R, 0)); break;
         case H_B: v.push_back(mk(Xi, Ln, 0, 0, dA, 0, 0, d, d, R, 1, R, R, d, 0)); break;
-        case H_DA2: v.push_back(mk(A, dA, dA, A, dA2, 0, 0, d, d, d, 2, d, d, d, 0)); break;
-        case H_DA3: v.push_back(mk(A2, dA, dA2, A, dA3, 0, 0, d, d, d, 2, d, d, d, 0)); break;
-        case H_DH: v.push_back(mk(dHp, A3, ch(3 + idx - 1), dA3, dHn, dA, dA2, d, d, d, 2, d, d, d, 0)); break;
         case H_DS: {
-          double2* S = ch(3 + nb - 1 + idx - 1);
+          double2* S = ch(kSlotY + idx - 1);
           v.push_back(mk(S, dHp, dHp, S, dHn, 0, 0, d, d, d, 2, d, d, d, 0));
           break;
         }
@@ -761,20 +849,20 @@ static int hgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArgs
 // Chunked prefix / suffix scans of the X / Lam recurrences (gate): depth ~2 sqrt(N)
 // launches instead of N, each batched over chunks x blocks.  Lc = chunk length.
 //   X: chunk 0 runs exactly from X_0; chunks c >= 1 form local prefixes P_i = U_i ... U_{cLc}
-//      (into h_dA2), the chunk starts X[cLc] = P_{cLc-1} X[(c-1)Lc] are carried sequentially,
+//      (into h_d[1]), the chunk starts X[cLc] = P_{cLc-1} X[(c-1)Lc] are carried sequentially,
 //      and X[i+1] = P_i X[cLc] fixes every slice up in one launch.
-//   Lam: the mirror image with local suffixes Q_i = U_i^dag ... U_{(c+1)Lc-1}^dag (into h_dA3).
+//   Lam: the mirror image with local suffixes Q_i = U_i^dag ... U_{(c+1)Lc-1}^dag (into h_d[2]).
 static ListRef scan_list(LargeGroup& g, int op, int idx, int Lc, int C) {
-  auto key = std::make_tuple(op * 1000000 + idx * 4, g.h_nb * 100 + g.h_s, Lc, C);
+  auto key = std::make_tuple(op * 1000000 + idx * 4, g.h_deg * 100 + g.h_s, Lc, C);
   auto it = g.hlists.find(key);
   if (it != g.hlists.end()) return it->second;
-  const int N = g.N, nb = g.h_nb;
+  const int N = g.N;
   std::vector<GemmItem> v;
-  auto U = [&](int i, int b) { return g.h_chain + ((size_t)(3 + nb + g.h_s - 1) * N + i) * g.total + g.off[b]; };
+  auto U = [&](int i, int b) { return g.h_chain + ((size_t)(kSlotY + g.h_s) * N + i) * g.total + g.off[b]; };
   auto X = [&](int i, int b) { return g.h_X + (size_t)i * g.totalr + g.offr[b]; };
   auto L = [&](int i, int b) { return g.h_L + (size_t)i * g.totalr + g.offr[b]; };
-  auto P = [&](int i, int b) { return g.h_dA2 + (size_t)i * g.total + g.off[b]; };
-  auto Q = [&](int i, int b) { return g.h_dA3 + (size_t)i * g.total + g.off[b]; };
+  auto P = [&](int i, int b) { return g.h_d[1] + (size_t)i * g.total + g.off[b]; };  // scratch before the
+  auto Q = [&](int i, int b) { return g.h_d[2] + (size_t)i * g.total + g.off[b]; };  // derivative chain
   auto I = [&](int b) { return g.h_I + g.offr[b]; };
   for (int b = 0; b < g.nblk; ++b) {
     const int d = g.blocks[b].d;
@@ -870,38 +958,24 @@ static int history_scans(LargeGroup& g, bool do_x, bool do_l, cudaStream_t st) {
   return SQOC_OK;
 }
 
-static int large_eval_history(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, int nb, int sq,
+static int large_eval_history(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, int sq,
                               cudaStream_t st) {
   const int K = g.K, N = g.N, nblk = g.nblk;
+  const PolyScheme& sc = scheme_of(g.h_deg);
   int maxd = 0;
   for (auto& b : g.blocks) maxd = std::max(maxd, b.d);
   const unsigned ew_x = (unsigned)std::max<size_t>(1, std::min<size_t>(((size_t)maxd * maxd + 255) / 256, 64));
   const dim3 grid_all(ew_x, nblk, N);
   const double scale = std::ldexp(1.0, -sq);
-  const double cm = inv_fact(3 * nb);
   const size_t stride = g.total;
-  auto ch = [&](int c) { return g.h_chain + (size_t)c * N * g.total; };
   GemmArgs one{1.0, 0.0, 0.0, 0.0};
   int rc;
   // ---- forward: all propagators, every intermediate kept ----
-  build_a_kernel<<<grid_all, 256, 0, st>>>(0, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, ch(0), stride);
+  build_a_kernel<<<grid_all, 256, 0, st>>>(0, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.h_chain, stride);
   LCHK(cudaGetLastError());
   g.launches++;
-  if ((rc = hgemm(g, H_A2, 0, 0, 0, N, one, st))) return rc;
-  if ((rc = hgemm(g, H_A3, 0, 0, 0, N, one, st))) return rc;
-  {
-    const int q = nb - 1;
-    horner_init_kernel<<<grid_all, 256, 0, st>>>(0, g.d_dev, g.off_dev, cm, inv_fact(3 * q), inv_fact(3 * q + 1),
-                                                 inv_fact(3 * q + 2), ch(0), ch(1), ch(2), nullptr, nullptr, nullptr,
-                                                 ch(3), nullptr, stride);
-    LCHK(cudaGetLastError());
-    g.launches++;
-  }
-  for (int t = 1; t <= nb - 1; ++t) {
-    const int q = nb - 1 - t;
-    if ((rc = hgemm(g, H_H, t, 0, 0, N, GemmArgs{1.0, inv_fact(3 * q + 1), inv_fact(3 * q + 2), inv_fact(3 * q)}, st)))
-      return rc;
-  }
+  for (int k = 0; k < sc.nsteps; ++k)
+    if ((rc = hgemm(g, H_STEP, k, 0, 0, N, step_args(sc.step[k]), st))) return rc;
   for (int i = 1; i <= sq; ++i)
     if ((rc = hgemm(g, H_S, i, 0, 0, N, one, st))) return rc;
   // ---- forward / backward recurrences (sequential over slices, batched over blocks) ----
@@ -925,22 +999,9 @@ static int large_eval_history(LargeGroup& g, const LargeArgs& a, int s_idx, cons
   }
   // ---- Frechet derivatives of every slice: L_R(A_i, X_i Lam_{i+1}^dag), derivative-only chain ----
   if ((rc = hgemm(g, H_B, 0, 0, 0, N, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
-  if ((rc = hgemm(g, H_DA2, 0, 0, 0, N, one, st))) return rc;
-  if ((rc = hgemm(g, H_DA3, 0, 0, 0, N, one, st))) return rc;
-  {
-    const int q = nb - 1;
-    horner_init_kernel<<<grid_all, 256, 0, st>>>(1, g.d_dev, g.off_dev, cm, 0.0, inv_fact(3 * q + 1),
-                                                 inv_fact(3 * q + 2), nullptr, nullptr, nullptr, g.h_dA, g.h_dA2,
-                                                 g.h_dA3, nullptr, g.h_dH[0], stride);
-    LCHK(cudaGetLastError());
-    g.launches++;
-  }
+  for (int k = 0; k < sc.nsteps; ++k)
+    if ((rc = hgemm(g, H_DSTEP, k, 0, 0, N, step_args(sc.step[k]), st))) return rc;
   int p = 0;
-  for (int t = 1; t <= nb - 1; ++t) {
-    const int q = nb - 1 - t;
-    if ((rc = hgemm(g, H_DH, t, p, 0, N, GemmArgs{1.0, inv_fact(3 * q + 1), inv_fact(3 * q + 2), 0.0}, st))) return rc;
-    p ^= 1;
-  }
   for (int i = 1; i <= sq; ++i) {
     if ((rc = hgemm(g, H_DS, i, p, 0, N, one, st))) return rc;
     p ^= 1;
@@ -955,7 +1016,8 @@ static int large_eval_history(LargeGroup& g, const LargeArgs& a, int s_idx, cons
 }
 
 // ------------------------------------------------------------------ state-vector schedule
-enum SOp { SV_A2, SV_A3, SV_H, SV_S, SV_PSI, SV_CHI, SV_W };
+enum SOp { SV_STEP, SV_S, SV_PSI, SV_CHI, SV_W };
+constexpr int kSvSlots = kSlots + 1;  // scheme slots + squaring partner
 
 static size_t sv_fixed_bytes(const LargeGroup& g) {
   const size_t N = g.N, K = g.K;
@@ -978,7 +1040,7 @@ static int sv_alloc(LargeGroup& g, bool with_u) {
   LCHK(cudaMalloc(&g.sv_U, N * g.total * sizeof(double2)));
   size_t free_b = 0, total_b = 0;
   LCHK(cudaMemGetInfo(&free_b, &total_b));
-  const size_t per_slice = 5 * g.total * sizeof(double2);
+  const size_t per_slice = kSvSlots * g.total * sizeof(double2);
   g.sv_S = (int)std::max<size_t>(1, std::min<size_t>(N, (size_t)(0.5 * (double)free_b) / per_slice));
   g.sv_S = std::min(g.sv_S, 64);
   LCHK(cudaMalloc(&g.sv_chunk, (size_t)g.sv_S * per_slice));
@@ -986,7 +1048,7 @@ static int sv_alloc(LargeGroup& g, bool with_u) {
 }
 
 static ListRef sv_list(LargeGroup& g, int op, int idx, int p, int i0, int i1) {
-  auto key = std::make_tuple(2000000000 + op * 1000000 + idx * 4 + p, g.last_nb * 100 + g.last_s, i0, i1);
+  auto key = std::make_tuple(2000000000 + op * 1000000 + idx * 4 + p, g.last_degree * 100 + g.last_s, i0, i1);
   auto it = g.hlists.find(key);
   if (it != g.hlists.end()) return it->second;
   std::vector<GemmItem> v;
@@ -1002,19 +1064,19 @@ static ListRef sv_list(LargeGroup& g, int op, int idx, int p, int i0, int i1) {
       v.push_back(mk(Vb, Bt + (size_t)idx * d * d, 0, 0, Wb, 0, 0, (int)rows, d, d, 1, d, d, d, 0));
     }
   } else {
+    const PolyScheme& sc = scheme_of(g.last_degree);
     for (int z = i0; z < i1; ++z)
       for (int b = 0; b < g.nblk; ++b) {
         const int d = g.blocks[b].d;
-        double2 *A = cb(0, z, b), *A2 = cb(1, z, b), *A3 = cb(2, z, b), *Tp = cb(3 + p, z, b), *Tn = cb(4 - p, z, b);
+        double2 *Tp = cb(kSlotY + p, z, b), *Tn = cb(kSlotY + 1 - p, z, b);
         double2* U = g.sv_U + (size_t)z * sl + g.off[b];
         double2* Pi = g.sv_psi + (size_t)z * g.totalr + g.offr[b];
         double2* Pn = g.sv_psi + (size_t)(z + 1) * g.totalr + g.offr[b];
         double2* Ci = g.sv_chi + (size_t)z * g.totalr + g.offr[b];
         double2* Cn = g.sv_chi + (size_t)(z + 1) * g.totalr + g.offr[b];
+        auto slot = [&](int c) { return cb(c, z, b); };
         switch (op) {
-          case SV_A2: v.push_back(mk(A, A, 0, 0, A2, 0, 0, d, d, d, 1, d, d, d, 0)); break;
-          case SV_A3: v.push_back(mk(A2, A, 0, 0, A3, 0, 0, d, d, d, 1, d, d, d, 0)); break;
-          case SV_H: v.push_back(mk(Tp, A3, 0, 0, Tn, A, A2, d, d, d, 1, d, d, d, 1)); break;
+          case SV_STEP: push_step(v, sc, idx, d, slot, slot, true, false); break;
           case SV_S: v.push_back(mk(Tp, Tp, 0, 0, Tn, 0, 0, d, d, d, 1, d, d, d, 0)); break;
           case SV_PSI: v.push_back(mk(U, Pi, 0, 0, Pn, 0, 0, d, 1, d, 1, d, 1, 1, 0)); break;
           case SV_CHI: v.push_back(mk(U, Cn, 0, 0, Ci, 0, 0, d, 1, d, 1, d, 1, 1, 0)); break;
@@ -1065,14 +1127,14 @@ static int taylor_terms(double beta) {
 
 static int sv_gradient(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, double bound, cudaStream_t st);
 
-static int large_eval_state_vector(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, int nb, int sq,
+static int large_eval_state_vector(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, int sq,
                                    double bound, cudaStream_t st) {
   const int K = g.K, N = g.N, nblk = g.nblk;
+  const PolyScheme& sc = scheme_of(g.last_degree);
   int maxd = 0;
   for (auto& b : g.blocks) maxd = std::max(maxd, b.d);
   const unsigned ew_x = (unsigned)std::max<size_t>(1, std::min<size_t>(((size_t)maxd * maxd + 255) / 256, 256));
   const double scale = std::ldexp(1.0, -sq);
-  const double cm = inv_fact(3 * nb);
   const size_t S = g.sv_S, sl = g.total;
   GemmArgs one{1.0, 0.0, 0.0, 0.0};
   int rc;
@@ -1083,27 +1145,14 @@ static int large_eval_state_vector(LargeGroup& g, const LargeArgs& a, int s_idx,
     build_a_kernel<<<grid, 256, 0, st>>>(i0, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.sv_chunk, sl);
     LCHK(cudaGetLastError());
     g.launches++;
-    if ((rc = svgemm(g, SV_A2, 0, 0, 0, n_here, one, st))) return rc;
-    if ((rc = svgemm(g, SV_A3, 0, 0, 0, n_here, one, st))) return rc;
-    const int q0 = nb - 1;
-    horner_init_kernel<<<grid, 256, 0, st>>>(0, g.d_dev, g.off_dev, cm, inv_fact(3 * q0), inv_fact(3 * q0 + 1),
-                                             inv_fact(3 * q0 + 2), g.sv_chunk, g.sv_chunk + S * sl,
-                                             g.sv_chunk + 2 * S * sl, nullptr, nullptr, nullptr,
-                                             g.sv_chunk + 3 * S * sl, nullptr, sl);
-    LCHK(cudaGetLastError());
-    g.launches++;
+    for (int k = 0; k < sc.nsteps; ++k)
+      if ((rc = svgemm(g, SV_STEP, k, 0, 0, n_here, step_args(sc.step[k]), st))) return rc;
     int p = 0;
-    for (int t = nb - 2; t >= 0; --t) {
-      if ((rc = svgemm(g, SV_H, 0, p, 0, n_here, GemmArgs{1.0, inv_fact(3 * t + 1), inv_fact(3 * t + 2), inv_fact(3 * t)},
-                       st)))
-        return rc;
-      p ^= 1;
-    }
     for (int i = 0; i < sq; ++i) {
       if ((rc = svgemm(g, SV_S, 0, p, 0, n_here, one, st))) return rc;
       p ^= 1;
     }
-    LCHK(cudaMemcpyAsync(g.sv_U + (size_t)i0 * sl, g.sv_chunk + (size_t)(3 + p) * S * sl,
+    LCHK(cudaMemcpyAsync(g.sv_U + (size_t)i0 * sl, g.sv_chunk + (size_t)(kSlotY + p) * S * sl,
                          (size_t)n_here * sl * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   }
   // ---- psi / chi sweeps (sequential over slices, batched over blocks) ----
@@ -1264,7 +1313,7 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
   g.launches = 0;
   for (int s = 0; s < a.batch; ++s) {
     const double* u = a.u + (size_t)s * K * N;
-    // ---- plan (nb, s) from the norm bound over all slices and blocks ----
+    // ---- plan (scheme, s) from the norm bound over all slices and blocks ----
     LCHK(cudaMemsetAsync(g.norm_dev, 0, sizeof(double), st));
     bound_kernel<<<std::max(1, std::min((N + 255) / 256, 148)), 256, 0, st>>>(
         u, K, N, nblk, g.gnorm_dev, reinterpret_cast<unsigned long long*>(g.norm_dev));
@@ -1273,9 +1322,9 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
     LCHK(cudaMemcpyAsync(&bound, g.norm_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
     LCHK(cudaStreamSynchronize(st));
     g.launches++;
-    int nb, sq;
-    choose_taylor_host(bound, nb, sq);
-    g.last_nb = nb;
+    int sq;
+    const PolyScheme& sc = *choose_scheme(bound, sq);
+    g.last_degree = sc.degree;
     g.last_s = sq;
     if (!g.gate && N > 0 && g.force_mode == 3) {  // matrix-free state schedule (opt-in)
       int rc = sv_alloc(g, false);
@@ -1297,7 +1346,7 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
         int rc = sv_alloc(g, true);
         if (rc != SQOC_OK) return rc;
         g.mode = 2;
-        rc = large_eval_state_vector(g, a, s, u, nb, sq, bound, st);
+        rc = large_eval_state_vector(g, a, s, u, sq, bound, st);
         if (rc != SQOC_OK) return rc;
         continue;
       }
@@ -1308,20 +1357,19 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
         size_t free_b = 0, total_b = 0;
         LCHK(cudaMemGetInfo(&free_b, &total_b));
         const size_t have = g.h_C ? history_bytes(g, g.h_C) : 0;
-        use_hist = history_bytes(g, 3 + nb + sq) <= (size_t)(0.6 * (double)(free_b + have));
+        use_hist = history_bytes(g, kSlots + sq) <= (size_t)(0.6 * (double)(free_b + have));
       }
       if (use_hist && N > 0) {
-        int rc = hist_alloc(g, nb, sq);
+        int rc = hist_alloc(g, sc.degree, sq);
         if (rc != SQOC_OK) return rc;
         g.mode = 1;
-        rc = large_eval_history(g, a, s, u, nb, sq, st);
+        rc = large_eval_history(g, a, s, u, sq, st);
         if (rc != SQOC_OK) return rc;
         continue;
       }
       g.mode = 0;
     }
     const double scale = std::ldexp(1.0, -sq);
-    const double cm = inv_fact(3 * nb);
     // ---- forward sweep ----
     {
       int rc0 = bc_init(g, g.X[0], g.L[0], ew_grid, st);
@@ -1334,20 +1382,9 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
       LCHK(cudaGetLastError());
       g.launches++;
       int rc;
-      if ((rc = gemm(g, F_A2, 0, 0, 0, one, st))) return rc;
-      if ((rc = gemm(g, F_A3, 0, 0, 0, one, st))) return rc;
-      const int t0 = nb - 1;
-      horner_init_kernel<<<ew_grid, 256, 0, st>>>(0, g.d_dev, g.off_dev, cm, inv_fact(3 * t0), inv_fact(3 * t0 + 1),
-                                                  inv_fact(3 * t0 + 2), g.A, g.A2, g.A3, g.Ad, g.dA2, g.dA3, g.T[0],
-                                                  g.dT[0], 0);
-      LCHK(cudaGetLastError());
-      g.launches++;
+      for (int k = 0; k < sc.nsteps; ++k)
+        if ((rc = gemm(g, F_STEP, k, sc.degree, 0, step_args(sc.step[k]), st))) return rc;
       int p = 0;
-      for (int t = nb - 2; t >= 0; --t) {
-        GemmArgs h{1.0, inv_fact(3 * t + 1), inv_fact(3 * t + 2), inv_fact(3 * t)};
-        if ((rc = gemm(g, F_H, p, 0, 0, h, st))) return rc;
-        p ^= 1;
-      }
       for (int i = 0; i < sq; ++i) {
         if ((rc = gemm(g, F_S, p, 0, 0, one, st))) return rc;
         p ^= 1;
@@ -1368,20 +1405,9 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
       g.launches++;
       int rc;
       if ((rc = gemm(g, B_C, 0, q, r, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
-      if ((rc = gemm(g, B_P2, 0, 0, 0, one, st))) return rc;
-      if ((rc = gemm(g, B_P3, 0, 0, 0, one, st))) return rc;
-      const int t0 = nb - 1;
-      horner_init_kernel<<<ew_grid, 256, 0, st>>>(1, g.d_dev, g.off_dev, cm, inv_fact(3 * t0), inv_fact(3 * t0 + 1),
-                                                  inv_fact(3 * t0 + 2), g.A, g.A2, g.A3, g.Ad, g.dA2, g.dA3, g.T[0],
-                                                  g.dT[0], 0);
-      LCHK(cudaGetLastError());
-      g.launches++;
+      for (int k = 0; k < sc.nsteps; ++k)
+        if ((rc = gemm(g, B_STEP, k, sc.degree, 0, step_args(sc.step[k]), st))) return rc;
       int p = 0;
-      for (int t = nb - 2; t >= 0; --t) {
-        GemmArgs h{1.0, inv_fact(3 * t + 1), inv_fact(3 * t + 2), inv_fact(3 * t)};
-        if ((rc = gemm(g, B_H, p, 0, 0, h, st))) return rc;
-        p ^= 1;
-      }
       for (int i = 0; i < sq; ++i) {
         if ((rc = gemm(g, B_S, p, 0, 0, one, st))) return rc;
         p ^= 1;

@@ -4,14 +4,14 @@
 // All large blocks of a problem are advanced together: every step below is ONE
 // launch whose work list holds one GEMM per block (zgemm.cuh), so the 16 D_14
 // blocks (495..1179) fill the 148 SMs together.  Per slice j (same algebra as
-// tiny.cuh, Taylor degree m = 3 nb and s squarings chosen once per evaluation
-// from the bound ||A_j|| <= ||a_0|| + sum_k |u_kj| ||a_k||):
+// tiny.cuh; the propagator scheme -- degree 12 in 4 products or degree 18 in 5 -- and
+// s squarings are chosen once per evaluation from the bound
+// ||A_j|| <= ||a_0|| + sum_k |u_kj| ||a_k||, large.cu "propagator schemes"):
 //
-//   forward : A, A2 = A A, A3 = A2 A, Horner T <- T A3 + Q_t, T <- T T (s x),
-//             X <- U X                                         (nb + 2 + s GEMMs)
-//   backward: Ad = 2^-s X Lam^dag, pairs (A2,dA2), (A3,dA3), Horner pairs,
-//             squaring pairs -> (U, N = L_R(A, X Lam^dag)); trace epilogue
-//             dtau_k = Tr(U^dag N E_k) (no D stored); X <- U^dag X, Lam <- U^dag Lam.
+//   forward : A, scheme steps (P products) -> Y, T <- T T (s x), X <- U X
+//   backward: Ad = 2^-s X Lam^dag, scheme steps as forward-mode pairs, squaring pairs
+//             -> (U, N = L_R(A, X Lam^dag)); trace epilogue dtau_k = Tr(U^dag N E_k)
+//             (no D stored); X <- U^dag X, Lam <- U^dag Lam.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -56,6 +56,7 @@ struct LargeGroup {
   std::vector<size_t> offr;   // block offsets into d x R arrays
   size_t total = 0, totalr = 0;
   double2 *A = nullptr, *Ad = nullptr, *A2 = nullptr, *dA2 = nullptr, *A3 = nullptr, *dA3 = nullptr;
+  double2 *xs[5] = {}, *dxs[5] = {};  // scheme slots 3..7 (A6, P, Q, W1, W2) and their derivatives
   double2 *T[2] = {nullptr, nullptr}, *dT[2] = {nullptr, nullptr};
   double2 *X[2] = {nullptr, nullptr}, *L[2] = {nullptr, nullptr};
   double2* trace_part = nullptr;  // [sum tiles][K]
@@ -79,11 +80,12 @@ struct LargeGroup {
   std::vector<void*> list_mem;
   int* tile_off_dev = nullptr;    // [nblk + 1] trace tile offsets
   // ---- history schedule: every slice resident, slice-batched GEMMs (chosen when memory allows) ----
-  int h_nb = -1, h_s = -1, h_C = 0;
-  double2* h_chain = nullptr;       // [C][N][total]: A, A2, A3, H_0..H_{nb-1}, S_1..S_s
+  int h_deg = -1, h_s = -1, h_C = 0;
+  double2* h_chain = nullptr;       // [C][N][total]: scheme slots 0..8 (A .. Y), S_1..S_s
   double2* h_X = nullptr;           // [N+1][totalr]
   double2* h_L = nullptr;           // [N+1][totalr]
-  double2 *h_dA = nullptr, *h_dA2 = nullptr, *h_dA3 = nullptr, *h_dH[2] = {nullptr, nullptr};  // [N][total]
+  double2* h_d[8] = {};             // [N][total] derivatives of scheme slots 0..7 (dA = seed)
+  double2* h_dH[2] = {nullptr, nullptr};  // [N][total] dY and the squaring derivatives
   double2* h_g = nullptr;           // [N][nblk][K] traces
   double2* h_I = nullptr;           // [totalr] identity per block (chunked scans)
   const double2** gent_dev = nullptr;  // per block a_k^T (K d*d), for the slice traces
@@ -92,7 +94,7 @@ struct LargeGroup {
   std::vector<void*> hlist_mem;
   // ---- state-vector schedule (state objective): U_j history, vector sweeps, augmented Taylor action ----
   double2* sv_U = nullptr;          // [N][total]
-  double2* sv_chunk = nullptr;      // [5][S][total]: A, A2, A3, T0, T1
+  double2* sv_chunk = nullptr;      // [10][S][total]: scheme slots 0..8, squaring partner
   int sv_S = 0;
   double2* sv_psi = nullptr;        // [N+1][totalr]
   double2* sv_chi = nullptr;        // [N+1][totalr]
@@ -103,7 +105,7 @@ struct LargeGroup {
   double2* mf_t = nullptr;          // matrix-free schedule: Taylor term vectors [3][totalr]
   const double2** gentall_dev = nullptr;  // per block a_k^T for k = 0..K
   std::vector<void*> gentall_mem;
-  int last_nb = 0, last_s = 0, last_taylor_terms = 0;
+  int last_degree = 0, last_s = 0, last_taylor_terms = 0;
   // boundary conditions for slice-chunk sharding (set by the engine for one sqoc_eval_chunk /
   // sqoc_chunk_product call, cleared afterwards)
   const double2** bc_x_dev = nullptr;     // device array of per-block X_start pointers, or null

@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "schemes.h"
+
 namespace sqoc {
 
 constexpr int kTinyMaxDim = 16;
@@ -79,11 +81,9 @@ struct TinyParams {
 // theta_12 = 0.3352 (sum_{k>12} t^k / k! <= 2^-53); each squaring doubles it, so the s4 scheme
 // with s squarings costs 4 + s products and beats every PS degree at every norm.
 // Layout: z0..z6 (z4..z6 = x4..x6), b0..b3, c0..c3.
-__constant__ double c_s4[15] = {
-    0.0, 2.1763083362520447e-12, 0.11462406647905307, 0.012167782611650191,
-    2.1931723165325633e-3, 2.7414653956657041e-4, 4.5691089927761735e-5,
-    5.5174437753427168, 1.3093238729655877, 4.3247187526118505e-3, 9.6586056829543493e-3,
-    1.0, 0.99999999998799234, -0.13243184210217061, -0.050548416421633109};
+__constant__ double c_s4[15] = {SQOC_S4_Z0, SQOC_S4_Z1, SQOC_S4_Z2, SQOC_S4_Z3, SQOC_S4_X4,
+                                SQOC_S4_X5, SQOC_S4_X6, SQOC_S4_B0, SQOC_S4_B1, SQOC_S4_B2,
+                                SQOC_S4_B3, SQOC_S4_C0, SQOC_S4_C1, SQOC_S4_C2, SQOC_S4_C3};
 constexpr double kTheta12 = 0.33;
 
 __device__ __forceinline__ int choose_squarings(double nrm) {

@@ -28,6 +28,9 @@ struct GemmItem {
   double2* C;
   const double2* E0;
   const double2* E1;
+  const double2* E2;
+  const double2* E3;
+  double2* C2;        // optional second output (same product, its own linear combination)
   const double2* F;   // trace epilogue: nF matrices, F + f * fstride
   double2* tr_out;    // trace epilogue: [tiles][nF] partials
   long fstride;
@@ -38,9 +41,37 @@ struct GemmItem {
   int nF;
 };
 
+// C  = alpha  acc + sum_t beta_t  E_t + gamma  [diag] I
+// C2 = alpha2 acc + sum_t beta2_t E_t + gamma2 [diag] I   (when it.C2)
 struct GemmArgs {
   double alpha, beta0, beta1, gamma;
+  double beta2, beta3;
+  double alpha2, beta2_0, beta2_1, beta2_2, beta2_3, gamma2;
 };
+
+__device__ __forceinline__ void epi_store(const GemmItem& it, const GemmArgs& a, int m, int n, double re, double im) {
+  const size_t off = (size_t)m * it.ldc + n;
+  const double2* E[4] = {it.E0, it.E1, it.E2, it.E3};
+  const double b1[4] = {a.beta0, a.beta1, a.beta2, a.beta3};
+  const double b2[4] = {a.beta2_0, a.beta2_1, a.beta2_2, a.beta2_3};
+  double2 c = make_double2(a.alpha * re, a.alpha * im);
+  double2 c2 = make_double2(a.alpha2 * re, a.alpha2 * im);
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+    if (E[t]) {
+      const double2 e = E[t][off];
+      c.x += b1[t] * e.x;
+      c.y += b1[t] * e.y;
+      c2.x += b2[t] * e.x;
+      c2.y += b2[t] * e.y;
+    }
+  if (it.diag && m == n) {
+    c.x += a.gamma;
+    c2.x += a.gamma2;
+  }
+  it.C[off] = c;
+  if (it.C2) it.C2[off] = c2;
+}
 
 constexpr int GBM = 64, GBN = 64, GBK = 8, GSTAGES = 4, GTHREADS = 128;
 constexpr int LD_KMAJ = GBK + 4;  // tiles stored [row][k]: ld = 12 (== 4 mod 8, conflict-free)
@@ -192,14 +223,7 @@ __global__ void __launch_bounds__(GTHREADS) zgemm_kernel(const GemmItem* __restr
         for (int v = 0; v < 2; ++v) {
           const int m = m0 + wm + mi * 8 + lr;
           const int n = n0 + wn + ni * 8 + 2 * lc + v;
-          if (m < it.m && n < it.n) {
-            double2 c = make_double2(args.alpha * acc[mi][ni][v], args.alpha * acc[mi][ni][2 + v]);
-            const size_t off = (size_t)m * it.ldc + n;
-            if (it.E0) { const double2 e = it.E0[off]; c.x += args.beta0 * e.x; c.y += args.beta0 * e.y; }
-            if (it.E1) { const double2 e = it.E1[off]; c.x += args.beta1 * e.x; c.y += args.beta1 * e.y; }
-            if (it.diag && m == n) c.x += args.gamma;
-            it.C[off] = c;
-          }
+          if (m < it.m && n < it.n) epi_store(it, args, m, n, acc[mi][ni][v], acc[mi][ni][2 + v]);
         }
   } else {
     // fused trace: partial_f = sum_{p,q in tile} alpha acc[p][q] F_f[q][p]
@@ -369,12 +393,7 @@ __global__ void __launch_bounds__(G3THREADS, 2) zgemm3m_kernel(const GemmItem* _
           const int n = n0 + wn + ni * 8 + 2 * lc + v;
           if (m < it.m && n < it.n) {
             const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
-            double2 c = make_double2(args.alpha * (t1 - t2), args.alpha * (t3 - t1 - t2));
-            const size_t off = (size_t)m * it.ldc + n;
-            if (it.E0) { const double2 e = it.E0[off]; c.x += args.beta0 * e.x; c.y += args.beta0 * e.y; }
-            if (it.E1) { const double2 e = it.E1[off]; c.x += args.beta1 * e.x; c.y += args.beta1 * e.y; }
-            if (it.diag && m == n) c.x += args.gamma;
-            it.C[off] = c;
+            epi_store(it, args, m, n, t1 - t2, t3 - t1 - t2);
           }
         }
   } else {

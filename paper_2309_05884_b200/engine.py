@@ -133,7 +133,7 @@ class GrapeEngine:
         nb, s, m = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         _lib.check(self.lib.sqoc_last_plan(self.handle, ctypes.byref(nb), ctypes.byref(s), ctypes.byref(m)),
                    "sqoc_last_plan")
-        return {"taylor_degree": 3 * nb.value, "squarings": s.value, "action_terms": m.value}
+        return {"taylor_degree": nb.value, "squarings": s.value, "action_terms": m.value}
 
     def set_timing(self, on: bool) -> None:
         _lib.check(self.lib.sqoc_set_timing(self.handle, 1 if on else 0), "sqoc_set_timing")

@@ -180,7 +180,7 @@ def s5_assemble(b6, s0, T, b0=None):
     s0, s1, s2, s3, s6 = R["s"]
     _, b1, b2, b3, b6 = R["b"]
     if b0 is None:
-        b0 = s0 / 2
+        b0 = mp.mpf(0)  # b0 = 0 keeps c0 = 1 (no cancellation in the identity term)
     b = {0: b0, 1: b1, 2: b2, 3: b3, 6: b6}
     e = {0: s0 - b0, 1: s1 - b1, 2: s2 - b2, 3: s3 - b3, 6: s6 - b6}
     z4, z5, z7, z8, z9 = (T[k] for k in ("z4", "z5", "z7", "z8", "z9"))
@@ -256,8 +256,9 @@ if __name__ == "__main__":
     print("//   b = b0..b3:", [fmt(x) for x in s4["b"]])
     print("//   c = c0..c3:", [fmt(x) for x in s4["c"]])
     sols = derive_s5()
-    print(f"// s5: {len(sols)} real solutions; theta_18 =", mp.nstr(theta_for({}, 18), 6))
-    for S in sols[:6]:
+    print(f"// s5: {len(sols)} real solutions (b0 = 0); theta_18 =", mp.nstr(theta_for({}, 18), 6),
+          "-- the kernels use the first (smallest proxy)")
+    for S in sols[:4]:
         print("// proxy", mp.nstr(S["proxy"], 6), "err", mp.nstr(S["err"], 3), "hi", mp.nstr(S["hi"], 3))
         print("//   B1 (I A A2 A3):", [fmt(x) for x in S["B1"]])
         print("//   B5 (A2 A3 A6):", [fmt(S["B5"][k]) for k in (2, 3, 6)])
