@@ -125,6 +125,14 @@ __device__ __forceinline__ double prob_sum(double v) {
 }
 template <int LP>
 __device__ __forceinline__ double2 prob_sum2(double2 v) { return make_double2(prob_sum<LP>(v.x), prob_sum<LP>(v.y)); }
+// Interleaved two-problem layout (see TinyCtx::IL): a problem's 16 lanes are lane bits {0,1,3,4}
+__device__ __forceinline__ double prob_sum_il(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 16);
+  return v;
+}
 // Sum over the LC lanes sharing a tile row (lanes base .. base+LC-1 with base a multiple of LC)
 template <int LC>
 __device__ __forceinline__ double row_sum(double v) {
@@ -418,6 +426,13 @@ struct TinyCtx {
   static constexpr int TSC = (D + LC - 1) / LC;
   static constexpr int DD = D * D;
   static constexpr int STRIDE = tiny_stride(D, MMA);
+  // Two problems per warp on 4 x 4 lane grids are interleaved inside every quarter-warp
+  // (lane = tc + 4 sub + 8 tr): LDS/STS.128 run in 8-lane phases, and with the bank-staggered
+  // buffers the 4 + 4 lanes of one phase hit 8 distinct 16-byte bank groups (r01: the
+  // contiguous layout put two rows of ONE problem in a phase -- row stride d = 1 mod 8 16-byte
+  // units -- and doubled the wavefronts of every own-entry load / store,
+  // profiles/r01_tiny9_ncu.txt).
+  static constexpr bool IL = !MMA && PPW == 2 && LC == 4;
   using T2 = double2[TSR][TSC];
 
   using TileT = typename TileSel<D, TSR, TSC, LR, LC, MMA>::type;
@@ -432,8 +447,13 @@ struct TinyCtx {
   __device__ __forceinline__ void init(const double2* gen_smem, double2* buf, int K_, int N_) {
     const int lane = threadIdx.x & 31;
     act = lane < PPW * LP;
-    sub = act ? lane / LP : 0;
-    q = act ? lane % LP : 0;
+    if (IL) {
+      sub = (lane >> 2) & 1;
+      q = (lane & 3) | ((lane >> 3) << 2);
+    } else {
+      sub = act ? lane / LP : 0;
+      q = act ? lane % LP : 0;
+    }
     tl = TileT{q / LC, q % LC};
     gen = gen_smem;
     K = K_;
@@ -634,7 +654,7 @@ struct TinyCtx {
 #pragma unroll
         for (int jj = 0; jj < TSC; ++jj)
           if (tl.ok(i, jj)) cfma(pk, t[i][jj], E[tl.rcol(jj) * D + tl.rrow(i)]);
-      dtau[k] = prob_sum2<LP>(pk);
+      dtau[k] = IL ? make_double2(prob_sum_il(pk.x), prob_sum_il(pk.y)) : prob_sum2<LP>(pk);
     }
   }
 
@@ -718,7 +738,7 @@ struct TinyCtx {
       for (int i = 0; i < TSR; ++i)
         if (tl.row_ok(i)) part = cadd(part, cmul(cconj(V[tl.rrow(i)]), X[tl.rrow(i)]));
     }
-    return prob_sum2<LP>(part);
+    return IL ? make_double2(prob_sum_il(part.x), prob_sum_il(part.y)) : prob_sum2<LP>(part);
   }
 };
 
