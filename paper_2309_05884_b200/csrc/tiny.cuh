@@ -333,11 +333,16 @@ struct MmaTile {
           t[mt][nt * 2 + v] = make_double2(t1 - t2, t3 - t1 - t2);
         }
   }
+  // k-tail: the last D % 4 (<= 2) k-steps run as DFMA rank-1 updates of the complex output
+  // fragments on the otherwise idle FP64 pipe instead of a mostly-zero DMMA k-step
+  // (d = 13: 3 DMMA k-steps instead of 4, i.e. 36 instead of 48 DMMAs per product).
+  static constexpr int KTAIL = (D % 4 <= 2) ? D % 4 : 0;
+  static constexpr int KMMA = D - KTAIL;  // k range of the DMMA main loop (zero-padded when KTAIL = 0)
   __device__ __forceinline__ void mul_op(double2 (&t)[TSR][TSC], const double2* L, const double2* M, bool adj) const {
     double acc[MT][MT][3][2];
     clear(acc);
 #pragma unroll 1
-    for (int k0 = 0; k0 < D; k0 += 4) {
+    for (int k0 = 0; k0 < KMMA; k0 += 4) {
       double2 a[MT], b[MT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) a[mt] = frag_a(L, mt, k0, adj);
@@ -346,6 +351,18 @@ struct MmaTile {
       acc3(acc, a, b);
     }
     finish(t, acc);
+#pragma unroll
+    for (int k = KMMA; k < D; ++k) {
+      double2 l[TSR], m[TSC];
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) l[i] = adj ? cconj(L[k * D + row(i)]) : L[row(i) * D + k];
+#pragma unroll
+      for (int j = 0; j < TSC; ++j) m[j] = M[k * D + col(j)];
+#pragma unroll
+      for (int i = 0; i < TSR; ++i)
+#pragma unroll
+        for (int j = 0; j < TSC; ++j) cfma(t[i][j], l[i], m[j]);
+    }
   }
   __device__ __forceinline__ void mul(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
     mul_op(t, L, M, false);
@@ -355,7 +372,7 @@ struct MmaTile {
     double acc[MT][MT][3][2];
     clear(acc);
 #pragma unroll 1
-    for (int k0 = 0; k0 < D; k0 += 4) {
+    for (int k0 = 0; k0 < KMMA; k0 += 4) {
       double2 a[MT], b[MT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) a[mt] = frag_a(L, mt, k0, false);
@@ -364,6 +381,18 @@ struct MmaTile {
       acc3(acc, a, b);
     }
     finish(t, acc);
+#pragma unroll
+    for (int k = KMMA; k < D; ++k) {
+      double2 l[TSR], m[TSC];
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) l[i] = L[row(i) * D + k];
+#pragma unroll
+      for (int j = 0; j < TSC; ++j) m[j] = cconj(M[col(j) * D + k]);
+#pragma unroll
+      for (int i = 0; i < TSR; ++i)
+#pragma unroll
+        for (int j = 0; j < TSC; ++j) cfma(t[i][j], l[i], m[j]);
+    }
   }
   __device__ __forceinline__ void mul_adj(double2 (&t)[TSR][TSC], const double2* U, const double2* M) const {
     mul_op(t, U, M, true);
@@ -375,7 +404,7 @@ struct MmaTile {
     clear(acc);
     clear(dacc);
 #pragma unroll 1
-    for (int k0 = 0; k0 < D; k0 += 4) {
+    for (int k0 = 0; k0 < KMMA; k0 += 4) {
       double2 a[MT], da[MT], b[MT], db[MT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
@@ -393,6 +422,25 @@ struct MmaTile {
     }
     finish(t, acc);
     finish(dt, dacc);
+#pragma unroll
+    for (int k = KMMA; k < D; ++k) {
+      double2 l[TSR], dl[TSR];
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) {
+        l[i] = L[row(i) * D + k];
+        dl[i] = dL[row(i) * D + k];
+      }
+#pragma unroll
+      for (int j = 0; j < TSC; ++j) {
+        const double2 m = M[k * D + col(j)], dm = dM[k * D + col(j)];
+#pragma unroll
+        for (int i = 0; i < TSR; ++i) {
+          cfma(t[i][j], l[i], m);
+          cfma(dt[i][j], dl[i], m);
+          cfma(dt[i][j], l[i], dm);
+        }
+      }
+    }
   }
 };
 
