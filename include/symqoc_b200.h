@@ -97,6 +97,14 @@ int sqoc_last_schedule(const sqoc_problem* p);
 int sqoc_set_tiny_schedule(sqoc_problem* p, int schedule);
 int sqoc_last_tiny_schedule(const sqoc_problem* p);
 
+/* Fused tiny schedule, X history: -1 auto (on when the per-slice states X_{j-1} of every
+ * (problem, slice) fit in 40% of free device memory -- 30 GB at cfg 1), 0 off (the backward
+ * sweep recomputes X_{j-1} = U_j^dag X_j), 1 on.  With the history the backward sweep seeds
+ * the Frechet chain with X_{j-1} Lam_j^dag and saves two GEMM-units per slice.
+ * sqoc_last_tiny_history reports whether the last fused evaluation used it (0/1, -1 none). */
+int sqoc_set_tiny_history(sqoc_problem* p, int mode);
+int sqoc_last_tiny_history(const sqoc_problem* p);
+
 /* Propagator plan of the last large-block evaluation: Taylor degree of the product scheme
  * (12: 4 products, 18: 5 products), `squarings` squarings, and the number of
  * augmented-action terms (state-vector). */

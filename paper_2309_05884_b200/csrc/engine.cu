@@ -45,6 +45,7 @@ struct BlockPlan {
   double2* target = nullptr;  // V or psi_f
   double2* park = nullptr;    // tiny: [slots][2][d*R]
   size_t park_slots = 0;
+  double2* xhist = nullptr;   // tiny fused: [slots][N][d*R] X history (allocated on first use)
   double2 *sp_U = nullptr, *sp_X = nullptr, *sp_L = nullptr;  // slice-parallel histories
   int sp_batch = 0;
   int nwarps = 1;       // fused kernel warps per CTA (capped by max_batch)
@@ -76,6 +77,9 @@ struct sqoc_problem {
   bool timing = false;
   int tiny_mode = -1;  // -1 auto, 0 fused, 1 slice-parallel
   int last_tiny_mode = -1;
+  int tiny_hist = -1;  // -1 auto, 0 off, 1 on (fused X history)
+  int last_tiny_hist = -1;
+  int hist_ok = -1;    // auto decision, made once: histories of all tiny blocks fit
   int launches = 0;
 };
 
@@ -169,6 +173,7 @@ static void free_problem(sqoc_problem* p) {
     cudaFree(b.x0);
     cudaFree(b.target);
     cudaFree(b.park);
+    cudaFree(b.xhist);
     cudaFree(b.sp_U);
     cudaFree(b.sp_X);
     cudaFree(b.sp_L);
@@ -384,6 +389,7 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
       // slice-parallel latency path for small batches (every (problem, slice) its own lane group)
       const bool sp_mode = p->N > 0 && (p->tiny_mode == 1 || (p->tiny_mode == -1 && batch <= kTinySliceParallelMaxBatch));
       p->last_tiny_mode = sp_mode ? 1 : 0;
+      if (sp_mode) p->last_tiny_hist = -1;
       int rc = SQOC_OK;
       if (sp_mode) {
         if (bp.sp_batch < batch) {
@@ -428,6 +434,18 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
         const int pg = 32 / tiny_lanes(bp.d, tiny_mma(bp.d));
         int nw = std::max(1, std::min(bp.nwarps, (batch + pg - 1) / pg));
         tp.nwarps = nw;
+        if (p->hist_ok < 0) {  // auto: all tiny blocks' histories in <= 40% of free memory
+          size_t need = 0, free_b = 0, total_b = 0;
+          for (auto& ob : p->blocks)
+            if (ob.tiny) need += ob.park_slots * p->N * ob.d * (gate ? ob.d : 1) * sizeof(double2);
+          SQOC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+          p->hist_ok = need <= (size_t)(0.4 * (double)free_b) ? 1 : 0;
+        }
+        const bool use_hist = p->N > 0 && (p->tiny_hist == 1 || (p->tiny_hist == -1 && p->hist_ok == 1));
+        if (use_hist && !bp.xhist)
+          SQOC_CUDA(cudaMalloc(&bp.xhist, bp.park_slots * p->N * bp.d * R * sizeof(double2)));
+        tp.xhist = use_hist ? bp.xhist : nullptr;
+        p->last_tiny_hist = use_hist ? 1 : 0;
         const int grid = (batch + pg * nw - 1) / (pg * nw);
         const size_t smem = tiny_smem_bytes(bp.d, p->K, nw, tiny_mma(bp.d));
         rc = gate ? launch_tiny<true>(bp.d, TK_FUSED, sp, grid, nw, smem, bp.stream)
@@ -624,6 +642,14 @@ int sqoc_set_tiny_schedule(sqoc_problem* p, int schedule) {
 }
 
 int sqoc_last_tiny_schedule(const sqoc_problem* p) { return p ? p->last_tiny_mode : -1; }
+
+int sqoc_set_tiny_history(sqoc_problem* p, int mode) {
+  if (!p || mode < -1 || mode > 1) return fail(SQOC_ERR_ARG, "tiny history mode must be -1, 0 or 1");
+  p->tiny_hist = mode;
+  return SQOC_OK;
+}
+
+int sqoc_last_tiny_history(const sqoc_problem* p) { return p ? p->last_tiny_hist : -1; }
 
 int sqoc_last_plan(const sqoc_problem* p, int* taylor_degree, int* squarings, int* action_terms) {
   if (!p || !taylor_degree || !squarings || !action_terms) return fail(SQOC_ERR_ARG, "NULL argument");

@@ -71,6 +71,7 @@ struct TinyParams {
   int tau_stride;
   double* grad_out;       // [batch][K][N] contribution of this block
   double2* park;          // [slots][2][d*R] workspace (X, Lam between phases)
+  double2* xhist;         // optional [slots][N][d*R]: X_{j-1} of every slice from the forward sweep
   int nwarps;             // warps per CTA
 };
 
@@ -690,10 +691,12 @@ struct TinyCtx {
     __syncwarp();
   }
 
-  // dtau_k = Tr(U^dag N E_k) with U in B6, N in B7 (sums over the problem's lanes)
-  __device__ __forceinline__ void traces(double2 (&dtau)[kMaxControls]) const {
+  // dtau_k = Tr(D E_k) over the problem's lanes, D = U^dag N with U in B6, N in B7 -- or, when
+  // the seed was X_{j-1} Lam_j^dag (X history), D = N itself
+  __device__ __forceinline__ void traces(double2 (&dtau)[kMaxControls], bool direct) const {
     T2 t;
-    tl.mul_adj(t, B6, B7);
+    if (direct) load_own(t, B7);
+    else tl.mul_adj(t, B6, B7);
     for (int k = 0; k < K; ++k) {
       const double2* E = gen + (k + 1) * DD;
       double2 pk = czero();
@@ -818,6 +821,11 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   double2* parkL = parkX + D * R;
 
   // ================= forward sweep: X_N =================
+  // With the X history (p.xhist) X_{j-1} of every slice is written out here and the backward
+  // sweep seeds L_R(A_j, X_{j-1} Lam_j^dag) directly: no U^dag N product for the traces and no
+  // X_{j-1} = U^dag X_j recurrence (21 -> 19 GEMM-units per slice at cfg 1).
+  const bool hist = p.xhist != nullptr;
+  double2* xh = hist ? p.xhist + (size_t)slot * N * D * R : nullptr;
   double2* X = c.B0;
   if (GATE) c.set_identity(X);
   else c.copy_x(X, p.x0);
@@ -827,6 +835,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
     int s;
     c.build_a(j, t, s);
     c.tl.store(c.B2, t, c.act);
+    if (hist) c.copy_x(xh + (size_t)j * D * R, X);  // X_{j-1}
     __syncwarp();
     c.expm_plain(s);
     c.mul_x(c.B6, false, X, X);  // X_j = U_j X_{j-1}
@@ -834,7 +843,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   }
   const double2 tau = c.overlap(p.target, X);
   if (c.real && c.q == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
-  c.copy_x(parkX, X);
+  if (!hist) c.copy_x(parkX, X);
   c.copy_x(parkL, p.target);
   __syncwarp();
 
@@ -842,22 +851,22 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   const double2 ctw = cscale(cconj(tau), 2.0 * p.weight);  // dF/du = Re(2 w conj(tau) dtau/du)
   for (int j = N - 1; j >= 0; --j) {
     int s;
-    c.copy_x(c.B0, parkX);  // stage X_j, Lam_j
+    c.copy_x(c.B0, hist ? xh + (size_t)j * D * R : parkX);  // stage X_{j-1} (history) or X_j, and Lam_j
     c.copy_x(c.B1, parkL);
     c.build_a(j, t, s);
     c.tl.store(c.B2, t, c.act);
     __syncwarp();
     c.seed_c(s);
     c.expm_pair(s);
-    c.copy_x(c.B0, parkX);  // restage X_j, Lam_j (B0/B1 were reused)
+    if (!hist) c.copy_x(c.B0, parkX);  // restage X_j, Lam_j (B0/B1 were reused)
     c.copy_x(c.B1, parkL);
     __syncwarp();
     double2 dtau[kMaxControls];
-    c.traces(dtau);
+    c.traces(dtau, hist);
     for (int k = 0; k < K; ++k)
       if (c.real && c.q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau[k].x - ctw.y * dtau[k].y;
-    c.mul_x(c.B6, true, c.B0, parkX);  // X_{j-1} = U^dag X_j, Lam_{j-1} = U^dag Lam_j -> park
-    c.mul_x(c.B6, true, c.B1, parkL);
+    if (!hist) c.mul_x(c.B6, true, c.B0, parkX);  // X_{j-1} = U^dag X_j
+    c.mul_x(c.B6, true, c.B1, parkL);               // Lam_{j-1} = U^dag Lam_j -> park
     __syncwarp();
   }
 }
@@ -972,7 +981,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_grad_kernel(TinySl
   c.seed_c(s);
   c.expm_pair(s);
   double2 dtau[kMaxControls];
-  c.traces(dtau);
+  c.traces(dtau, false);
   const double2 tau = p.tau_out[(size_t)prob * p.tau_stride];
   const double2 ctw = cscale(cconj(tau), 2.0 * p.weight);
   for (int k = 0; k < K; ++k)

@@ -128,6 +128,15 @@ class GrapeEngine:
     def last_tiny_schedule(self) -> str:
         return {-1: "none", 0: "fused", 1: "slice-parallel"}[self.lib.sqoc_last_tiny_schedule(self.handle)]
 
+    def set_tiny_history(self, mode: str) -> None:
+        """Fused tiny schedule X history: 'auto', 'off' (recompute X_{j-1}) or 'on'."""
+        _lib.check(self.lib.sqoc_set_tiny_history(self.handle, {"auto": -1, "off": 0, "on": 1}[mode]),
+                   "sqoc_set_tiny_history")
+
+    @property
+    def last_tiny_history(self) -> str:
+        return {-1: "none", 0: "off", 1: "on"}[self.lib.sqoc_last_tiny_history(self.handle)]
+
     @property
     def last_plan(self) -> dict:
         nb, s, m = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()

@@ -33,12 +33,15 @@ def random_system(d, objective, n_slices, seed):
 def test_random_dense_block(d, objective):
     s = random_system(d, objective, 9, seed=100 + d)
     u = np.random.default_rng(d).uniform(-1, 1, (3, 2, 9))
-    schedules = ["fused", "slice-parallel"] if d <= 16 else ["auto"]
+    schedules = ["fused", "fused-recompute", "slice-parallel"] if d <= 16 else ["auto"]
     for sched in schedules:
         eng = GrapeEngine(s, max_batch=3)
         if d <= 16:
-            eng.set_tiny_schedule(sched)
+            eng.set_tiny_schedule("fused" if sched.startswith("fused") else sched)
+            eng.set_tiny_history("off" if sched == "fused-recompute" else "on")
         F, g = eng.objective(u)
+        if d <= 16 and sched.startswith("fused"):
+            assert eng.last_tiny_history == ("off" if sched == "fused-recompute" else "on")
         for b in range(3):
             Fo, go, _ = O.objective(s, u[b])
             assert abs(F[b] - Fo) <= 1e-10, (d, objective, sched)
