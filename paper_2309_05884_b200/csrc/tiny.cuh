@@ -35,17 +35,17 @@ constexpr int kTinyMaxDim = 16;
 constexpr int kTinyBuffers = 8;   // d x d matrices per problem in shared memory
 constexpr int kMaxControls = 4;
 // Lane grid per problem: LR x LC lanes, each owning a TSR x TSC register tile (rows tr + LR i,
-// cols tc + LC j).  Measured per sector (r01, cfg1 at N_t=100, serialised): 3 x 3 grids (three
-// problems per warp) win for d = 5 (2.17 vs 3.0 ms) and tie for d = 3, but lose for d = 9 (9.5 vs
-// 9.2 ms: LC = 3 row loads conflict and 5 lanes idle) and d = 1; 4 x 4 (two per warp) elsewhere
-// up to d = 12; d >= 13 uses one warp per problem as 4 x 8 (all-16-lane layout: 352 ms per cfg1
-// batch vs 386 ms with 32 lanes everywhere).
+// cols tc + LC j).  3 x 3 grids (three problems per warp, table-mapped lanes, exact tiles) for
+// d = 3, 5, 6, 9; 4 x 4 (two per warp, interleaved lanes) for d = 1, 4, 10..12; d >= 13 without
+// DMMA uses one warp per problem as 4 x 8.  r01 (cfg1, N_t=100, serialised): d = 9 on 3 x 3
+// mapped lanes 6.6 ms vs 7.5 ms on 4 x 4 (12 x 12 coverage of a 9 x 9 matrix); the first 3 x 3
+// attempt without the conflict-free lane tables lost (9.5 vs 9.2 ms).
 // DMMA (tensor-core) tiles for d = 7, 8 (one 8x8 tile) and d >= 13 (2x2 tiles) in the fused
 // throughput kernel (r01: d=13 15.5 -> 13.9 ms, d=7 4.3 -> 2.3 ms per cfg1 launch at N_t=100);
 // the slice-parallel latency kernels keep DFMA tiles (shorter dependency chains per warp).
 __host__ __device__ constexpr bool tiny_mma(int d) { return d >= 13 || d == 7 || d == 8; }
 __host__ __device__ constexpr int tiny_lr(int d, bool mma) {
-  return mma ? 8 : d >= 13 ? 4 : d == 2 ? 2 : (d == 3 || d == 5 || d == 6) ? 3 : 4;
+  return mma ? 8 : d >= 13 ? 4 : d == 2 ? 2 : (d == 3 || d == 5 || d == 6 || d == 9) ? 3 : 4;
 }
 __host__ __device__ constexpr int tiny_lc(int d, bool mma) { return mma ? 4 : d >= 13 ? 8 : tiny_lr(d, false); }
 __host__ __device__ constexpr int tiny_lanes(int d, bool mma) { return tiny_lr(d, mma) * tiny_lc(d, mma); }
@@ -54,8 +54,26 @@ __host__ __device__ constexpr int tiny_lanes(int d, bool mma) { return tiny_lr(d
 // so without the pad every problem of a warp starts on bank 0 and the broadcast loads of
 // the LP-lane groups collide (2 wavefronts instead of 1 for two problems per warp).
 __host__ __device__ constexpr int tiny_pad(int d, bool mma) {
-  return (32 / tiny_lanes(d, mma)) == 2 ? 4 : (32 / tiny_lanes(d, mma)) == 3 ? 3 : (32 / tiny_lanes(d, mma)) == 8 ? 2 : 0;
+  return (32 / tiny_lanes(d, mma)) == 2   ? 4
+         : (32 / tiny_lanes(d, mma)) == 3 ? (d == 6 || d == 9 ? 3 : 1)  // sigma of tools/lane_maps.py
+         : (32 / tiny_lanes(d, mma)) == 8 ? 2
+                                          : 0;
 }
+// Three problems per warp (3 x 3 lane grid each, d = 3, 5, 6, 9): lane -> 9 sub + 3 tr + tc
+// (255 = idle), so that every 8-lane shared-memory phase is conflict-free for the own-entry,
+// operand, seed and generator accesses (searched by tools/lane_maps.py with the pads above).
+__host__ __device__ constexpr int tiny_map_id(int d) { return d == 3 ? 0 : d == 5 ? 1 : d == 6 ? 2 : 3; }
+__constant__ unsigned char c_lane_map[4][32] = {
+    {0, 9, 10, 15, 19, 255, 255, 255, 11, 12, 13, 14, 16, 17, 26, 255, 18, 20, 21, 22, 23, 24, 25, 255, 1, 2, 3, 4, 5, 6, 7, 8},
+    {0, 4, 18, 19, 21, 23, 24, 25, 2, 9, 11, 17, 20, 255, 255, 255, 1, 3, 5, 6, 7, 8, 22, 26, 10, 12, 13, 14, 15, 16, 255, 255},
+    {1, 3, 4, 5, 7, 10, 14, 255, 15, 17, 18, 20, 22, 24, 26, 255, 12, 13, 16, 19, 21, 23, 25, 255, 0, 2, 6, 8, 9, 11, 255, 255},
+    {9, 10, 11, 16, 19, 20, 25, 26, 4, 5, 12, 13, 14, 21, 22, 23, 0, 1, 2, 7, 17, 18, 255, 255, 3, 6, 8, 15, 24, 255, 255, 255}};
+// inverse: lane of entry 9 sub + q
+__constant__ unsigned char c_lane_inv[4][27] = {
+    {0, 24, 25, 26, 27, 28, 29, 30, 31, 1, 2, 8, 9, 10, 11, 3, 12, 13, 16, 4, 17, 18, 19, 20, 21, 22, 14},
+    {0, 16, 8, 17, 1, 18, 19, 20, 21, 9, 24, 10, 25, 26, 27, 28, 29, 11, 2, 3, 12, 4, 22, 5, 6, 7, 23},
+    {24, 0, 25, 1, 2, 3, 26, 4, 27, 28, 5, 29, 16, 17, 6, 8, 18, 9, 10, 19, 11, 20, 12, 21, 13, 22, 14},
+    {16, 17, 18, 24, 8, 9, 25, 19, 26, 0, 1, 2, 10, 11, 12, 27, 3, 20, 21, 4, 5, 13, 14, 15, 28, 6, 7}};
 __host__ __device__ constexpr int tiny_stride(int d, bool mma) { return kTinyBuffers * d * d + tiny_pad(d, mma); }
 constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
@@ -482,6 +500,8 @@ struct TinyCtx {
   // units -- and doubled the wavefronts of every own-entry load / store,
   // profiles/r01_tiny9_ncu.txt).
   static constexpr bool IL = !MMA && PPW == 2 && LC == 4;
+  static constexpr bool MAPPED = !MMA && PPW == 3;  // table layout (c_lane_map)
+  static constexpr int MAP = tiny_map_id(D);
   using T2 = double2[TSR][TSC];
 
   using TileT = typename TileSel<D, TSR, TSC, LR, LC, MMA>::type;
@@ -499,6 +519,11 @@ struct TinyCtx {
     if (IL) {
       sub = (lane >> 2) & 1;
       q = (lane & 3) | ((lane >> 3) << 2);
+    } else if (MAPPED) {
+      const int e = c_lane_map[MAP][lane];
+      act = e != 255;
+      sub = act ? e / 9 : 0;
+      q = act ? e % 9 : 0;
     } else {
       sub = act ? lane / LP : 0;
       q = act ? lane % LP : 0;
@@ -509,6 +534,26 @@ struct TinyCtx {
     N = N_;
     B0 = buf; B1 = B0 + DD; B2 = B1 + DD; B3 = B2 + DD; B4 = B3 + DD; B5 = B4 + DD; B6 = B5 + DD; B7 = B6 + DD;
   }
+
+  // sum over the problem's lanes / over the LC lanes of a tile row (fixed order, every lane gets it)
+  __device__ __forceinline__ double psum(double v) const {
+    if constexpr (IL) return prob_sum_il(v);
+    else if constexpr (MAPPED) {
+      double r = 0.0;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) r += __shfl_sync(0xffffffffu, v, c_lane_inv[MAP][sub * 9 + i]);
+      return r;
+    } else return prob_sum<LP>(v);
+  }
+  __device__ __forceinline__ double rsum(double v) const {
+    if constexpr (MAPPED) {
+      double r = 0.0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) r += __shfl_sync(0xffffffffu, v, c_lane_inv[MAP][sub * 9 + tl.tr * 3 + i]);
+      return r;
+    } else return row_sum<LC>(v);
+  }
+  __device__ __forceinline__ double2 psum2(double2 v) const { return make_double2(psum(v.x), psum(v.y)); }
 
   __device__ __forceinline__ void scale(T2& t, double c) const {
 #pragma unroll
@@ -541,7 +586,7 @@ struct TinyCtx {
     }
     double nrm = 0.0;
 #pragma unroll
-    for (int i = 0; i < TSR; ++i) nrm = fmax(nrm, row_sum<LC>(rowsum[i]));
+    for (int i = 0; i < TSR; ++i) nrm = fmax(nrm, rsum(rowsum[i]));
     nrm = warp_max(real ? nrm : 0.0);  // plan is warp-uniform, from real problems only
     s = choose_squarings(nrm);
     scale(a, ldexp(1.0, -s));
@@ -705,7 +750,7 @@ struct TinyCtx {
 #pragma unroll
         for (int jj = 0; jj < TSC; ++jj)
           if (tl.ok(i, jj)) cfma(pk, t[i][jj], E[tl.rcol(jj) * D + tl.rrow(i)]);
-      dtau[k] = IL ? make_double2(prob_sum_il(pk.x), prob_sum_il(pk.y)) : prob_sum2<LP>(pk);
+      dtau[k] = psum2(pk);
     }
   }
 
@@ -731,7 +776,7 @@ struct TinyCtx {
         }
       }
 #pragma unroll
-      for (int i = 0; i < TSR; ++i) v[i] = make_double2(row_sum<LC>(v[i].x), row_sum<LC>(v[i].y));
+      for (int i = 0; i < TSR; ++i) v[i] = make_double2(rsum(v[i].x), rsum(v[i].y));
       __syncwarp();
       if (act && tl.tc == 0) {
 #pragma unroll
@@ -789,7 +834,7 @@ struct TinyCtx {
       for (int i = 0; i < TSR; ++i)
         if (tl.row_ok(i)) part = cadd(part, cmul(cconj(V[tl.rrow(i)]), X[tl.rrow(i)]));
     }
-    return IL ? make_double2(prob_sum_il(part.x), prob_sum_il(part.y)) : prob_sum2<LP>(part);
+    return psum2(part);
   }
 };
 
