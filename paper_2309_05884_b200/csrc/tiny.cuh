@@ -282,8 +282,15 @@ template <int D, int MT = (D + 7) / 8>
 struct MmaTile {
   static constexpr int TSR = MT, TSC = 2 * MT;  // MT = number of 8-row DMMA tiles (1 or 2)
   int tr, tc;  // lane / 4, lane % 4
-  __device__ __forceinline__ int rrow(int i) const { return tr + 8 * i; }
-  __device__ __forceinline__ int rcol(int j) const { return 2 * tc + (j & 1) + 8 * (j >> 1); }
+  // Rows and columns inside each 8-wide DMMA tile are permuted (odd D): MMA index x <-> matrix
+  // index pm(x) = 0 4 1 5 2 6 3 7.  The lanes of one 8-lane shared-memory phase then touch rows /
+  // columns 4 apart, which with an odd row stride D land in disjoint halves of the 8 bank groups:
+  // fragment loads, own-entry stores and the transposed generator reads are all conflict-free
+  // (r01: identity order gave 2-way conflicts on every fragment load, 3.2e8 per d = 13 launch).
+  static constexpr bool PERM = (D & 1) != 0;
+  __device__ __forceinline__ static int pm(int x) { return PERM ? ((x & 1) ? 4 + (x >> 1) : (x >> 1)) : x; }
+  __device__ __forceinline__ int rrow(int i) const { return pm(tr) + 8 * i; }
+  __device__ __forceinline__ int rcol(int j) const { return pm(2 * tc + (j & 1)) + 8 * (j >> 1); }
   __device__ __forceinline__ int row(int i) const { return min(rrow(i), D - 1); }
   __device__ __forceinline__ int col(int j) const { return min(rcol(j), D - 1); }
   __device__ __forceinline__ bool ok(int i, int j) const { return rrow(i) < D && rcol(j) < D; }
@@ -305,19 +312,19 @@ struct MmaTile {
   }
   // A fragment (m = mt*8 + tr, k = k0 + tc) of op(L) (L or L^dag), zero outside D
   __device__ __forceinline__ double2 frag_a(const double2* L, int mt, int k0, bool adj) const {
-    const int m = mt * 8 + tr, k = k0 + tc;
+    const int m = mt * 8 + pm(tr), k = k0 + tc;
     if (m >= D || k >= D) return czero();
     return adj ? cconj(L[k * D + m]) : L[m * D + k];
   }
   // B fragment (k = k0 + tc, n = nt*8 + tr) of M, zero outside D
   __device__ __forceinline__ double2 frag_b(const double2* M, int nt, int k0) const {
-    const int k = k0 + tc, n = nt * 8 + tr;
+    const int k = k0 + tc, n = nt * 8 + pm(tr);
     if (k >= D || n >= D) return czero();
     return M[k * D + n];
   }
   // B fragment of M^dag: (k, n) -> conj(M[n][k])
   __device__ __forceinline__ double2 frag_b_adj(const double2* M, int nt, int k0) const {
-    const int k = k0 + tc, n = nt * 8 + tr;
+    const int k = k0 + tc, n = nt * 8 + pm(tr);
     if (k >= D || n >= D) return czero();
     return cconj(M[n * D + k]);
   }
