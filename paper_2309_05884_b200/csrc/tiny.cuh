@@ -32,7 +32,7 @@
 namespace sqoc {
 
 constexpr int kTinyMaxDim = 16;
-constexpr int kTinyBuffers = 8;   // d x d matrices per problem in shared memory
+constexpr int kTinyBuffers = 6;   // d x d matrices per problem in shared memory
 constexpr int kMaxControls = 4;
 // Lane grid per problem: LR x LC lanes, each owning a TSR x TSC register tile (rows tr + LR i,
 // cols tc + LC j).  3 x 3 grids (three problems per warp, table-mapped lanes, exact tiles) for
@@ -53,11 +53,15 @@ __host__ __device__ constexpr int tiny_lanes(int d, bool mma) { return tiny_lr(d
 // problems of one warp across the 32 banks.  8 d^2 double2 is always a multiple of 32 words,
 // so without the pad every problem of a warp starts on bank 0 and the broadcast loads of
 // the LP-lane groups collide (2 wavefronts instead of 1 for two problems per warp).
-__host__ __device__ constexpr int tiny_pad(int d, bool mma) {
+// desired stride residue (16-byte bank groups, mod 8) between consecutive problems of a warp
+__host__ __device__ constexpr int tiny_sigma(int d, bool mma) {
   return (32 / tiny_lanes(d, mma)) == 2   ? 4
          : (32 / tiny_lanes(d, mma)) == 3 ? (d == 6 || d == 9 ? 3 : 1)  // sigma of tools/lane_maps.py
          : (32 / tiny_lanes(d, mma)) == 8 ? 2
                                           : 0;
+}
+__host__ __device__ constexpr int tiny_pad(int d, bool mma) {
+  return ((tiny_sigma(d, mma) - kTinyBuffers * d * d) % 8 + 8) % 8;
 }
 // Three problems per warp (3 x 3 lane grid each, d = 3, 5, 6, 9): lane -> 9 sub + 3 tr + tc
 // (255 = idle), so that every 8-lane shared-memory phase is conflict-free for the own-entry,
@@ -75,7 +79,7 @@ __constant__ unsigned char c_lane_inv[4][27] = {
     {24, 0, 25, 1, 2, 3, 26, 4, 27, 28, 5, 29, 16, 17, 6, 8, 18, 9, 10, 19, 11, 20, 12, 21, 13, 22, 14},
     {16, 17, 18, 24, 8, 9, 25, 19, 26, 0, 1, 2, 10, 11, 12, 27, 3, 20, 21, 4, 5, 13, 14, 15, 28, 6, 7}};
 __host__ __device__ constexpr int tiny_stride(int d, bool mma) { return kTinyBuffers * d * d + tiny_pad(d, mma); }
-constexpr int kTinyMaxWarps = 10;  // warps (problems) per CTA
+constexpr int kTinyMaxWarps = 12;  // warps per CTA (12 x 32 threads x 168 registers fills the register file)
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
 
 struct TinyParams {
@@ -172,6 +176,22 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Left-operand views for the tile products: a plain shared-memory matrix, or a linear
+// combination c1 M1 + c2 M2 + c3 M3 formed on the fly in the operand loads (the scheme's
+// P = x4 A + x5 A2 + x6 A3 never needs a buffer of its own).
+struct OpP {
+  const double2* p;
+  __device__ __forceinline__ double2 at(int o) const { return p[o]; }
+};
+struct OpL3 {
+  const double2 *p1, *p2, *p3;
+  double c1, c2, c3;
+  __device__ __forceinline__ double2 at(int o) const {
+    const double2 a = p1[o], b = p2[o], c = p3[o];
+    return make_double2(fma(c1, a.x, fma(c2, b.x, c3 * c.x)), fma(c1, a.y, fma(c2, b.y, c3 * c.y)));
+  }
+};
+
 // Tile helpers.  Lane (tr, tc) owns rows tr + 4i and cols tc + 8j of a D x D matrix
 // (ld D).  The interleaved ownership makes the 8 lanes of a tile row read 8 consecutive
 // complex values of a matrix row in one LDS.128 wavefront (no bank conflict).
@@ -208,12 +228,16 @@ struct Tile {
   }
   // t = L M   (L, M: D x D in smem)
   __device__ __forceinline__ void mul(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
+    mulL(t, OpP{L}, M);
+  }
+  template <class OL>
+  __device__ __forceinline__ void mulL(double2 (&t)[TSR][TSC], const OL& L, const double2* M) const {
     zero(t);
 #pragma unroll 2
     for (int k = 0; k < D; ++k) {
       double2 l[TSR], m[TSC];
 #pragma unroll
-      for (int i = 0; i < TSR; ++i) l[i] = L[row(i) * D + k];
+      for (int i = 0; i < TSR; ++i) l[i] = L.at(row(i) * D + k);
 #pragma unroll
       for (int j = 0; j < TSC; ++j) m[j] = M[k * D + col(j)];
 #pragma unroll
@@ -241,6 +265,11 @@ struct Tile {
   // (t, dt) = (L, dL)(M, dM) = (L M, L dM + dL M)
   __device__ __forceinline__ void pair(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const double2* L,
                                        const double2* dL, const double2* M, const double2* dM) const {
+    pairL(t, dt, OpP{L}, OpP{dL}, M, dM);
+  }
+  template <class OL>
+  __device__ __forceinline__ void pairL(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const OL& L, const OL& dL,
+                                        const double2* M, const double2* dM) const {
     zero(t);
     zero(dt);
 #pragma unroll 1
@@ -248,8 +277,8 @@ struct Tile {
       double2 l[TSR], dl[TSR];
 #pragma unroll
       for (int i = 0; i < TSR; ++i) {
-        l[i] = L[row(i) * D + k];
-        dl[i] = dL[row(i) * D + k];
+        l[i] = L.at(row(i) * D + k);
+        dl[i] = dL.at(row(i) * D + k);
       }
 #pragma unroll
       for (int j = 0; j < TSC; ++j) {
@@ -315,6 +344,12 @@ struct MmaTile {
     const int m = mt * 8 + pm(tr), k = k0 + tc;
     if (m >= D || k >= D) return czero();
     return adj ? cconj(L[k * D + m]) : L[m * D + k];
+  }
+  template <class OL>
+  __device__ __forceinline__ double2 frag_a_op(const OL& L, int mt, int k0) const {
+    const int m = mt * 8 + pm(tr), k = k0 + tc;
+    if (m >= D || k >= D) return czero();
+    return L.at(m * D + k);
   }
   // B fragment (k = k0 + tc, n = nt*8 + tr) of M, zero outside D
   __device__ __forceinline__ double2 frag_b(const double2* M, int nt, int k0) const {
@@ -393,6 +428,33 @@ struct MmaTile {
   __device__ __forceinline__ void mul(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
     mul_op(t, L, M, false);
   }
+  template <class OL>
+  __device__ __forceinline__ void mulL(double2 (&t)[TSR][TSC], const OL& L, const double2* M) const {
+    double acc[MT][MT][3][2];
+    clear(acc);
+#pragma unroll 1
+    for (int k0 = 0; k0 < KMMA; k0 += 4) {
+      double2 a[MT], b[MT];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) a[mt] = frag_a_op(L, mt, k0);
+#pragma unroll
+      for (int nt = 0; nt < MT; ++nt) b[nt] = frag_b(M, nt, k0);
+      acc3(acc, a, b);
+    }
+    finish(t, acc);
+#pragma unroll
+    for (int k = KMMA; k < D; ++k) {
+      double2 l[TSR], m[TSC];
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) l[i] = L.at(row(i) * D + k);
+#pragma unroll
+      for (int j = 0; j < TSC; ++j) m[j] = M[k * D + col(j)];
+#pragma unroll
+      for (int i = 0; i < TSR; ++i)
+#pragma unroll
+        for (int j = 0; j < TSC; ++j) cfma(t[i][j], l[i], m[j]);
+    }
+  }
   // t = L M^dag
   __device__ __forceinline__ void mul_bt(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
     double acc[MT][MT][3][2];
@@ -426,6 +488,11 @@ struct MmaTile {
   // (t, dt) = (L M, L dM + dL M)
   __device__ __forceinline__ void pair(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const double2* L,
                                        const double2* dL, const double2* M, const double2* dM) const {
+    pairL(t, dt, OpP{L}, OpP{dL}, M, dM);
+  }
+  template <class OL>
+  __device__ __forceinline__ void pairL(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const OL& L, const OL& dL,
+                                        const double2* M, const double2* dM) const {
     double acc[MT][MT][3][2], dacc[MT][MT][3][2];
     clear(acc);
     clear(dacc);
@@ -434,8 +501,8 @@ struct MmaTile {
       double2 a[MT], da[MT], b[MT], db[MT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        a[mt] = frag_a(L, mt, k0, false);
-        da[mt] = frag_a(dL, mt, k0, false);
+        a[mt] = frag_a_op(L, mt, k0);
+        da[mt] = frag_a_op(dL, mt, k0);
       }
 #pragma unroll
       for (int nt = 0; nt < MT; ++nt) {
@@ -453,8 +520,8 @@ struct MmaTile {
       double2 l[TSR], dl[TSR];
 #pragma unroll
       for (int i = 0; i < TSR; ++i) {
-        l[i] = L[row(i) * D + k];
-        dl[i] = dL[row(i) * D + k];
+        l[i] = L.at(row(i) * D + k);
+        dl[i] = dL.at(row(i) * D + k);
       }
 #pragma unroll
       for (int j = 0; j < TSC; ++j) {
@@ -516,7 +583,7 @@ struct TinyCtx {
   int K, N, q, sub;
   bool act;  // lane belongs to a problem group (lanes past PPW * LP idle and never store)
   const double2* gen;  // (K+1) DD in smem
-  double2 *B0, *B1, *B2, *B3, *B4, *B5, *B6, *B7;
+  double2 *B0, *B1, *B2, *B3, *B4, *B5;
   const double* up;  // this problem's u [K][N]
   bool real;
 
@@ -539,7 +606,7 @@ struct TinyCtx {
     gen = gen_smem;
     K = K_;
     N = N_;
-    B0 = buf; B1 = B0 + DD; B2 = B1 + DD; B3 = B2 + DD; B4 = B3 + DD; B5 = B4 + DD; B6 = B5 + DD; B7 = B6 + DD;
+    B0 = buf; B1 = B0 + DD; B2 = B1 + DD; B3 = B2 + DD; B4 = B3 + DD; B5 = B4 + DD;
   }
 
   // sum over the problem's lanes / over the LC lanes of a tile row (fixed order, every lane gets it)
@@ -627,44 +694,44 @@ struct TinyCtx {
       for (int jj = 0; jj < TSC; ++jj) t[i][jj] = M[tl.row(i) * D + tl.col(jj)];
   }
 
-  // U = R(A) with A (scaled) in B2; uses B1 (A2), B4 (A3), B5 (Z); U -> B6
+  // Six d x d buffers per problem (was eight): the scheme's P = x4 A + x5 A2 + x6 A3 is formed
+  // in the operand loads (OpL3) and the final step's inputs overwrite the basis in place, so
+  // more problems fit per SM (r01: d = 13 10 -> 12 warps, d = 9 / 11 7 -> 9 warps per SM).
+
+  // U = R(A) with A (scaled) in B1; uses B2 (A2), B3 (A3), B4 (Z), B5 (W); U -> B2
   __device__ __forceinline__ void expm_plain(int s) const {
     T2 t, w;
-    tl.mul(t, B2, B2);  // A2
-    tl.store(B1, t, act);
+    tl.mul(t, B1, B1);  // A2
+    tl.store(B2, t, act);
     __syncwarp();
-    tl.mul(t, B1, B2);  // A3
-    tl.store(B4, t, act);  // own entries are read back below without a sync
-    scale(t, c_s4[6]);     // x4 A + x5 A2 + x6 A3
-    add_poly(t, 0.0, c_s4[4], B2, c_s4[5], B1, 0.0, nullptr);
-    tl.store(B6, t, act);
+    tl.mul(t, B2, B1);  // A3
+    tl.store(B3, t, act);
     __syncwarp();
-    tl.mul(t, B6, B4);  // Z = (x4 A + x5 A2 + x6 A3) A3 + z(A)
-    add_poly(t, c_s4[0], c_s4[1], B2, c_s4[2], B1, c_s4[3], B4);
+    tl.mulL(t, OpL3{B1, B2, B3, c_s4[4], c_s4[5], c_s4[6]}, B3);  // Z = (x4 A + x5 A2 + x6 A3) A3 + z(A)
+    add_poly(t, c_s4[0], c_s4[1], B1, c_s4[2], B2, c_s4[3], B3);
 #pragma unroll
     for (int i = 0; i < TSR; ++i)
 #pragma unroll
       for (int jj = 0; jj < TSC; ++jj) w[i][jj] = t[i][jj];
-    add_poly(w, c_s4[7], c_s4[8], B2, c_s4[9], B1, c_s4[10], B4);  // W = Z + b(A)
+    add_poly(w, c_s4[7], c_s4[8], B1, c_s4[9], B2, c_s4[10], B3);  // W = Z + b(A)
+    tl.store(B4, t, act);
+    tl.store(B5, w, act);
     __syncwarp();
-    tl.store(B5, t, act);
-    tl.store(B6, w, act);
+    tl.mul(t, B5, B4);  // y = W Z + c(A)
+    add_poly(t, c_s4[11], c_s4[12], B1, c_s4[13], B2, c_s4[14], B3);
     __syncwarp();
-    tl.mul(t, B6, B5);  // y = W Z + c(A)
-    add_poly(t, c_s4[11], c_s4[12], B2, c_s4[13], B1, c_s4[14], B4);
-    __syncwarp();
-    tl.store(B6, t, act);
+    tl.store(B2, t, act);
     for (int r = 0; r < s; ++r) {
       __syncwarp();
-      tl.mul(t, B6, B6);
+      tl.mul(t, B2, B2);
       __syncwarp();
-      tl.store(B6, t, act);
+      tl.store(B2, t, act);
     }
     __syncwarp();
   }
 
   // (U, N) = (R(A), L_R(A, Adot)) with A in B2, Adot in B3 (both scaled), forward-mode pairs
-  // through the same 4-product scheme; uses B0, B1, B4, B5; U -> B6, N -> B7
+  // through the same 4-product scheme; U -> B0, N -> B1 (all six buffers are used)
   __device__ __forceinline__ void expm_pair(int s) const {
     T2 t, dt;
     tl.pair(t, dt, B2, B3, B2, B3);  // (A2, dA2)
@@ -674,46 +741,55 @@ struct TinyCtx {
     tl.pair(t, dt, B0, B1, B2, B3);  // (A3, dA3)
     tl.store(B4, t, act);
     tl.store(B5, dt, act);
-    scale(t, c_s4[6]);
-    scale(dt, c_s4[6]);
-    add_poly(t, 0.0, c_s4[4], B2, c_s4[5], B0, 0.0, nullptr);
-    add_poly(dt, 0.0, c_s4[4], B3, c_s4[5], B1, 0.0, nullptr);
-    tl.store(B6, t, act);
-    tl.store(B7, dt, act);
     __syncwarp();
-    tl.pair(t, dt, B6, B7, B4, B5);  // (Z, dZ) before the z(A) terms
-    add_poly(t, c_s4[0], c_s4[1], B2, c_s4[2], B0, c_s4[3], B4);
-    add_poly(dt, 0.0, c_s4[1], B3, c_s4[2], B1, c_s4[3], B5);
+    tl.pairL(t, dt, OpL3{B2, B0, B4, c_s4[4], c_s4[5], c_s4[6]}, OpL3{B3, B1, B5, c_s4[4], c_s4[5], c_s4[6]}, B4,
+             B5);  // (P A3, P dA3 + dP A3)
     __syncwarp();
-    tl.store(B6, t, act);  // Z
-    tl.store(B7, dt, act);  // dZ
-    // own entries only from here to the next sync: W = Z + b(A) -> B4, C = c(A) -> B0,
-    // dW = dZ + b(dA) -> B5, dC = c(dA) -> B1 (each lane reads its entries before overwriting)
-    load_own(dt, B6);
-    add_poly(dt, c_s4[7], c_s4[8], B2, c_s4[9], B0, c_s4[10], B4);
-    tl.zero(t);
-    add_poly(t, c_s4[11], c_s4[12], B2, c_s4[13], B0, c_s4[14], B4);
-    tl.store(B4, dt, act);
+    // own entries only, in place: Z -> B0 (A2), W = Z + b(A) -> B2 (A), C = c(A) -> B4 (A3);
+    // dZ -> B1 (dA2), dW -> B3 (dA), dC -> B5 (dA3)
+#pragma unroll
+    for (int i = 0; i < TSR; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TSC; ++jj) {
+        const int o = tl.row(i) * D + tl.col(jj);
+        const bool dg = tl.rrow(i) == tl.rcol(jj);
+        const double2 a = B2[o], a2 = B0[o], a3 = B4[o], da = B3[o], da2 = B1[o], da3 = B5[o];
+        double2 z = t[i][jj], dz = dt[i][jj];
+        z.x += c_s4[1] * a.x + c_s4[2] * a2.x + c_s4[3] * a3.x + (dg ? c_s4[0] : 0.0);
+        z.y += c_s4[1] * a.y + c_s4[2] * a2.y + c_s4[3] * a3.y;
+        dz.x += c_s4[1] * da.x + c_s4[2] * da2.x + c_s4[3] * da3.x;
+        dz.y += c_s4[1] * da.y + c_s4[2] * da2.y + c_s4[3] * da3.y;
+        const double2 w = make_double2(z.x + c_s4[8] * a.x + c_s4[9] * a2.x + c_s4[10] * a3.x + (dg ? c_s4[7] : 0.0),
+                                       z.y + c_s4[8] * a.y + c_s4[9] * a2.y + c_s4[10] * a3.y);
+        const double2 cc = make_double2(c_s4[12] * a.x + c_s4[13] * a2.x + c_s4[14] * a3.x + (dg ? c_s4[11] : 0.0),
+                                        c_s4[12] * a.y + c_s4[13] * a2.y + c_s4[14] * a3.y);
+        const double2 dw = make_double2(dz.x + c_s4[8] * da.x + c_s4[9] * da2.x + c_s4[10] * da3.x,
+                                        dz.y + c_s4[8] * da.y + c_s4[9] * da2.y + c_s4[10] * da3.y);
+        const double2 dc = make_double2(c_s4[12] * da.x + c_s4[13] * da2.x + c_s4[14] * da3.x,
+                                        c_s4[12] * da.y + c_s4[13] * da2.y + c_s4[14] * da3.y);
+        if (act && tl.ok(i, jj)) {
+          const int q = tl.rrow(i) * D + tl.rcol(jj);
+          B0[q] = z;
+          B2[q] = w;
+          B4[q] = cc;
+          B1[q] = dz;
+          B3[q] = dw;
+          B5[q] = dc;
+        }
+      }
+    __syncwarp();
+    tl.pair(t, dt, B2, B3, B0, B1);  // (W Z, dW Z + W dZ)
+    add_poly(t, 0.0, 1.0, B4, 0.0, B4, 0.0, nullptr);  // + C
+    add_poly(dt, 0.0, 1.0, B5, 0.0, B5, 0.0, nullptr);  // + dC
+    __syncwarp();
     tl.store(B0, t, act);
-    load_own(dt, B7);
-    add_poly(dt, 0.0, c_s4[8], B3, c_s4[9], B1, c_s4[10], B5);
-    tl.zero(t);
-    add_poly(t, 0.0, c_s4[12], B3, c_s4[13], B1, c_s4[14], B5);
-    tl.store(B5, dt, act);
-    tl.store(B1, t, act);
-    __syncwarp();
-    tl.pair(t, dt, B4, B5, B6, B7);  // (W Z, dW Z + W dZ)
-    add_poly(t, 0.0, 1.0, B0, 0.0, B0, 0.0, nullptr);  // + C
-    add_poly(dt, 0.0, 1.0, B1, 0.0, B1, 0.0, nullptr);  // + dC
-    __syncwarp();
-    tl.store(B6, t, act);
-    tl.store(B7, dt, act);
+    tl.store(B1, dt, act);
     for (int r = 0; r < s; ++r) {
       __syncwarp();
-      tl.pair(t, dt, B6, B7, B6, B7);
+      tl.pair(t, dt, B0, B1, B0, B1);
       __syncwarp();
-      tl.store(B6, t, act);
-      tl.store(B7, dt, act);
+      tl.store(B0, t, act);
+      tl.store(B1, dt, act);
     }
     __syncwarp();
   }
@@ -743,12 +819,12 @@ struct TinyCtx {
     __syncwarp();
   }
 
-  // dtau_k = Tr(D E_k) over the problem's lanes, D = U^dag N with U in B6, N in B7 -- or, when
+  // dtau_k = Tr(D E_k) over the problem's lanes, D = U^dag N with U in B0, N in B1 -- or, when
   // the seed was X_{j-1} Lam_j^dag (X history), D = N itself
   __device__ __forceinline__ void traces(double2 (&dtau)[kMaxControls], bool direct) const {
     T2 t;
-    if (direct) load_own(t, B7);
-    else tl.mul_adj(t, B6, B7);
+    if (direct) load_own(t, B1);
+    else tl.mul_adj(t, B0, B1);
     for (int k = 0; k < K; ++k) {
       const double2* E = gen + (k + 1) * DD;
       double2 pk = czero();
@@ -886,11 +962,11 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   for (int j = 0; j < N; ++j) {
     int s;
     c.build_a(j, t, s);
-    c.tl.store(c.B2, t, c.act);
+    c.tl.store(c.B1, t, c.act);
     if (hist) c.copy_x(xh + (size_t)j * D * R, X);  // X_{j-1}
     __syncwarp();
     c.expm_plain(s);
-    c.mul_x(c.B6, false, X, X);  // X_j = U_j X_{j-1}
+    c.mul_x(c.B2, false, X, X);  // X_j = U_j X_{j-1}
     __syncwarp();
   }
   const double2 tau = c.overlap(p.target, X);
@@ -909,16 +985,16 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
     c.tl.store(c.B2, t, c.act);
     __syncwarp();
     c.seed_c(s);
-    c.expm_pair(s);
-    if (!hist) c.copy_x(c.B0, parkX);  // restage X_j, Lam_j (B0/B1 were reused)
-    c.copy_x(c.B1, parkL);
+    c.expm_pair(s);                     // U -> B0, N -> B1
+    if (!hist) c.copy_x(c.B2, parkX);  // restage X_j, Lam_j (the buffers were reused)
+    c.copy_x(c.B3, parkL);
     __syncwarp();
     double2 dtau[kMaxControls];
     c.traces(dtau, hist);
     for (int k = 0; k < K; ++k)
       if (c.real && c.q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau[k].x - ctw.y * dtau[k].y;
-    if (!hist) c.mul_x(c.B6, true, c.B0, parkX);  // X_{j-1} = U^dag X_j
-    c.mul_x(c.B6, true, c.B1, parkL);               // Lam_{j-1} = U^dag Lam_j -> park
+    if (!hist) c.mul_x(c.B0, true, c.B2, parkX);  // X_{j-1} = U^dag X_j
+    c.mul_x(c.B0, true, c.B3, parkL);               // Lam_{j-1} = U^dag Lam_j -> park
     __syncwarp();
   }
 }
@@ -954,10 +1030,10 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_expm_kernel(TinySl
   typename C::T2 t;
   int s;
   c.build_a(j, t, s);
-  c.tl.store(c.B2, t, c.act);
+  c.tl.store(c.B1, t, c.act);
   __syncwarp();
   c.expm_plain(s);
-  if (c.real) c.copy_dd(sp.Uh + (size_t)item * C::DD, c.B6);
+  if (c.real) c.copy_dd(sp.Uh + (size_t)item * C::DD, c.B2);
 }
 
 // phase 2: X / Lam recurrences (one lane group per problem), tau
@@ -985,9 +1061,9 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_sweep_kernel(TinyS
   __syncwarp();
   if (c.real) c.copy_x(Xh, X);
   for (int j = 0; j < N; ++j) {
-    c.copy_dd(c.B6, U + (size_t)j * C::DD);
+    c.copy_dd(c.B2, U + (size_t)j * C::DD);
     __syncwarp();
-    c.mul_x(c.B6, false, X, X);
+    c.mul_x(c.B2, false, X, X);
     __syncwarp();
     if (c.real) c.copy_x(Xh + (size_t)(j + 1) * D * R, X);
   }
@@ -997,9 +1073,9 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_sweep_kernel(TinyS
   __syncwarp();
   if (c.real) c.copy_x(Lh + (size_t)N * D * R, L);
   for (int j = N - 1; j >= 0; --j) {
-    c.copy_dd(c.B6, U + (size_t)j * C::DD);
+    c.copy_dd(c.B2, U + (size_t)j * C::DD);
     __syncwarp();
-    c.mul_x(c.B6, true, L, L);
+    c.mul_x(c.B2, true, L, L);
     __syncwarp();
     if (c.real) c.copy_x(Lh + (size_t)j * D * R, L);
   }
