@@ -304,8 +304,11 @@ __device__ __forceinline__ void g3_mainloop(double (&acc)[4][2][3][2], const Gem
     const int ksteps = (half_tail && kin == kt_per_seg - 1) ? 1 : 2;
     if (++kin == kt_per_seg) kin = 0;
     if constexpr (MC > 0 && NC > 0) {
-#pragma unroll 1
-    for (int ks = 0; ks < ksteps; ++ks) {
+    // both k-steps of a stage unrolled (loads of the second overlap the first's DMMAs); only the
+    // segment's last stage may skip its all-zero second half
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      if (ks >= ksteps) break;
       const int kk = ks * 4;
       double ar[MC], ai[MC], as[MC], br[NC], bi[NC], bs[NC];
 #pragma unroll
