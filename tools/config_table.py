@@ -22,7 +22,7 @@ CASES = {
     "1": dict(cfg=1, batch=4096, reps=3, warm=2),
     "2": dict(cfg=2, batch=1, reps=5, warm=2),
     "3": dict(cfg=3, batch=1, reps=1, warm=0),
-    "4": dict(cfg=4, batch=1, reps=1, warm=0),
+    "4": dict(cfg=4, batch=1, reps=1, warm=1),
     "4a1": dict(cfg=4, batch=1, reps=5, warm=2, full=False),
 }
 
