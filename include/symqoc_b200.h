@@ -97,11 +97,14 @@ int sqoc_last_schedule(const sqoc_problem* p);
 int sqoc_set_tiny_schedule(sqoc_problem* p, int schedule);
 int sqoc_last_tiny_schedule(const sqoc_problem* p);
 
-/* Fused tiny schedule, X history: -1 auto (on when the per-slice states X_{j-1} of every
- * (problem, slice) fit in 40% of free device memory -- 30 GB at cfg 1), 0 off (the backward
- * sweep recomputes X_{j-1} = U_j^dag X_j), 1 on.  With the history the backward sweep seeds
- * the Frechet chain with X_{j-1} Lam_j^dag and saves two GEMM-units per slice.
- * sqoc_last_tiny_history reports whether the last fused evaluation used it (0/1, -1 none). */
+/* Fused tiny schedule, histories kept in device memory between the forward and backward sweeps:
+ * 0 none (the backward sweep recomputes X_{j-1} = U_j^dag X_j and re-runs the full forward-mode
+ * pairs), 1 X history (X_{j-1} of every slice; the Frechet chain is seeded with
+ * X_{j-1} Lam_j^dag: two GEMM-units per slice fewer), 2 X + chain history (also the propagator
+ * chain A2, A3, Z, Y of every slice: only the derivative halves of the pairs run, four more units
+ * fewer).  -1 auto (default): X histories when they fit in 40% of free memory, chain histories
+ * for the largest blocks first while the total stays within 70%.
+ * sqoc_last_tiny_history reports the highest level the last fused evaluation used (-1 none). */
 int sqoc_set_tiny_history(sqoc_problem* p, int mode);
 int sqoc_last_tiny_history(const sqoc_problem* p);
 

@@ -46,6 +46,8 @@ struct BlockPlan {
   double2* park = nullptr;    // tiny: [slots][2][d*R]
   size_t park_slots = 0;
   double2* xhist = nullptr;   // tiny fused: [slots][N][d*R] X history (allocated on first use)
+  double2* chist = nullptr;   // tiny fused: [slots][N][4][d*d] propagator-chain history
+  int hist_level = -1;        // auto decision per block: 0 none, 1 X, 2 X + chain
   double2 *sp_U = nullptr, *sp_X = nullptr, *sp_L = nullptr;  // slice-parallel histories
   int sp_batch = 0;
   int nwarps = 1;       // fused kernel warps per CTA (capped by max_batch)
@@ -77,9 +79,9 @@ struct sqoc_problem {
   bool timing = false;
   int tiny_mode = -1;  // -1 auto, 0 fused, 1 slice-parallel
   int last_tiny_mode = -1;
-  int tiny_hist = -1;  // -1 auto, 0 off, 1 on (fused X history)
+  int tiny_hist = -1;  // -1 auto, 0 off, 1 X history, 2 X + chain history
   int last_tiny_hist = -1;
-  int hist_ok = -1;    // auto decision, made once: histories of all tiny blocks fit
+  bool hist_planned = false;  // auto levels decided (once, from free memory)
   int launches = 0;
 };
 
@@ -174,6 +176,7 @@ static void free_problem(sqoc_problem* p) {
     cudaFree(b.target);
     cudaFree(b.park);
     cudaFree(b.xhist);
+    cudaFree(b.chist);
     cudaFree(b.sp_U);
     cudaFree(b.sp_X);
     cudaFree(b.sp_L);
@@ -352,6 +355,7 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
   const bool dev = memory == SQOC_MEM_DEVICE;
   const double* u_dev = u;
   p->launches = 0;
+  p->last_tiny_hist = -1;
   if (!dev && KN) {
     SQOC_CUDA(cudaMemcpyAsync(p->u_dev, u, batch * KN * sizeof(double), cudaMemcpyHostToDevice, st));
     u_dev = p->u_dev;
@@ -434,18 +438,37 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
         const int pg = 32 / tiny_lanes(bp.d, tiny_mma(bp.d));
         int nw = std::max(1, std::min(bp.nwarps, (batch + pg - 1) / pg));
         tp.nwarps = nw;
-        if (p->hist_ok < 0) {  // auto: all tiny blocks' histories in <= 40% of free memory
-          size_t need = 0, free_b = 0, total_b = 0;
-          for (auto& ob : p->blocks)
-            if (ob.tiny) need += ob.park_slots * p->N * ob.d * (gate ? ob.d : 1) * sizeof(double2);
+        if (!p->hist_planned) {
+          // auto: X histories of all tiny blocks if they fit in 40% of free memory, then chain
+          // histories for the largest blocks first while the total stays within 70%
+          size_t free_b = 0, total_b = 0, used = 0;
           SQOC_CUDA(cudaMemGetInfo(&free_b, &total_b));
-          p->hist_ok = need <= (size_t)(0.4 * (double)free_b) ? 1 : 0;
+          for (auto& ob : p->blocks)
+            if (ob.tiny) used += ob.park_slots * p->N * ob.d * (gate ? ob.d : 1) * sizeof(double2);
+          const bool x_ok = used <= (size_t)(0.4 * (double)free_b);
+          std::vector<int> order;
+          for (int i = 0; i < p->nblocks; ++i)
+            if (p->blocks[i].tiny) order.push_back(i);
+          std::sort(order.begin(), order.end(), [&](int a, int b) { return p->blocks[a].d > p->blocks[b].d; });
+          for (int i : order) {
+            BlockPlan& ob = p->blocks[i];
+            ob.hist_level = x_ok ? 1 : 0;
+            const size_t cb = ob.park_slots * p->N * 4 * ob.d * ob.d * sizeof(double2);
+            if (x_ok && used + cb <= (size_t)(0.7 * (double)free_b)) {
+              ob.hist_level = 2;
+              used += cb;
+            }
+          }
+          p->hist_planned = true;
         }
-        const bool use_hist = p->N > 0 && (p->tiny_hist == 1 || (p->tiny_hist == -1 && p->hist_ok == 1));
-        if (use_hist && !bp.xhist)
+        const int level = p->N == 0 ? 0 : p->tiny_hist >= 0 ? p->tiny_hist : bp.hist_level;
+        if (level >= 1 && !bp.xhist)
           SQOC_CUDA(cudaMalloc(&bp.xhist, bp.park_slots * p->N * bp.d * R * sizeof(double2)));
-        tp.xhist = use_hist ? bp.xhist : nullptr;
-        p->last_tiny_hist = use_hist ? 1 : 0;
+        if (level >= 2 && !bp.chist)
+          SQOC_CUDA(cudaMalloc(&bp.chist, bp.park_slots * p->N * 4 * bp.d * bp.d * sizeof(double2)));
+        tp.xhist = level >= 1 ? bp.xhist : nullptr;
+        tp.chist = level >= 2 ? bp.chist : nullptr;
+        p->last_tiny_hist = std::max(p->last_tiny_hist, level);
         const int grid = (batch + pg * nw - 1) / (pg * nw);
         const size_t smem = tiny_smem_bytes(bp.d, p->K, nw, tiny_mma(bp.d));
         rc = gate ? launch_tiny<true>(bp.d, TK_FUSED, sp, grid, nw, smem, bp.stream)
@@ -644,7 +667,7 @@ int sqoc_set_tiny_schedule(sqoc_problem* p, int schedule) {
 int sqoc_last_tiny_schedule(const sqoc_problem* p) { return p ? p->last_tiny_mode : -1; }
 
 int sqoc_set_tiny_history(sqoc_problem* p, int mode) {
-  if (!p || mode < -1 || mode > 1) return fail(SQOC_ERR_ARG, "tiny history mode must be -1, 0 or 1");
+  if (!p || mode < -1 || mode > 2) return fail(SQOC_ERR_ARG, "tiny history mode must be -1, 0, 1 or 2");
   p->tiny_hist = mode;
   return SQOC_OK;
 }

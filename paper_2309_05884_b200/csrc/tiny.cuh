@@ -94,6 +94,7 @@ struct TinyParams {
   double* grad_out;       // [batch][K][N] contribution of this block
   double2* park;          // [slots][2][d*R] workspace (X, Lam between phases)
   double2* xhist;         // optional [slots][N][d*R]: X_{j-1} of every slice from the forward sweep
+  double2* chist;         // optional [slots][N][4][d*d]: A2, A3, Z, Y of every slice (needs xhist)
   int nwarps;             // warps per CTA
 };
 
@@ -270,7 +271,17 @@ struct Tile {
   template <class OL>
   __device__ __forceinline__ void pairL(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const OL& L, const OL& dL,
                                         const double2* M, const double2* dM) const {
-    zero(t);
+    pair_impl<true>(t, dt, L, dL, M, dM);
+  }
+  template <class OL>
+  __device__ __forceinline__ void dpairL(double2 (&dt)[TSR][TSC], const OL& L, const OL& dL, const double2* M,
+                                         const double2* dM) const {
+    pair_impl<false>(dt, dt, L, dL, M, dM);
+  }
+  template <bool WT, class OL>
+  __device__ __forceinline__ void pair_impl(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const OL& L,
+                                            const OL& dL, const double2* M, const double2* dM) const {
+    if (WT) zero(t);
     zero(dt);
 #pragma unroll 1
     for (int k = 0; k < D; ++k) {
@@ -286,7 +297,7 @@ struct Tile {
         const double2 dm = dM[k * D + col(j)];
 #pragma unroll
         for (int i = 0; i < TSR; ++i) {
-          cfma(t[i][j], l[i], m);
+          if (WT) cfma(t[i][j], l[i], m);
           cfma(dt[i][j], dl[i], m);
           cfma(dt[i][j], l[i], dm);
         }
@@ -493,8 +504,19 @@ struct MmaTile {
   template <class OL>
   __device__ __forceinline__ void pairL(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const OL& L, const OL& dL,
                                         const double2* M, const double2* dM) const {
+    pair_impl<true>(t, dt, L, dL, M, dM);
+  }
+  // derivative only: dt = L dM + dL M (the value L M is known from the chain history)
+  template <class OL>
+  __device__ __forceinline__ void dpairL(double2 (&dt)[TSR][TSC], const OL& L, const OL& dL, const double2* M,
+                                         const double2* dM) const {
+    pair_impl<false>(dt, dt, L, dL, M, dM);
+  }
+  template <bool WT, class OL>
+  __device__ __forceinline__ void pair_impl(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const OL& L,
+                                            const OL& dL, const double2* M, const double2* dM) const {
     double acc[MT][MT][3][2], dacc[MT][MT][3][2];
-    clear(acc);
+    if (WT) clear(acc);
     clear(dacc);
 #pragma unroll 1
     for (int k0 = 0; k0 < KMMA; k0 += 4) {
@@ -509,11 +531,11 @@ struct MmaTile {
         b[nt] = frag_b(M, nt, k0);
         db[nt] = frag_b(dM, nt, k0);
       }
-      acc3(acc, a, b);
+      if (WT) acc3(acc, a, b);
       acc3(dacc, a, db);
       acc3(dacc, da, b);
     }
-    finish(t, acc);
+    if (WT) finish(t, acc);
     finish(dt, dacc);
 #pragma unroll
     for (int k = KMMA; k < D; ++k) {
@@ -528,7 +550,7 @@ struct MmaTile {
         const double2 m = M[k * D + col(j)], dm = dM[k * D + col(j)];
 #pragma unroll
         for (int i = 0; i < TSR; ++i) {
-          cfma(t[i][j], l[i], m);
+          if (WT) cfma(t[i][j], l[i], m);
           cfma(dt[i][j], dl[i], m);
           cfma(dt[i][j], l[i], dm);
         }
@@ -698,14 +720,17 @@ struct TinyCtx {
   // in the operand loads (OpL3) and the final step's inputs overwrite the basis in place, so
   // more problems fit per SM (r01: d = 13 10 -> 12 warps, d = 9 / 11 7 -> 9 warps per SM).
 
-  // U = R(A) with A (scaled) in B1; uses B2 (A2), B3 (A3), B4 (Z), B5 (W); U -> B2
-  __device__ __forceinline__ void expm_plain(int s) const {
+  // U = R(A) with A (scaled) in B1; uses B2 (A2), B3 (A3), B4 (Z), B5 (W); U -> B2.  With a chain
+  // history slot ch (4 d x d matrices in global memory) the unsquared chain A2, A3, Z, Y is kept.
+  __device__ __forceinline__ void expm_plain(int s, double2* ch = nullptr) const {
     T2 t, w;
     tl.mul(t, B1, B1);  // A2
     tl.store(B2, t, act);
+    if (ch) tl.store(ch, t, act);
     __syncwarp();
     tl.mul(t, B2, B1);  // A3
     tl.store(B3, t, act);
+    if (ch) tl.store(ch + DD, t, act);
     __syncwarp();
     tl.mulL(t, OpL3{B1, B2, B3, c_s4[4], c_s4[5], c_s4[6]}, B3);  // Z = (x4 A + x5 A2 + x6 A3) A3 + z(A)
     add_poly(t, c_s4[0], c_s4[1], B1, c_s4[2], B2, c_s4[3], B3);
@@ -716,9 +741,11 @@ struct TinyCtx {
     add_poly(w, c_s4[7], c_s4[8], B1, c_s4[9], B2, c_s4[10], B3);  // W = Z + b(A)
     tl.store(B4, t, act);
     tl.store(B5, w, act);
+    if (ch) tl.store(ch + 2 * DD, t, act);
     __syncwarp();
     tl.mul(t, B5, B4);  // y = W Z + c(A)
     add_poly(t, c_s4[11], c_s4[12], B1, c_s4[13], B2, c_s4[14], B3);
+    if (ch) tl.store(ch + 3 * DD, t, act);
     __syncwarp();
     tl.store(B2, t, act);
     for (int r = 0; r < s; ++r) {
@@ -726,6 +753,69 @@ struct TinyCtx {
       tl.mul(t, B2, B2);
       __syncwarp();
       tl.store(B2, t, act);
+    }
+    __syncwarp();
+  }
+
+  // Backward propagator step from the chain history ch = (A2, A3, Z, Y) of this slice: with A in
+  // B2 and Adot in B3 only the derivative halves of the pairs run (8 instead of 12 GEMM-units at
+  // s = 0); U -> B0, N -> B1 as expm_pair.
+  __device__ __forceinline__ void expm_dchain(int s, const double2* ch) const {
+    T2 dt;
+    copy_dd(B0, ch);       // A2
+    copy_dd(B4, ch + DD);  // A3
+    __syncwarp();
+    tl.dpairL(dt, OpP{B2}, OpP{B3}, B2, B3);  // dA2 = A dA + dA A
+    tl.store(B1, dt, act);
+    __syncwarp();
+    tl.dpairL(dt, OpP{B0}, OpP{B1}, B2, B3);  // dA3 = A2 dA + dA2 A
+    tl.store(B5, dt, act);
+    __syncwarp();
+    tl.dpairL(dt, OpL3{B2, B0, B4, c_s4[4], c_s4[5], c_s4[6]}, OpL3{B3, B1, B5, c_s4[4], c_s4[5], c_s4[6]}, B4,
+              B5);  // P dA3 + dP A3
+    __syncwarp();
+    // own entries, in place: Z (history) -> B0, W = Z + b(A) -> B2, dZ -> B1, dW -> B3, dC -> B5
+#pragma unroll
+    for (int i = 0; i < TSR; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TSC; ++jj) {
+        const int o = tl.row(i) * D + tl.col(jj);
+        const bool dg = tl.rrow(i) == tl.rcol(jj);
+        const double2 a = B2[o], a2 = B0[o], a3 = B4[o], da = B3[o], da2 = B1[o], da3 = B5[o];
+        const double2 z = ch[2 * DD + o];
+        double2 dz = dt[i][jj];
+        dz.x += c_s4[1] * da.x + c_s4[2] * da2.x + c_s4[3] * da3.x;
+        dz.y += c_s4[1] * da.y + c_s4[2] * da2.y + c_s4[3] * da3.y;
+        const double2 w = make_double2(z.x + c_s4[8] * a.x + c_s4[9] * a2.x + c_s4[10] * a3.x + (dg ? c_s4[7] : 0.0),
+                                       z.y + c_s4[8] * a.y + c_s4[9] * a2.y + c_s4[10] * a3.y);
+        const double2 dw = make_double2(dz.x + c_s4[8] * da.x + c_s4[9] * da2.x + c_s4[10] * da3.x,
+                                        dz.y + c_s4[8] * da.y + c_s4[9] * da2.y + c_s4[10] * da3.y);
+        const double2 dc = make_double2(c_s4[12] * da.x + c_s4[13] * da2.x + c_s4[14] * da3.x,
+                                        c_s4[12] * da.y + c_s4[13] * da2.y + c_s4[14] * da3.y);
+        if (act && tl.ok(i, jj)) {
+          const int q = tl.rrow(i) * D + tl.rcol(jj);
+          B0[q] = z;
+          B2[q] = w;
+          B1[q] = dz;
+          B3[q] = dw;
+          B5[q] = dc;
+        }
+      }
+    __syncwarp();
+    tl.dpairL(dt, OpP{B2}, OpP{B3}, B0, B1);  // dY = W dZ + dW Z (+ dC)
+    add_poly(dt, 0.0, 1.0, B5, 0.0, B5, 0.0, nullptr);
+    __syncwarp();
+    copy_dd(B0, ch + 3 * DD);  // Y
+    tl.store(B1, dt, act);
+    if (s > 0) {
+      T2 t;
+      for (int r = 0; r < s; ++r) {
+        __syncwarp();
+        tl.pair(t, dt, B0, B1, B0, B1);
+        __syncwarp();
+        tl.store(B0, t, act);
+        tl.store(B1, dt, act);
+      }
     }
     __syncwarp();
   }
@@ -954,6 +1044,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   // X_{j-1} = U^dag X_j recurrence (21 -> 19 GEMM-units per slice at cfg 1).
   const bool hist = p.xhist != nullptr;
   double2* xh = hist ? p.xhist + (size_t)slot * N * D * R : nullptr;
+  double2* chh = (hist && p.chist) ? p.chist + (size_t)slot * N * 4 * C::DD : nullptr;
   double2* X = c.B0;
   if (GATE) c.set_identity(X);
   else c.copy_x(X, p.x0);
@@ -965,7 +1056,7 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
     c.tl.store(c.B1, t, c.act);
     if (hist) c.copy_x(xh + (size_t)j * D * R, X);  // X_{j-1}
     __syncwarp();
-    c.expm_plain(s);
+    c.expm_plain(s, chh ? chh + (size_t)j * 4 * C::DD : nullptr);
     c.mul_x(c.B2, false, X, X);  // X_j = U_j X_{j-1}
     __syncwarp();
   }
@@ -985,7 +1076,8 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
     c.tl.store(c.B2, t, c.act);
     __syncwarp();
     c.seed_c(s);
-    c.expm_pair(s);                     // U -> B0, N -> B1
+    if (chh) c.expm_dchain(s, chh + (size_t)j * 4 * C::DD);  // U -> B0, N -> B1
+    else c.expm_pair(s);
     if (!hist) c.copy_x(c.B2, parkX);  // restage X_j, Lam_j (the buffers were reused)
     c.copy_x(c.B3, parkL);
     __syncwarp();

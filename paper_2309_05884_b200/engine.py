@@ -128,14 +128,16 @@ class GrapeEngine:
     def last_tiny_schedule(self) -> str:
         return {-1: "none", 0: "fused", 1: "slice-parallel"}[self.lib.sqoc_last_tiny_schedule(self.handle)]
 
+    TINY_HISTORY = {"auto": -1, "off": 0, "x": 1, "on": 1, "chain": 2}
+
     def set_tiny_history(self, mode: str) -> None:
-        """Fused tiny schedule X history: 'auto', 'off' (recompute X_{j-1}) or 'on'."""
-        _lib.check(self.lib.sqoc_set_tiny_history(self.handle, {"auto": -1, "off": 0, "on": 1}[mode]),
-                   "sqoc_set_tiny_history")
+        """Fused tiny schedule histories: 'auto', 'off' (recompute), 'x' (X_{j-1} per slice) or
+        'chain' (X and the propagator chain per slice)."""
+        _lib.check(self.lib.sqoc_set_tiny_history(self.handle, self.TINY_HISTORY[mode]), "sqoc_set_tiny_history")
 
     @property
     def last_tiny_history(self) -> str:
-        return {-1: "none", 0: "off", 1: "on"}[self.lib.sqoc_last_tiny_history(self.handle)]
+        return {-1: "none", 0: "off", 1: "x", 2: "chain"}[self.lib.sqoc_last_tiny_history(self.handle)]
 
     @property
     def last_plan(self) -> dict:

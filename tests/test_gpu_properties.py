@@ -12,10 +12,11 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(scope="module")
 def cfg1():
     s = systems.config(1)  # n=12 all-to-all, 7 sectors, N=1000
-    eng = GrapeEngine(s, max_batch=4096)
+    eng = GrapeEngine(s, max_batch=4096)  # auto histories: up to ~70% of free device memory
     u = s.controls(31, batch=4096)
     F, g, tau = eng.evaluate(u, want_tau=True)
-    return s, eng, u, F, g, tau
+    yield s, eng, u, F, g, tau
+    eng.close()  # release the histories before the full-size large-block tests
 
 
 def test_cfg1_fidelity_bounds_and_tau(cfg1):
@@ -58,6 +59,11 @@ def test_cfg1_target_phase_invariance():
     F2, g2 = GrapeEngine(s, max_batch=16).objective(u)
     np.testing.assert_allclose(F2, F, atol=1e-14)
     np.testing.assert_allclose(g2, g, atol=1e-12 * np.abs(g).max())
+
+
+def test_cfg1_release(cfg1):
+    """Free the module's cfg 1 engine (tens of GB of histories) before the full-size cfg 2/4 tests."""
+    cfg1[1].close()
 
 
 def test_cfg2_full_size_schedules_agree_and_gauge():

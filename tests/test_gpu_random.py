@@ -33,15 +33,17 @@ def random_system(d, objective, n_slices, seed):
 def test_random_dense_block(d, objective):
     s = random_system(d, objective, 9, seed=100 + d)
     u = np.random.default_rng(d).uniform(-1, 1, (3, 2, 9))
-    schedules = ["fused", "fused-recompute", "slice-parallel"] if d <= 16 else ["auto"]
+    hist = {"fused-recompute": "off", "fused-x": "x", "fused-chain": "chain"}
+    schedules = list(hist) + ["slice-parallel"] if d <= 16 else ["auto"]
     for sched in schedules:
         eng = GrapeEngine(s, max_batch=3)
         if d <= 16:
             eng.set_tiny_schedule("fused" if sched.startswith("fused") else sched)
-            eng.set_tiny_history("off" if sched == "fused-recompute" else "on")
+            if sched in hist:
+                eng.set_tiny_history(hist[sched])
         F, g = eng.objective(u)
-        if d <= 16 and sched.startswith("fused"):
-            assert eng.last_tiny_history == ("off" if sched == "fused-recompute" else "on")
+        if sched in hist:
+            assert eng.last_tiny_history == hist[sched]
         for b in range(3):
             Fo, go, _ = O.objective(s, u[b])
             assert abs(F[b] - Fo) <= 1e-10, (d, objective, sched)
