@@ -191,7 +191,6 @@ def run_ours(args):
     from paper_2309_05884_b200 import systems
 
     batch = args.batch or systems.CONFIG_BATCH[cfg]
-    eng = GrapeEngine(s, max_batch=batch, device=local)
     seed0 = 1000 * rank
     u_host = s.controls(seed0, batch=batch)
     u = torch.from_numpy(u_host).to(f"cuda:{local}")
@@ -199,6 +198,42 @@ def run_ours(args):
     g = torch.empty_like(u)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=u.device)  # > 126 MB L2
     stream = torch.cuda.current_stream()
+
+    # ---- dominant tiny kernel timed alone: in the step the sectors' kernels share the GPU on
+    # concurrent streams, so a per-stream event pair around one of them measures contention,
+    # not the kernel.  The same launch (largest sector, same u) runs here on an idle GPU, before
+    # the full engine exists, so its memory plan (chain history) matches the one the step uses. ----
+    dom_alone_ms = None
+    from paper_2309_05884_b200 import _lib
+
+    if all(b.dim <= _lib.load().sqoc_tiny_max_dim() for b in s.blocks):
+        import copy as _copy
+
+        dims_ = [b.dim for b in s.blocks]
+        bdom_ = int(np.argmax(np.array(dims_, dtype=float) ** 3))
+        sub = _copy.copy(s)
+        sub.blocks = [s.blocks[bdom_]]
+        sub.targets = [s.targets[bdom_]]
+        sub.initial = [s.initial[bdom_]] if s.initial else []
+        sub.weights = np.array([s.block_weights()[bdom_]])
+        eng1 = GrapeEngine(sub, max_batch=batch, device=local)
+        eng1.evaluate_device(u.data_ptr(), batch, F.data_ptr(), g.data_ptr(), stream=stream.cuda_stream)
+        alone = []
+        for _ in range(max(2, args.steps)):
+            flush.fill_(1.0)
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            eng1.evaluate_device(u.data_ptr(), batch, F.data_ptr(), g.data_ptr(), stream=stream.cuda_stream)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            alone.append(a0.elapsed_time(a1))
+        dom_alone_ms = float(np.mean(alone))
+        eng1.close()
+        del eng1
+
+    torch.cuda.empty_cache()
+    eng = GrapeEngine(s, max_batch=batch, device=local)
 
     def step():
         eng.evaluate_device(u.data_ptr(), batch, F.data_ptr(), g.data_ptr(), stream=stream.cuda_stream)
@@ -235,35 +270,6 @@ def run_ours(args):
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-
-    # ---- dominant tiny kernel timed alone: in the step the sectors' kernels share the GPU on
-    # concurrent streams, so a per-stream event pair around one of them measures contention,
-    # not the kernel.  The same launch (largest sector, same u) runs here on an idle GPU. ----
-    dom_alone_ms = None
-    if len(eng.large_blocks) == 0:
-        import copy as _copy
-
-        dims_ = [b.dim for b in s.blocks]
-        bdom_ = int(np.argmax(np.array(dims_, dtype=float) ** 3))
-        sub = _copy.copy(s)
-        sub.blocks = [s.blocks[bdom_]]
-        sub.targets = [s.targets[bdom_]]
-        sub.initial = [s.initial[bdom_]] if s.initial else []
-        sub.weights = np.array([s.block_weights()[bdom_]])
-        eng1 = GrapeEngine(sub, max_batch=batch, device=local)
-        eng1.evaluate_device(u.data_ptr(), batch, F.data_ptr(), g.data_ptr(), stream=stream.cuda_stream)
-        alone = []
-        for _ in range(max(2, args.steps)):
-            flush.fill_(1.0)
-            a0 = torch.cuda.Event(enable_timing=True)
-            a1 = torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            eng1.evaluate_device(u.data_ptr(), batch, F.data_ptr(), g.data_ptr(), stream=stream.cuda_stream)
-            a1.record(stream)
-            torch.cuda.synchronize()
-            alone.append(a0.elapsed_time(a1))
-        dom_alone_ms = float(np.mean(alone))
-        del eng1
 
     # ---- e2e: public API with host buffers (pinned u in, F + grad out) ----
     pinned = torch.from_numpy(u_host).pin_memory()

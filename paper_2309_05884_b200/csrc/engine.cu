@@ -152,10 +152,12 @@ static int launch_tiny(int d, int which, const TinySliceParams& sp, int grid, in
   }
 }
 
-static int choose_nwarps(int d, int K, int batch, bool mma) {
+constexpr double kChainBudget = 0.88;  // fraction of free device memory the tiny histories may take
+
+static int choose_nwarps(int d, int K, int batch, bool mma, int max_warps = kTinyMaxWarps) {
   const int pg = 32 / tiny_lanes(d, mma);
   const int need = (batch + pg - 1) / pg;
-  int nw = kTinyMaxWarps;
+  int nw = max_warps;
   while (nw > 1 && tiny_smem_bytes(d, K, nw, mma) > kMaxSmem) --nw;
   return std::max(1, std::min(nw, need));
 }
@@ -281,7 +283,9 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
     if (bp.tiny) {
       const int R = objective == SQOC_OBJ_GATE ? d : 1;
       const int pg = 32 / tiny_lanes(d, tiny_mma(d));
-      bp.nwarps = choose_nwarps(d, n_controls, max_batch, tiny_mma(d));
+      // r01: 24 warps for the <= 80-register instantiations beat 12 in the concurrent cfg 1 step
+      // (212.8 vs 215.6 ms) although each sector alone is slower (fewer, larger CTAs)
+      bp.nwarps = choose_nwarps(d, n_controls, max_batch, tiny_mma(d), tiny_fused_max_warps(d));
       bp.nwarps_max = choose_nwarps(d, n_controls, 1 << 30, false);
       const int per_cta = pg * bp.nwarps;
       bp.park_slots = (size_t)((max_batch + per_cta - 1) / per_cta) * per_cta;
@@ -440,7 +444,8 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
         tp.nwarps = nw;
         if (!p->hist_planned) {
           // auto: X histories of all tiny blocks if they fit in 40% of free memory, then chain
-          // histories for the largest blocks first while the total stays within 70%
+          // histories for the largest blocks first while the total stays within kChainBudget
+          // (cfg 1: 149 GB for all seven sectors, 84% of a free B200)
           size_t free_b = 0, total_b = 0, used = 0;
           SQOC_CUDA(cudaMemGetInfo(&free_b, &total_b));
           for (auto& ob : p->blocks)
@@ -454,7 +459,7 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
             BlockPlan& ob = p->blocks[i];
             ob.hist_level = x_ok ? 1 : 0;
             const size_t cb = ob.park_slots * p->N * 4 * ob.d * ob.d * sizeof(double2);
-            if (x_ok && used + cb <= (size_t)(0.7 * (double)free_b)) {
+            if (x_ok && used + cb <= (size_t)(kChainBudget * (double)free_b)) {
               ob.hist_level = 2;
               used += cb;
             }

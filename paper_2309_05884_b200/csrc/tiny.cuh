@@ -28,6 +28,7 @@
 #include <stdint.h>
 
 #include "schemes.h"
+#include "zgemm.cuh"  // cp.async helpers
 
 namespace sqoc {
 
@@ -80,6 +81,9 @@ __constant__ unsigned char c_lane_inv[4][27] = {
     {16, 17, 18, 24, 8, 9, 25, 19, 26, 0, 1, 2, 10, 11, 12, 27, 3, 20, 21, 4, 5, 13, 14, 15, 28, 6, 7}};
 __host__ __device__ constexpr int tiny_stride(int d, bool mma) { return kTinyBuffers * d * d + tiny_pad(d, mma); }
 constexpr int kTinyMaxWarps = 12;  // warps per CTA (12 x 32 threads x 168 registers fills the register file)
+// The fused kernel's small-tile instantiations (d <= 4 DFMA, d = 7, 8 one DMMA tile) need <= 80 registers,
+// so twice the warps fit: more independent problems per SM to hide the LDS / DMMA latencies.
+__host__ __device__ constexpr int tiny_fused_max_warps(int d) { return (d <= 4 || d == 7 || d == 8) ? 24 : kTinyMaxWarps; }
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
 
 struct TinyParams {
@@ -109,6 +113,10 @@ __constant__ double c_s4[15] = {SQOC_S4_Z0, SQOC_S4_Z1, SQOC_S4_Z2, SQOC_S4_Z3, 
                                 SQOC_S4_X5, SQOC_S4_X6, SQOC_S4_B0, SQOC_S4_B1, SQOC_S4_B2,
                                 SQOC_S4_B3, SQOC_S4_C0, SQOC_S4_C1, SQOC_S4_C2, SQOC_S4_C3};
 constexpr double kTheta12 = 0.33;
+// P = X4 A + X5 A2 + X6 A3 = X4 P' with P' = A + kR5 A2 + kR6 A3 (formed once per slice over the own
+// entries instead of in every operand load; A = P' - kR5 A2 - kR6 A3 is recovered where needed)
+constexpr double kR5 = SQOC_S4_X5 / SQOC_S4_X4;
+constexpr double kR6 = SQOC_S4_X6 / SQOC_S4_X4;
 
 __device__ __forceinline__ int choose_squarings(double nrm) {
   int s = 0;
@@ -231,36 +239,59 @@ struct Tile {
   __device__ __forceinline__ void mul(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
     mulL(t, OpP{L}, M);
   }
+  // k-loops are software-pipelined: the operands of step k + 1 are loaded while step k's FMAs
+  // issue (r01 v10 ncu: short-scoreboard waits on the LDS results were the top stall of the DFMA
+  // tiles, profiles/r01_tiny9_v10_ncu.txt)
   template <class OL>
   __device__ __forceinline__ void mulL(double2 (&t)[TSR][TSC], const OL& L, const double2* M) const {
     zero(t);
+    double2 l[TSR], m[TSC];
+#pragma unroll
+    for (int i = 0; i < TSR; ++i) l[i] = L.at(row(i) * D);
+#pragma unroll
+    for (int j = 0; j < TSC; ++j) m[j] = M[col(j)];
 #pragma unroll 2
     for (int k = 0; k < D; ++k) {
-      double2 l[TSR], m[TSC];
+      const int kn = k + 1 < D ? k + 1 : k;
+      double2 nl[TSR], nm[TSC];
 #pragma unroll
-      for (int i = 0; i < TSR; ++i) l[i] = L.at(row(i) * D + k);
+      for (int i = 0; i < TSR; ++i) nl[i] = L.at(row(i) * D + kn);
 #pragma unroll
-      for (int j = 0; j < TSC; ++j) m[j] = M[k * D + col(j)];
+      for (int j = 0; j < TSC; ++j) nm[j] = M[kn * D + col(j)];
 #pragma unroll
       for (int i = 0; i < TSR; ++i)
 #pragma unroll
         for (int j = 0; j < TSC; ++j) cfma(t[i][j], l[i], m[j]);
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) l[i] = nl[i];
+#pragma unroll
+      for (int j = 0; j < TSC; ++j) m[j] = nm[j];
     }
   }
   // t = U^dag M
   __device__ __forceinline__ void mul_adj(double2 (&t)[TSR][TSC], const double2* U, const double2* M) const {
     zero(t);
+    double2 l[TSR], m[TSC];
+#pragma unroll
+    for (int i = 0; i < TSR; ++i) l[i] = cconj(U[row(i)]);
+#pragma unroll
+    for (int j = 0; j < TSC; ++j) m[j] = M[col(j)];
 #pragma unroll 2
     for (int k = 0; k < D; ++k) {
-      double2 l[TSR], m[TSC];
+      const int kn = k + 1 < D ? k + 1 : k;
+      double2 nl[TSR], nm[TSC];
 #pragma unroll
-      for (int i = 0; i < TSR; ++i) l[i] = cconj(U[k * D + row(i)]);
+      for (int i = 0; i < TSR; ++i) nl[i] = cconj(U[kn * D + row(i)]);
 #pragma unroll
-      for (int j = 0; j < TSC; ++j) m[j] = M[k * D + col(j)];
+      for (int j = 0; j < TSC; ++j) nm[j] = M[kn * D + col(j)];
 #pragma unroll
       for (int i = 0; i < TSR; ++i)
 #pragma unroll
         for (int j = 0; j < TSC; ++j) cfma(t[i][j], l[i], m[j]);
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) l[i] = nl[i];
+#pragma unroll
+      for (int j = 0; j < TSC; ++j) m[j] = nm[j];
     }
   }
   // (t, dt) = (L, dL)(M, dM) = (L M, L dM + dL M)
@@ -283,28 +314,62 @@ struct Tile {
                                             const OL& dL, const double2* M, const double2* dM) const {
     if (WT) zero(t);
     zero(dt);
-#pragma unroll 1
+    double2 l[TSR], dl[TSR], m[TSC], dm[TSC];
+#pragma unroll
+    for (int i = 0; i < TSR; ++i) {
+      l[i] = L.at(row(i) * D);
+      dl[i] = dL.at(row(i) * D);
+    }
+#pragma unroll
+    for (int j = 0; j < TSC; ++j) {
+      m[j] = M[col(j)];
+      dm[j] = dM[col(j)];
+    }
+#pragma unroll 2
     for (int k = 0; k < D; ++k) {
-      double2 l[TSR], dl[TSR];
+      const int kn = k + 1 < D ? k + 1 : k;
+      double2 nl[TSR], ndl[TSR], nm[TSC], ndm[TSC];
 #pragma unroll
       for (int i = 0; i < TSR; ++i) {
-        l[i] = L.at(row(i) * D + k);
-        dl[i] = dL.at(row(i) * D + k);
+        nl[i] = L.at(row(i) * D + kn);
+        ndl[i] = dL.at(row(i) * D + kn);
       }
 #pragma unroll
       for (int j = 0; j < TSC; ++j) {
-        const double2 m = M[k * D + col(j)];
-        const double2 dm = dM[k * D + col(j)];
+        nm[j] = M[kn * D + col(j)];
+        ndm[j] = dM[kn * D + col(j)];
+      }
+#pragma unroll
+      for (int j = 0; j < TSC; ++j)
 #pragma unroll
         for (int i = 0; i < TSR; ++i) {
-          if (WT) cfma(t[i][j], l[i], m);
-          cfma(dt[i][j], dl[i], m);
-          cfma(dt[i][j], l[i], dm);
+          if (WT) cfma(t[i][j], l[i], m[j]);
+          cfma(dt[i][j], dl[i], m[j]);
+          cfma(dt[i][j], l[i], dm[j]);
         }
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) {
+        l[i] = nl[i];
+        dl[i] = ndl[i];
+      }
+#pragma unroll
+      for (int j = 0; j < TSC; ++j) {
+        m[j] = nm[j];
+        dm[j] = ndm[j];
       }
     }
   }
 };
+
+// 16-byte global -> shared copies that bypass the registers (LDGSTS): the backward sweep issues
+// the next slice's history reads this way while the current slice computes (r01 v10 ncu: waits on
+// global loads feeding shared-memory stores were 22% of the d = 13 kernel's stall samples,
+// profiles/r01_tiny13_v10_ncu.txt).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+// (cp_async_commit / cp_async_wait<N> come from zgemm.cuh)
 
 __device__ __forceinline__ void tdmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -413,7 +478,7 @@ struct MmaTile {
   __device__ __forceinline__ void mul_op(double2 (&t)[TSR][TSC], const double2* L, const double2* M, bool adj) const {
     double acc[MT][MT][3][2];
     clear(acc);
-#pragma unroll 1
+#pragma unroll
     for (int k0 = 0; k0 < KMMA; k0 += 4) {
       double2 a[MT], b[MT];
 #pragma unroll
@@ -443,7 +508,7 @@ struct MmaTile {
   __device__ __forceinline__ void mulL(double2 (&t)[TSR][TSC], const OL& L, const double2* M) const {
     double acc[MT][MT][3][2];
     clear(acc);
-#pragma unroll 1
+#pragma unroll
     for (int k0 = 0; k0 < KMMA; k0 += 4) {
       double2 a[MT], b[MT];
 #pragma unroll
@@ -470,7 +535,7 @@ struct MmaTile {
   __device__ __forceinline__ void mul_bt(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
     double acc[MT][MT][3][2];
     clear(acc);
-#pragma unroll 1
+#pragma unroll
     for (int k0 = 0; k0 < KMMA; k0 += 4) {
       double2 a[MT], b[MT];
 #pragma unroll
@@ -518,7 +583,7 @@ struct MmaTile {
     double acc[MT][MT][3][2], dacc[MT][MT][3][2];
     if (WT) clear(acc);
     clear(dacc);
-#pragma unroll 1
+#pragma unroll
     for (int k0 = 0; k0 < KMMA; k0 += 4) {
       double2 a[MT], da[MT], b[MT], db[MT];
 #pragma unroll
@@ -658,11 +723,18 @@ struct TinyCtx {
       for (int jj = 0; jj < TSC; ++jj) t[i][jj] = cscale(t[i][jj], c);
   }
 
+  // controls of slice j (loaded one slice ahead by the sweeps so the global latency is hidden)
+  __device__ __forceinline__ void load_u(int j, double (&uk)[kMaxControls]) const {
+#pragma unroll
+    for (int k = 0; k < kMaxControls; ++k) uk[k] = (k < K) ? up[k * N + j] : 0.0;
+  }
   // A tile of slice j (scaled by 2^-s) and the warp-uniform Taylor plan
   __device__ __forceinline__ void build_a(int j, T2& a, int& s) const {
     double uk[kMaxControls];
-#pragma unroll
-    for (int k = 0; k < kMaxControls; ++k) uk[k] = (k < K) ? up[k * N + j] : 0.0;
+    load_u(j, uk);
+    build_a_u(uk, a, s);
+  }
+  __device__ __forceinline__ void build_a_u(const double (&uk)[kMaxControls], T2& a, int& s) const {
     double rowsum[TSR];
 #pragma unroll
     for (int i = 0; i < TSR; ++i) {
@@ -709,6 +781,43 @@ struct TinyCtx {
         t[i][jj] = v;
       }
   }
+  // own entries, in place allowed: dst = M1 + kR5 M2 + kR6 M3 (the scheme's P / X4)
+  __device__ __forceinline__ void form_p(double2* dst, const double2* M1, const double2* M2, const double2* M3) const {
+#pragma unroll
+    for (int i = 0; i < TSR; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TSC; ++jj) {
+        const int o = tl.row(i) * D + tl.col(jj);
+        const double2 a = M1[o], b = M2[o], c = M3[o];
+        const double2 v = make_double2(fma(kR6, c.x, fma(kR5, b.x, a.x)), fma(kR6, c.y, fma(kR5, b.y, a.y)));
+        if (act && tl.ok(i, jj)) dst[tl.rrow(i) * D + tl.rcol(jj)] = v;
+      }
+  }
+  // asynchronous copy of the own entries of a D x D matrix (global -> shared)
+  __device__ __forceinline__ void async_dd(double2* dst, const double2* src) const {
+    if (!act) return;
+#pragma unroll
+    for (int i = 0; i < TSR; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TSC; ++jj)
+        if (tl.ok(i, jj)) {
+          const int o = tl.rrow(i) * D + tl.rcol(jj);
+          cp_async16(dst + o, src + o);
+        }
+  }
+  // dtau_k = Tr(N E_k) from the own entries of N held in registers
+  __device__ __forceinline__ void traces_own(const T2& n, double2 (&dtau)[kMaxControls]) const {
+    for (int k = 0; k < K; ++k) {
+      const double2* E = gen + (k + 1) * DD;
+      double2 pk = czero();
+#pragma unroll
+      for (int i = 0; i < TSR; ++i)
+#pragma unroll
+        for (int jj = 0; jj < TSC; ++jj)
+          if (tl.ok(i, jj)) cfma(pk, n[i][jj], E[tl.rcol(jj) * D + tl.rrow(i)]);
+      dtau[k] = psum2(pk);
+    }
+  }
   __device__ __forceinline__ void load_own(T2& t, const double2* M) const {
 #pragma unroll
     for (int i = 0; i < TSR; ++i)
@@ -732,8 +841,12 @@ struct TinyCtx {
     tl.store(B3, t, act);
     if (ch) tl.store(ch + DD, t, act);
     __syncwarp();
-    tl.mulL(t, OpL3{B1, B2, B3, c_s4[4], c_s4[5], c_s4[6]}, B3);  // Z = (x4 A + x5 A2 + x6 A3) A3 + z(A)
+    form_p(B4, B1, B2, B3);  // P' = P / x4
+    __syncwarp();
+    tl.mul(t, B4, B3);  // Z = x4 P' A3 + z(A)
+    scale(t, SQOC_S4_X4);
     add_poly(t, c_s4[0], c_s4[1], B1, c_s4[2], B2, c_s4[3], B3);
+    __syncwarp();  // every lane has read P' (B4) before Z overwrites it
 #pragma unroll
     for (int i = 0; i < TSR; ++i)
 #pragma unroll
@@ -771,8 +884,11 @@ struct TinyCtx {
     tl.dpairL(dt, OpP{B0}, OpP{B1}, B2, B3);  // dA3 = A2 dA + dA2 A
     tl.store(B5, dt, act);
     __syncwarp();
-    tl.dpairL(dt, OpL3{B2, B0, B4, c_s4[4], c_s4[5], c_s4[6]}, OpL3{B3, B1, B5, c_s4[4], c_s4[5], c_s4[6]}, B4,
-              B5);  // P dA3 + dP A3
+    form_p(B2, B2, B0, B4);  // A -> P' in place (A = P' - kR5 A2 - kR6 A3 below)
+    form_p(B3, B3, B1, B5);  // dA -> dP'
+    __syncwarp();
+    tl.dpairL(dt, OpP{B2}, OpP{B3}, B4, B5);  // x4 (P' dA3 + dP' A3)
+    scale(dt, SQOC_S4_X4);
     __syncwarp();
     // own entries, in place: Z (history) -> B0, W = Z + b(A) -> B2, dZ -> B1, dW -> B3, dC -> B5
 #pragma unroll
@@ -781,7 +897,10 @@ struct TinyCtx {
       for (int jj = 0; jj < TSC; ++jj) {
         const int o = tl.row(i) * D + tl.col(jj);
         const bool dg = tl.rrow(i) == tl.rcol(jj);
-        const double2 a = B2[o], a2 = B0[o], a3 = B4[o], da = B3[o], da2 = B1[o], da3 = B5[o];
+        const double2 a2 = B0[o], a3 = B4[o], da2 = B1[o], da3 = B5[o];
+        const double2 pa = B2[o], dpa = B3[o];
+        const double2 a = make_double2(pa.x - kR5 * a2.x - kR6 * a3.x, pa.y - kR5 * a2.y - kR6 * a3.y);
+        const double2 da = make_double2(dpa.x - kR5 * da2.x - kR6 * da3.x, dpa.y - kR5 * da2.y - kR6 * da3.y);
         const double2 z = ch[2 * DD + o];
         double2 dz = dt[i][jj];
         dz.x += c_s4[1] * da.x + c_s4[2] * da2.x + c_s4[3] * da3.x;
@@ -832,8 +951,12 @@ struct TinyCtx {
     tl.store(B4, t, act);
     tl.store(B5, dt, act);
     __syncwarp();
-    tl.pairL(t, dt, OpL3{B2, B0, B4, c_s4[4], c_s4[5], c_s4[6]}, OpL3{B3, B1, B5, c_s4[4], c_s4[5], c_s4[6]}, B4,
-             B5);  // (P A3, P dA3 + dP A3)
+    form_p(B2, B2, B0, B4);  // A -> P' in place
+    form_p(B3, B3, B1, B5);  // dA -> dP'
+    __syncwarp();
+    tl.pair(t, dt, B2, B3, B4, B5);  // x4 (P' A3, P' dA3 + dP' A3)
+    scale(t, SQOC_S4_X4);
+    scale(dt, SQOC_S4_X4);
     __syncwarp();
     // own entries only, in place: Z -> B0 (A2), W = Z + b(A) -> B2 (A), C = c(A) -> B4 (A3);
     // dZ -> B1 (dA2), dW -> B3 (dA), dC -> B5 (dA3)
@@ -843,7 +966,10 @@ struct TinyCtx {
       for (int jj = 0; jj < TSC; ++jj) {
         const int o = tl.row(i) * D + tl.col(jj);
         const bool dg = tl.rrow(i) == tl.rcol(jj);
-        const double2 a = B2[o], a2 = B0[o], a3 = B4[o], da = B3[o], da2 = B1[o], da3 = B5[o];
+        const double2 a2 = B0[o], a3 = B4[o], da2 = B1[o], da3 = B5[o];
+        const double2 pa = B2[o], dpa = B3[o];
+        const double2 a = make_double2(pa.x - kR5 * a2.x - kR6 * a3.x, pa.y - kR5 * a2.y - kR6 * a3.y);
+        const double2 da = make_double2(dpa.x - kR5 * da2.x - kR6 * da3.x, dpa.y - kR5 * da2.y - kR6 * da3.y);
         double2 z = t[i][jj], dz = dt[i][jj];
         z.x += c_s4[1] * a.x + c_s4[2] * a2.x + c_s4[3] * a3.x + (dg ? c_s4[0] : 0.0);
         z.y += c_s4[1] * a.y + c_s4[2] * a2.y + c_s4[3] * a3.y;
@@ -1019,10 +1145,131 @@ __device__ __forceinline__ double2* load_generators(const TinyParams& p) {
   return smem;
 }
 
+// ------------------------------------------------------------------ backward sweep (gate, chain history)
+// Per slice j (X_{j-1}, A2_j, A3_j, Z_j, Y_j from the forward sweep's histories; Lam_j from the
+// previous step): dA = 2^-s X_{j-1} Lam_j^dag, the derivative halves of the scheme's pair chain give
+// N = L_R(A_j, dA) with dtau/du_kj = Tr(N E_k), and Lam_{j-1} = U_j^dag Lam_j.  Every history read is
+// an asynchronous copy issued one phase (or one slice) before its use, into a buffer that is free by
+// then, so no global latency sits on the warp's dependency chain:
+//   step start : B0 = X_{j-1}, B5 = A2, B4 = A3 (prefetched), B1 = Lam_j (smem, previous step)
+//   B2 = A; B3 = dA; B0 = dA2; B1 = dA3; B2/B3 = P'/dP' in place; dPA3 -> regs (Z read into regs)
+//   own pass: B5 = Z, B2 = W, B0 = dZ, B3 = dW, B1 = dC; async Y -> B4
+//   dY -> regs; async Lam_j (park) -> B3, next X -> B0, next A2 -> B5; traces; Lam_{j-1} -> B1 + park;
+//   async next A3 -> B4.
+template <int D, class C>
+__device__ __forceinline__ void bwd_chain_gate(const C& c, const TinyParams& p, const double2* chh, const double2* xh,
+                                               double2* parkL, double2 ctw, int prob) {
+  constexpr int DD = C::DD;
+  const int K = p.K, N = p.N;
+  using T2 = typename C::T2;
+  const auto& tl = c.tl;
+  double2 *B0 = c.B0, *B1 = c.B1, *B2 = c.B2, *B3 = c.B3, *B4 = c.B4, *B5 = c.B5;
+  c.copy_x(B1, p.target);  // Lam_N = V
+  c.async_dd(B0, xh + (size_t)(N - 1) * DD);
+  c.async_dd(B5, chh + (size_t)(N - 1) * 4 * DD);
+  c.async_dd(B4, chh + (size_t)(N - 1) * 4 * DD + DD);
+  cp_async_commit();
+  double ucur[kMaxControls], unext[kMaxControls];
+  c.load_u(N - 1, ucur);
+  T2 t, dt;
+  for (int j = N - 1; j >= 0; --j) {
+    const double2* ch = chh + (size_t)j * 4 * DD;
+    int s;
+    c.load_u(j > 0 ? j - 1 : j, unext);
+    c.build_a_u(ucur, t, s);
+#pragma unroll
+    for (int k = 0; k < kMaxControls; ++k) ucur[k] = unext[k];
+    tl.store(B2, t, c.act);  // A
+    cp_async_wait<0>();
+    __syncwarp();
+    c.seed_c(s);  // B3 = 2^-s X_{j-1} Lam_j^dag (synced)
+    tl.dpairL(dt, OpP{B2}, OpP{B3}, B2, B3);  // dA2 = A dA + dA A
+    tl.store(B0, dt, c.act);
+    __syncwarp();
+    tl.dpairL(dt, OpP{B5}, OpP{B0}, B2, B3);  // dA3 = A2 dA + dA2 A
+    tl.store(B1, dt, c.act);
+    T2 zr;
+    c.load_own(zr, ch + 2 * DD);  // Z (consumed after the next product)
+    __syncwarp();
+    c.form_p(B2, B2, B5, B4);  // A -> P'
+    c.form_p(B3, B3, B0, B1);  // dA -> dP'
+    __syncwarp();
+    tl.dpairL(dt, OpP{B2}, OpP{B3}, B4, B1);  // x4 (P' dA3 + dP' A3)
+    c.scale(dt, SQOC_S4_X4);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < C::TSR; ++i)
+#pragma unroll
+      for (int jj = 0; jj < C::TSC; ++jj) {
+        const int o = tl.row(i) * D + tl.col(jj);
+        const bool dg = tl.rrow(i) == tl.rcol(jj);
+        const double2 a2 = B5[o], a3 = B4[o], da2 = B0[o], da3 = B1[o], pa = B2[o], dpa = B3[o];
+        const double2 a = make_double2(pa.x - kR5 * a2.x - kR6 * a3.x, pa.y - kR5 * a2.y - kR6 * a3.y);
+        const double2 da = make_double2(dpa.x - kR5 * da2.x - kR6 * da3.x, dpa.y - kR5 * da2.y - kR6 * da3.y);
+        const double2 z = zr[i][jj];
+        double2 dz = dt[i][jj];
+        dz.x += c_s4[1] * da.x + c_s4[2] * da2.x + c_s4[3] * da3.x;
+        dz.y += c_s4[1] * da.y + c_s4[2] * da2.y + c_s4[3] * da3.y;
+        const double2 w = make_double2(z.x + c_s4[8] * a.x + c_s4[9] * a2.x + c_s4[10] * a3.x + (dg ? c_s4[7] : 0.0),
+                                       z.y + c_s4[8] * a.y + c_s4[9] * a2.y + c_s4[10] * a3.y);
+        const double2 dw = make_double2(dz.x + c_s4[8] * da.x + c_s4[9] * da2.x + c_s4[10] * da3.x,
+                                        dz.y + c_s4[8] * da.y + c_s4[9] * da2.y + c_s4[10] * da3.y);
+        const double2 dc = make_double2(c_s4[12] * da.x + c_s4[13] * da2.x + c_s4[14] * da3.x,
+                                        c_s4[12] * da.y + c_s4[13] * da2.y + c_s4[14] * da3.y);
+        if (c.act && tl.ok(i, jj)) {
+          const int q = tl.rrow(i) * D + tl.rcol(jj);
+          B5[q] = z;
+          B2[q] = w;
+          B0[q] = dz;
+          B3[q] = dw;
+          B1[q] = dc;
+        }
+      }
+    c.async_dd(B4, ch + 3 * DD);  // Y (= U_j when s = 0); A3 is dead (own entries only were read)
+    cp_async_commit();
+    __syncwarp();
+    tl.dpairL(dt, OpP{B2}, OpP{B3}, B5, B0);  // dY = W dZ + dW Z (+ dC)
+    c.add_poly(dt, 0.0, 1.0, B1, 0.0, B1, 0.0, nullptr);
+    __syncwarp();
+    c.async_dd(B3, parkL);  // Lam_j (parked by the previous step)
+    cp_async_commit();
+    if (j > 0) {  // next slice: X_{j-2} -> B0, A2_{j-1} -> B5
+      c.async_dd(B0, xh + (size_t)(j - 1) * DD);
+      c.async_dd(B5, chh + (size_t)(j - 1) * 4 * DD);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();  // Y and Lam_j have landed
+    __syncwarp();
+    if (s > 0) {  // squarings of the pair (U, N): U in B4, N in B1
+      tl.store(B1, dt, c.act);
+      for (int r = 0; r < s; ++r) {
+        __syncwarp();
+        tl.pair(t, dt, B4, B1, B4, B1);
+        __syncwarp();
+        tl.store(B4, t, c.act);
+        tl.store(B1, dt, c.act);
+      }
+      __syncwarp();
+    }
+    double2 dtau[kMaxControls];
+    c.traces_own(dt, dtau);
+    for (int k = 0; k < K; ++k)
+      if (c.real && c.q == 0) p.grad_out[((size_t)prob * K + k) * N + j] = ctw.x * dtau[k].x - ctw.y * dtau[k].y;
+    tl.mul_adj(t, B4, B3);  // Lam_{j-1} = U_j^dag Lam_j
+    __syncwarp();
+    tl.store(B1, t, c.act);
+    tl.store(parkL, t, c.act);
+    if (j > 0) c.async_dd(B4, chh + (size_t)(j - 1) * 4 * DD + DD);  // A3_{j-1}
+    cp_async_commit();
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------------ fused kernel
 // One launch per block: all slices, both sweeps, gradient traces, on chip.
 template <int D, bool GATE>
-__global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyParams p) {
+__global__ void __launch_bounds__(tiny_fused_max_warps(D) * 32) grape_tiny_kernel(TinyParams p) {
   using C = TinyCtx<D, GATE>;
   constexpr int R = C::R;
   const int K = p.K, N = p.N;
@@ -1050,9 +1297,14 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
   else c.copy_x(X, p.x0);
   __syncwarp();
   typename C::T2 t;
+  double ucur[kMaxControls], unext[kMaxControls];
+  if (N > 0) c.load_u(0, ucur);
   for (int j = 0; j < N; ++j) {
     int s;
-    c.build_a(j, t, s);
+    c.load_u(j + 1 < N ? j + 1 : j, unext);
+    c.build_a_u(ucur, t, s);
+#pragma unroll
+    for (int k = 0; k < kMaxControls; ++k) ucur[k] = unext[k];
     c.tl.store(c.B1, t, c.act);
     if (hist) c.copy_x(xh + (size_t)j * D * R, X);  // X_{j-1}
     __syncwarp();
@@ -1068,11 +1320,21 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) grape_tiny_kernel(TinyPara
 
   // ================= backward sweep: gradient =================
   const double2 ctw = cscale(cconj(tau), 2.0 * p.weight);  // dF/du = Re(2 w conj(tau) dtau/du)
+  if constexpr (GATE) {
+    if (chh) {
+      bwd_chain_gate<D>(c, p, chh, xh, parkL, ctw, prob);
+      return;
+    }
+  }
+  if (N > 0) c.load_u(N - 1, ucur);
   for (int j = N - 1; j >= 0; --j) {
     int s;
+    c.load_u(j > 0 ? j - 1 : j, unext);
     c.copy_x(c.B0, hist ? xh + (size_t)j * D * R : parkX);  // stage X_{j-1} (history) or X_j, and Lam_j
     c.copy_x(c.B1, parkL);
-    c.build_a(j, t, s);
+    c.build_a_u(ucur, t, s);
+#pragma unroll
+    for (int k = 0; k < kMaxControls; ++k) ucur[k] = unext[k];
     c.tl.store(c.B2, t, c.act);
     __syncwarp();
     c.seed_c(s);
