@@ -83,7 +83,15 @@ __host__ __device__ constexpr int tiny_stride(int d, bool mma) { return kTinyBuf
 constexpr int kTinyMaxWarps = 12;  // warps per CTA (12 x 32 threads x 168 registers fills the register file)
 // The fused kernel's small-tile instantiations (d <= 4 DFMA, d = 7, 8 one DMMA tile) need <= 80 registers,
 // so twice the warps fit: more independent problems per SM to hide the LDS / DMMA latencies.
-__host__ __device__ constexpr int tiny_fused_max_warps(int d) { return (d <= 4 || d == 7 || d == 8) ? 24 : kTinyMaxWarps; }
+// The DFMA-tile sectors d = 9..12 are shared-memory bound below 12 warps (K = 2: 9, 11, 9, 8 warps).  Each
+// SM sub-partition owns a quarter of the register file, so 9 warps (3 on one sub-partition) still cap a
+// thread at 168 registers and leave the sub-partitions unbalanced; 8 warps (2 per sub-partition) give the
+// operand prefetch up to 255 registers (r01: d = 11 77.5 -> 60.1 ms, d = 9 77.8 -> 64.2 ms alone; cfg 1 step
+// 212.4 -> 200.8 ms).  d = 13 stays at 12 warps: 8 warps speed it up alone (90.7 -> 86.8 ms) but slow the
+// concurrent step (207.5 ms).
+__host__ __device__ constexpr int tiny_fused_max_warps(int d) {
+  return (d <= 4 || d == 7 || d == 8) ? 24 : (d >= 9 && d <= 12) ? 8 : kTinyMaxWarps;
+}
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
 
 struct TinyParams {
@@ -1269,7 +1277,7 @@ __device__ __forceinline__ void bwd_chain_gate(const C& c, const TinyParams& p, 
 // ------------------------------------------------------------------ fused kernel
 // One launch per block: all slices, both sweeps, gradient traces, on chip.
 template <int D, bool GATE>
-__global__ void __launch_bounds__(tiny_fused_max_warps(D) * 32) grape_tiny_kernel(TinyParams p) {
+__global__ void __launch_bounds__(tiny_fused_max_warps(D) * 32, 1) grape_tiny_kernel(TinyParams p) {
   using C = TinyCtx<D, GATE>;
   constexpr int R = C::R;
   const int K = p.K, N = p.N;
