@@ -279,11 +279,14 @@ def run_ours(args):
     e2e = []
     if ws > 1:
         dist.barrier()
-    for _ in range(max(1, min(args.steps, 3))):
+    clocks_e2e = ClockSampler(local)
+    clocks_e2e.start()
+    for _ in range(max(3, args.steps)):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         eng.evaluate_host_ptr(pinned.data_ptr(), batch, Fh.data_ptr(), gh.data_ptr())
         e2e.append(time.perf_counter() - t0)
+    clk_e2e = clocks_e2e.stop()
     e2e_s = float(np.mean(e2e))
     te = torch.tensor([e2e_s], dtype=torch.float64, device=u.device)
     if ws > 1:
@@ -338,6 +341,7 @@ def run_ours(args):
                 "l2": "flushed between timed steps (256 MB write, untimed)",
                 "algorithmic_flops_per_eval": flops_eval,
                 "step_tflops_algorithmic": flops_eval * batch / (ms_max / 1e3) / 1e12,
+                "steps_ms": [round(t, 2) for t in times],
             },
             "roofline": {
                 "bound": "tensor",
@@ -357,6 +361,8 @@ def run_ours(args):
                 "unit": UNIT,
                 "h2d_bytes_per_step": int(u_host.nbytes),
                 "d2h_bytes_per_step": int(Fh.numel() * 8 + gh.numel() * 8),
+                "calls_ms": [round(t * 1e3, 2) for t in e2e],
+                "clocks": clk_e2e,
             },
             "gpu_launches": int(launches),
             "clocks": clk,

@@ -88,9 +88,9 @@ constexpr int kTinyMaxWarps = 12;  // warps per CTA (12 x 32 threads x 168 regis
 // thread at 168 registers and leave the sub-partitions unbalanced; 8 warps (2 per sub-partition) give the
 // operand prefetch up to 255 registers (r01: d = 11 77.5 -> 60.1 ms, d = 9 77.8 -> 64.2 ms alone; cfg 1 step
 // 212.4 -> 200.8 ms).  d = 13 stays at 12 warps: 8 warps speed it up alone (90.7 -> 86.8 ms) but slow the
-// concurrent step (207.5 ms).
+// concurrent step (207.5 ms); d = 5, 6 keep 12 (8 or 16 warps: 24.6 / 23.1 ms alone vs 17.5).
 __host__ __device__ constexpr int tiny_fused_max_warps(int d) {
-  return (d <= 4 || d == 7 || d == 8) ? 24 : (d >= 9 && d <= 12) ? 8 : kTinyMaxWarps;
+  return (d <= 4 || d == 7 || d == 8) ? 24 :  (d >= 9 && d <= 12) ? 8 : kTinyMaxWarps;
 }
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
 
