@@ -276,7 +276,17 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
       if (rc) break;
       chk(cudaMemcpy(bp.x0, initial[b], d * sizeof(double2), cudaMemcpyHostToDevice), "copy x0");
     }
-    chk(cudaStreamCreateWithFlags(&bp.stream, cudaStreamNonBlocking), "stream");
+    {
+      // Longest-first CTA dispatch among the concurrent block kernels: the larger the block, the
+      // higher its stream priority (distinct larger dims ranked; ties share a level).
+      int least = 0, greatest = 0;
+      cudaDeviceGetStreamPriorityRange(&least, &greatest);
+      std::vector<int> larger;
+      for (int o = 0; o < n_blocks; ++o)
+        if (dims[o] > d && std::find(larger.begin(), larger.end(), dims[o]) == larger.end()) larger.push_back(dims[o]);
+      const int prio = std::min(least, greatest + (int)larger.size());
+      chk(cudaStreamCreateWithPriority(&bp.stream, cudaStreamNonBlocking, prio), "stream");
+    }
     chk(cudaEventCreateWithFlags(&bp.done, cudaEventDisableTiming), "event");
     chk(cudaEventCreate(&bp.t0), "event");
     chk(cudaEventCreate(&bp.t1), "event");
