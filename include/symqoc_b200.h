@@ -103,7 +103,7 @@ int sqoc_last_tiny_schedule(const sqoc_problem* p);
  * X_{j-1} Lam_j^dag: two GEMM-units per slice fewer), 2 X + chain history (also the propagator
  * chain A2, A3, Z, Y of every slice: only the derivative halves of the pairs run, four more units
  * fewer).  -1 auto (default): X histories when they fit in 40% of free memory, chain histories
- * for the largest blocks first while the total stays within 70%.
+ * for the largest blocks first while the total stays within 88%.
  * sqoc_last_tiny_history reports the highest level the last fused evaluation used (-1 none). */
 int sqoc_set_tiny_history(sqoc_problem* p, int mode);
 int sqoc_last_tiny_history(const sqoc_problem* p);
@@ -151,6 +151,31 @@ int sqoc_block_time_ms(const sqoc_problem* p, int block, double* ms);
 
 /* Device kernel launches issued by the last sqoc_eval on this problem. */
 int sqoc_last_launch_count(const sqoc_problem* p);
+
+/* On-GPU D_n symmetry-adapted basis.  Builds, on `device`, the full
+ * D_n block basis of n spins (3 <= n <= 16) with the reference's block order and column order
+ * (adjoint._dn_full_projected, adjoint.py:198-220: irrep rows A1, A2, (B1, B2), E_k(j); each
+ * row's matrix-element projector applied to Fock states, Gram-Schmidt with tolerance 1e-8,
+ * columns sorted by (Hamming weight, generating index)); every column is supported on one
+ * D_n orbit.  The reference refuses n > 10 (adjoint.py:231-232).
+ *   sqoc_basis_info     : number of blocks, dims[b], irrep row of each block
+ *                         (0 A1, 1 A2, then B1, B2 for even n, then E_k rows j = 1, 2)
+ *   sqoc_basis_nnz      : stored entries of block b's columns
+ *   sqoc_basis_columns  : keys[i] = generating Fock index of column i, col_nnz[i] = its support size;
+ *                         rows/vals = the support (ascending Fock index) and real entries, column by column
+ *   sqoc_basis_compress : A_b^T H A_b for every block b (AdjointMatrix.compress, adjoint.py:61-64)
+ *                         of H = sum_t coef_t P_t, P_t e_x = (-1)^popcount(x & sign[t]) e_{x ^ flip[t]}
+ *                         (coef complex interleaved; a Pauli string with X/Y letters in flip, Z/Y letters
+ *                         in sign and the factor i^#Y folded into coef); out[b] = d_b x d_b complex
+ *                         host buffers.  Deterministic (one thread per block column, fixed order). */
+typedef struct sqoc_basis sqoc_basis;
+int sqoc_dn_basis_create(sqoc_basis** out, int device, int n);
+int sqoc_basis_info(const sqoc_basis* b, int* n_blocks, int* dims, int* irrep_rows);
+int sqoc_basis_nnz(const sqoc_basis* b, int block, long long* nnz);
+int sqoc_basis_columns(const sqoc_basis* b, int block, int* keys, int* col_nnz, int* rows, double* vals);
+int sqoc_basis_compress(const sqoc_basis* b, int n_terms, const int* flip, const int* sign, const double* coef,
+                        double* const* out);
+int sqoc_basis_destroy(sqoc_basis* b);
 
 /* Largest block dimension the fused on-chip (tiny) path handles. */
 int sqoc_tiny_max_dim(void);

@@ -50,6 +50,12 @@ SIGNATURES = {
     "sqoc_eval_chunk": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _P]),
     "sqoc_block_time_ms": (_I, [_P, _I, _D]),
     "sqoc_tiny_max_dim": (_I, []),
+    "sqoc_dn_basis_create": (_I, [ctypes.POINTER(_P), _I, _I]),
+    "sqoc_basis_info": (_I, [_P, ctypes.POINTER(_I), _P, _P]),
+    "sqoc_basis_nnz": (_I, [_P, _I, ctypes.POINTER(ctypes.c_longlong)]),
+    "sqoc_basis_columns": (_I, [_P, _I, _P, _P, _P, _P]),
+    "sqoc_basis_compress": (_I, [_P, _I, _P, _P, _P, _P]),
+    "sqoc_basis_destroy": (_I, [_P]),
     "sqoc_last_error": (ctypes.c_char_p, []),
     "sqoc_abi_version": (_I, []),
 }

@@ -26,6 +26,7 @@ static int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+int report_error(int code, const std::string& msg) { return fail(code, msg); }  // other translation units
 
 #define SQOC_CUDA(call)                                                                      \
   do {                                                                                       \

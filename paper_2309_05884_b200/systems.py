@@ -163,9 +163,27 @@ def state_transfer_ring(n: int, T: float, n_slices: int, seed: int = 0, full: bo
     return GrapeSystem(f"ring{n}-A1", n, [blk], "state", T, n_slices, [phi_f], [psi0])
 
 
-def gate_ring(n: int, T: float, n_slices: int, seed: int = 0) -> GrapeSystem:
-    h0, hk = _operators(n, "ring")
-    blocks = _blocks_from_basis(symmetry.dn_full_basis(n), h0, hk)
+def gate_ring(n: int, T: float, n_slices: int, seed: int = 0, builder: str = "host") -> GrapeSystem:
+    """D_n-blocked ring, gate fidelity per block.  ``builder="gpu"`` builds the basis and the
+    compressed generators on the GPU (gpu_basis.py); same blocks, same order."""
+    if builder == "gpu":
+        from . import gpu_basis
+
+        gb = gpu_basis.GpuDnBasis(n)
+        try:
+            bases = gb.blocks()
+            mats = [gb.compress(t) for t in (ring_heisenberg(n), *global_controls(n))]
+        finally:
+            gb.close()
+        blocks = [
+            Block(b.label, hermitian_part(mats[0][i]), [hermitian_part(mats[1][i]), hermitian_part(mats[2][i])], b)
+            for i, b in enumerate(bases)
+        ]
+    elif builder == "host":
+        h0, hk = _operators(n, "ring")
+        blocks = _blocks_from_basis(symmetry.dn_full_basis(n), h0, hk)
+    else:
+        raise ValueError(f"unknown basis builder {builder!r}")
     rng = np.random.default_rng((seed, 0x6A7E))
     targets = [haar_unitary(rng, b.dim) for b in blocks]
     return GrapeSystem(f"ring{n}-Dn", n, blocks, "gate", T, n_slices, targets)
@@ -193,9 +211,9 @@ def config(index: int, seed: int = 0, **overrides) -> GrapeSystem:
     if index == 1:
         return gate_all_to_all(overrides.get("n", 12), T, n_sl, seed)
     if index == 2:
-        return gate_ring(overrides.get("n", 10), T, n_sl, seed)
+        return gate_ring(overrides.get("n", 10), T, n_sl, seed, builder=overrides.get("builder", "host"))
     if index == 3:
-        return gate_ring(overrides.get("n", 14), T, n_sl, seed)
+        return gate_ring(overrides.get("n", 14), T, n_sl, seed, builder=overrides.get("builder", "host"))
     if index == 4:
         return state_transfer_ring(overrides.get("n", 12), T, n_sl, seed, full=overrides.get("full", True))
     raise ValueError(f"no config {index}")

@@ -60,3 +60,21 @@ def test_dn14_block_sizes():
     """n=14 is refused by the reference (adjoint.py:231-232); sizes from the character formula."""
     sizes = [b.dim for b in symmetry.dn_full_basis(14)]
     assert sizes == [687, 495, 549, 613] + [1161, 1161, 1179, 1179] * 3
+
+
+def test_pauli_term_encoding_for_gpu_compression():
+    """gpu_basis.pauli_terms reproduces pauli.realize (CPU check of the GPU compression input)."""
+    import numpy as np
+
+    from paper_2309_05884_b200 import gpu_basis, pauli, systems
+
+    n = 5
+    for op in (systems.ring_heisenberg(n), *systems.global_controls(n),
+               pauli.PauliTermSum(n, [pauli.PauliString(n, "XYZIY", 0.7), pauli.PauliString(n, "YYIZX", -1.3)])):
+        flip, sign, coef = gpu_basis.pauli_terms(op)
+        dense = np.zeros((1 << n, 1 << n), dtype=np.complex128)
+        for f, sg, cr, ci in zip(flip, sign, coef[0::2], coef[1::2]):
+            for x in range(1 << n):
+                par = bin(x & int(sg)).count("1") & 1
+                dense[x ^ int(f), x] += (cr + 1j * ci) * (-1.0 if par else 1.0)
+        assert np.abs(dense - pauli.realize(op).toarray()).max() <= 1e-15
