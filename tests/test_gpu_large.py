@@ -237,3 +237,22 @@ def test_other_control_counts(K):
     Fo, go, _ = O.objective(s, u)
     assert abs(F - Fo) <= F_TOL
     assert rel(g, go) <= G_TOL
+
+
+def test_cfg3_blocks_short_grid_against_oracle():
+    """cfg 3 (n = 14, D_14 blocks built on the GPU): the A1 block and one block of each large size
+    (687, 1161, 1179) on a 3-slice grid of the config's dt, against the eigh/Daleckii-Krein oracle."""
+    import copy
+
+    full = systems.config(3, n_slices=3, builder="gpu")
+    keep = [0, 4, 6]
+    s = copy.copy(full)
+    s.blocks = [full.blocks[b] for b in keep]
+    s.targets = [full.targets[b] for b in keep]
+    assert [b.dim for b in s.blocks] == [687, 1161, 1179]
+    eng = GrapeEngine(s, max_batch=1)
+    u = s.controls(5)
+    F, g = eng.objective(u)
+    Fo, go, _ = O.objective(s, u)
+    assert abs(F - Fo) <= F_TOL
+    assert rel(g, go) <= G_TOL
