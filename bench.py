@@ -90,9 +90,13 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_system(cfg: int):
+def build_system(cfg: int, gpu_basis: bool = False):
+    """BASELINE configs[cfg].  Our arm builds the D_n bases of cfg 2 / 3 on the GPU (SURVEY 8f-2,
+    untimed setup); the CPU baseline (worker processes) always uses the host restatement."""
     from paper_2309_05884_b200 import systems
 
+    if gpu_basis and cfg in (2, 3):
+        return systems.config(cfg, builder="gpu")
     return systems.config(cfg)
 
 
@@ -187,7 +191,7 @@ def run_ours(args):
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = args.config
-    s = build_system(cfg)
+    s = build_system(cfg, gpu_basis=True)
     from paper_2309_05884_b200 import systems
 
     batch = args.batch or systems.CONFIG_BATCH[cfg]
@@ -387,7 +391,7 @@ def run_sharded(args):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = args.config
-    s = build_system(cfg)
+    s = build_system(cfg, gpu_basis=True)
     comm = parallel.Comm(device=torch.device("cuda", local))
     obj = parallel.ShardedObjective(s, comm, lambda sys_: GrapeEngine(sys_, max_batch=1, device=local))
     u = s.controls(0)

@@ -297,6 +297,9 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
       // r01: 24 warps for the <= 80-register instantiations beat 12 in the concurrent cfg 1 step
       // (212.8 vs 215.6 ms) although each sector alone is slower (fewer, larger CTAs)
       bp.nwarps = choose_nwarps(d, n_controls, max_batch, tiny_mma(d), tiny_fused_max_warps(d));
+      // One CTA fills an SM (12 or 8 warps).  r01: 4-warp CTAs (3 per SM) run the d = 13 sector alone
+      // in 79.0 instead of 90.7 ms (shorter tail) but spend 10% more active SM time (77.3 vs 69.9
+      // SM-ms: SMs partly filled between CTAs), so the concurrent cfg 1 step slows to 212.9 ms.
       bp.nwarps_max = choose_nwarps(d, n_controls, 1 << 30, false);
       const int per_cta = pg * bp.nwarps;
       bp.park_slots = (size_t)((max_batch + per_cta - 1) / per_cta) * per_cta;

@@ -50,7 +50,14 @@ def pauli_terms(term_sum: pauli.PauliTermSum):
 class GpuDnBasis:
     """Full D_n block basis of n spins built on the GPU."""
 
-    def __init__(self, n: int, device: int = 0):
+    def __init__(self, n: int, device: int | None = None):
+        if device is None:  # the caller's current CUDA device (one process per GPU under torchrun)
+            try:
+                import torch
+
+                device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+            except ImportError:
+                device = 0
         self.lib = _lib.load()
         self.n = n
         h = ctypes.c_void_p()
