@@ -480,11 +480,20 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
           }
           p->hist_planned = true;
         }
-        const int level = p->N == 0 ? 0 : p->tiny_hist >= 0 ? p->tiny_hist : bp.hist_level;
-        if (level >= 1 && !bp.xhist)
-          SQOC_CUDA(cudaMalloc(&bp.xhist, bp.park_slots * p->N * bp.d * R * sizeof(double2)));
-        if (level >= 2 && !bp.chist)
-          SQOC_CUDA(cudaMalloc(&bp.chist, bp.park_slots * p->N * 4 * bp.d * bp.d * sizeof(double2)));
+        int level = p->N == 0 ? 0 : p->tiny_hist >= 0 ? p->tiny_hist : bp.hist_level;
+        // histories are an optimisation: if the device cannot hold them, run with less history
+        if (level >= 1 && !bp.xhist &&
+            cudaMalloc(&bp.xhist, bp.park_slots * p->N * bp.d * R * sizeof(double2)) != cudaSuccess) {
+          (void)cudaGetLastError();
+          bp.xhist = nullptr;
+          bp.hist_level = level = 0;
+        }
+        if (level >= 2 && !bp.chist &&
+            cudaMalloc(&bp.chist, bp.park_slots * p->N * 4 * bp.d * bp.d * sizeof(double2)) != cudaSuccess) {
+          (void)cudaGetLastError();
+          bp.chist = nullptr;
+          bp.hist_level = level = 1;
+        }
         tp.xhist = level >= 1 ? bp.xhist : nullptr;
         tp.chist = level >= 2 ? bp.chist : nullptr;
         p->last_tiny_hist = std::max(p->last_tiny_hist, level);
