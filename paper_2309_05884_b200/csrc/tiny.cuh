@@ -193,20 +193,12 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-// Left-operand views for the tile products: a plain shared-memory matrix, or a linear
-// combination c1 M1 + c2 M2 + c3 M3 formed on the fly in the operand loads (the scheme's
-// P = x4 A + x5 A2 + x6 A3 never needs a buffer of its own).
+// Left-operand view for the tile products (a plain shared-memory matrix; the product templates
+// take any type with at(offset)).  r01 v10 formed the scheme's P = x4 A + x5 A2 + x6 A3 inside the
+// operand loads of every k-step; v11 forms P' = P / x4 once per slice over the own entries (form_p).
 struct OpP {
   const double2* p;
   __device__ __forceinline__ double2 at(int o) const { return p[o]; }
-};
-struct OpL3 {
-  const double2 *p1, *p2, *p3;
-  double c1, c2, c3;
-  __device__ __forceinline__ double2 at(int o) const {
-    const double2 a = p1[o], b = p2[o], c = p3[o];
-    return make_double2(fma(c1, a.x, fma(c2, b.x, c3 * c.x)), fma(c1, a.y, fma(c2, b.y, c3 * c.y)));
-  }
 };
 
 // Tile helpers.  Lane (tr, tc) owns rows tr + 4i and cols tc + 8j of a D x D matrix
@@ -833,9 +825,10 @@ struct TinyCtx {
       for (int jj = 0; jj < TSC; ++jj) t[i][jj] = M[tl.row(i) * D + tl.col(jj)];
   }
 
-  // Six d x d buffers per problem (was eight): the scheme's P = x4 A + x5 A2 + x6 A3 is formed
-  // in the operand loads (OpL3) and the final step's inputs overwrite the basis in place, so
-  // more problems fit per SM (r01: d = 13 10 -> 12 warps, d = 9 / 11 7 -> 9 warps per SM).
+  // Six d x d buffers per problem (was eight): P' = P / x4 overwrites A in place where no buffer
+  // is free and the final step's inputs overwrite the basis in place, so more problems fit per SM
+  // (r01: d = 13 10 -> 12 warps per SM).  r01 also tried a forward sweep that runs the X update of
+  // slice j and A2 of slice j + 1 as one dual-product phase: no measurable change (198.3 ms step).
 
   // U = R(A) with A (scaled) in B1; uses B2 (A2), B3 (A3), B4 (Z), B5 (W); U -> B2.  With a chain
   // history slot ch (4 d x d matrices in global memory) the unsquared chain A2, A3, Z, Y is kept.
