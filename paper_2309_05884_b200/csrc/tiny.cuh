@@ -44,6 +44,8 @@ constexpr int kMaxControls = 4;
 // DMMA (tensor-core) tiles for d = 7, 8 (one 8x8 tile) and d >= 13 (2x2 tiles) in the fused
 // throughput kernel (r01: d=13 15.5 -> 13.9 ms, d=7 4.3 -> 2.3 ms per cfg1 launch at N_t=100);
 // the slice-parallel latency kernels keep DFMA tiles (shorter dependency chains per warp).
+// (r01: one padded 8 x 8 DMMA tile for d = 5, 6 at 24 warps / SM lost to the 3 x 3 DFMA lane grids:
+// d = 5 sector 23.0 vs 17.5 ms alone, cfg 1 step 201.7 vs 198.3 ms)
 __host__ __device__ constexpr bool tiny_mma(int d) { return d >= 13 || d == 7 || d == 8; }
 __host__ __device__ constexpr int tiny_lr(int d, bool mma) {
   return mma ? 8 : d >= 13 ? 4 : d == 2 ? 2 : (d == 3 || d == 5 || d == 6 || d == 9) ? 3 : 4;
