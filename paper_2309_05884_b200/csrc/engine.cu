@@ -437,14 +437,14 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
         const size_t smem = tiny_smem_bytes(bp.d, p->K, nw, false);
         const int grid_units = (warps_units + nw - 1) / nw;
         const int warps_b = (batch + pg - 1) / pg;
-        const int nw_b = std::max(1, std::min(bp.nwarps_max, warps_b));
-        const int grid_b = (warps_b + nw_b - 1) / nw_b;
+        const int nw_b = 1;  // one warp per CTA: room for the sweep's U_j prefetch ring
+        const int grid_b = warps_b;
         rc = gate ? launch_tiny<true>(bp.d, TK_SP_EXPM, sp, grid_units, nw, smem, bp.stream)
                   : launch_tiny<false>(bp.d, TK_SP_EXPM, sp, grid_units, nw, smem, bp.stream);
         if (rc == SQOC_OK) {
           TinySliceParams sp2 = sp;
           sp2.p.nwarps = nw_b;
-          const size_t smem_b = tiny_smem_bytes(bp.d, p->K, nw_b, false);
+          const size_t smem_b = tiny_sweep_smem_bytes(bp.d, p->K, nw_b);
           rc = gate ? launch_tiny<true>(bp.d, TK_SP_SWEEP, sp2, grid_b, nw_b, smem_b, bp.stream)
                     : launch_tiny<false>(bp.d, TK_SP_SWEEP, sp2, grid_b, nw_b, smem_b, bp.stream);
         }

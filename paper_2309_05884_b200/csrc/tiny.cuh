@@ -95,6 +95,7 @@ __host__ __device__ constexpr int tiny_fused_max_warps(int d) {
   return (d <= 4 || d == 7 || d == 8) ? 24 :  (d >= 9 && d <= 12) ? 8 : kTinyMaxWarps;
 }
 constexpr int kTinySliceParallelMaxBatch = 16;  // auto: slice-parallel latency path up to this batch
+constexpr int kSweepRing = 16;                  // slice-parallel sweep: U_j prefetch depth (d x d buffers)
 
 struct TinyParams {
   int K, N, batch;
@@ -1417,25 +1418,51 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_sweep_kernel(TinyS
   else c.copy_x(X, p.x0);
   __syncwarp();
   if (c.real) c.copy_x(Xh, X);
+  // U_j stream through a ring of kSweepRing d x d buffers (dynamic shared memory past the problem
+  // buffers; the sweep launches one warp per CTA) by cp.async, kSweepRing - 1 slices ahead: the
+  // sweep is a chain of tiny dependent products, so the global latency of every U_j read was its
+  // cost (r01: 195 us of the 259 us cfg 0 evaluation with one synchronous copy per slice).
+  constexpr int kRing = kSweepRing;
+  double2* ring_base = gen + (K + 1) * C::DD + (size_t)p.nwarps * C::PPW * C::STRIDE +
+                       (size_t)(warp * C::PPW + c.sub) * kRing * C::DD;
+  auto ring_at = [&](int i) { return ring_base + (size_t)(i % kRing) * C::DD; };
+#pragma unroll
+  for (int i = 0; i < kRing - 1; ++i) {
+    if (i < N) c.async_dd(ring_at(i), U + (size_t)i * C::DD);
+    cp_async_commit();
+  }
   for (int j = 0; j < N; ++j) {
-    c.copy_dd(c.B2, U + (size_t)j * C::DD);
+    cp_async_wait<kRing - 2>();  // U_j has landed
     __syncwarp();
-    c.mul_x(c.B2, false, X, X);
+    c.mul_x(ring_at(j), false, X, X);
     __syncwarp();
+    if (j + kRing - 1 < N) c.async_dd(ring_at(j + kRing - 1), U + (size_t)(j + kRing - 1) * C::DD);
+    cp_async_commit();
     if (c.real) c.copy_x(Xh + (size_t)(j + 1) * D * R, X);
   }
+  cp_async_wait<0>();
+  __syncwarp();
   const double2 tau = c.overlap(p.target, X);
   if (c.real && c.q == 0) p.tau_out[(size_t)prob * p.tau_stride] = tau;
   c.copy_x(L, p.target);
   __syncwarp();
   if (c.real) c.copy_x(Lh + (size_t)N * D * R, L);
-  for (int j = N - 1; j >= 0; --j) {
-    c.copy_dd(c.B2, U + (size_t)j * C::DD);
+#pragma unroll
+  for (int i = 0; i < kRing - 1; ++i) {
+    if (i < N) c.async_dd(ring_at(i), U + (size_t)(N - 1 - i) * C::DD);
+    cp_async_commit();
+  }
+  for (int i = 0; i < N; ++i) {  // slice j = N - 1 - i
+    const int j = N - 1 - i;
+    cp_async_wait<kRing - 2>();
     __syncwarp();
-    c.mul_x(c.B2, true, L, L);
+    c.mul_x(ring_at(i), true, L, L);
     __syncwarp();
+    if (i + kRing - 1 < N) c.async_dd(ring_at(i + kRing - 1), U + (size_t)(j - (kRing - 1)) * C::DD);
+    cp_async_commit();
     if (c.real) c.copy_x(Lh + (size_t)j * D * R, L);
   }
+  cp_async_wait<0>();
 }
 
 // phase 3: Frechet pair chain + traces for every (problem, slice)
@@ -1476,6 +1503,11 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_grad_kernel(TinySl
 inline size_t tiny_smem_bytes(int d, int K, int nwarps, bool mma) {
   const int ppw = 32 / tiny_lanes(d, mma);
   return sizeof(double2) * ((size_t)(K + 1) * d * d + (size_t)nwarps * ppw * tiny_stride(d, mma));
+}
+// the slice-parallel sweep kernel adds its U_j prefetch ring per problem
+inline size_t tiny_sweep_smem_bytes(int d, int K, int nwarps) {
+  const int ppw = 32 / tiny_lanes(d, false);
+  return tiny_smem_bytes(d, K, nwarps, false) + sizeof(double2) * (size_t)nwarps * ppw * kSweepRing * d * d;
 }
 
 }  // namespace sqoc
