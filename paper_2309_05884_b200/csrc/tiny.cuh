@@ -1089,6 +1089,19 @@ struct TinyCtx {
     }
   }
 
+  // x = Op(U) x for a state vector (R = 1), one row per lane (q < D): a dependent chain of D complex
+  // FMAs per lane instead of the tile layout's partial sums + shuffle reduction (the latency sweep)
+  __device__ __forceinline__ void mv_rows(const double2* U, bool adj, double2* x) const {
+    double2 acc = czero();
+    const bool mine = act && q < D;
+    if (mine) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) cfma(acc, adj ? cconj(U[k * D + q]) : U[q * D + k], x[k]);
+    }
+    __syncwarp();
+    if (mine) x[q] = acc;
+  }
+
   // copy a D x R matrix (own entries)
   __device__ __forceinline__ void copy_x(double2* dst, const double2* src) const {
     if (!act) return;
@@ -1434,7 +1447,8 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_sweep_kernel(TinyS
   for (int j = 0; j < N; ++j) {
     cp_async_wait<kRing - 2>();  // U_j has landed
     __syncwarp();
-    c.mul_x(ring_at(j), false, X, X);
+    if constexpr (GATE) c.mul_x(ring_at(j), false, X, X);
+    else c.mv_rows(ring_at(j), false, X);
     __syncwarp();
     if (j + kRing - 1 < N) c.async_dd(ring_at(j + kRing - 1), U + (size_t)(j + kRing - 1) * C::DD);
     cp_async_commit();
@@ -1456,7 +1470,8 @@ __global__ void __launch_bounds__(kTinyMaxWarps * 32) tiny_sp_sweep_kernel(TinyS
     const int j = N - 1 - i;
     cp_async_wait<kRing - 2>();
     __syncwarp();
-    c.mul_x(ring_at(i), true, L, L);
+    if constexpr (GATE) c.mul_x(ring_at(i), true, L, L);
+    else c.mv_rows(ring_at(i), true, L);
     __syncwarp();
     if (i + kRing - 1 < N) c.async_dd(ring_at(i + kRing - 1), U + (size_t)(j - (kRing - 1)) * C::DD);
     cp_async_commit();
