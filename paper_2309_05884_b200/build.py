@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             objs.append(obj)
             if not force and not _obj_stale(src, obj):
                 continue
-            cmd = [nvcc, *NVCC_FLAGS, "-c", "-o", obj, src]
+            cmd = [nvcc, *NVCC_FLAGS, *os.environ.get("SQOC_NVCC_EXTRA", "").split(), "-c", "-o", obj, src]
             if verbose:
                 print(" ".join(cmd), flush=True)
             procs.append(subprocess.Popen(cmd))

@@ -73,7 +73,15 @@ __device__ __forceinline__ void epi_store(const GemmItem& it, const GemmArgs& a,
   if (it.C2) it.C2[off] = c2;
 }
 
-constexpr int GBM = 64, GBN = 64, GBK = 8, GSTAGES = 4, GTHREADS = 128;
+// K depth per pipeline stage and stage count (build-time knobs; r01 cfg 2: GBK 8 x 4 stages 39.4 ms,
+// 16 x 3 stages (1 CTA / SM) 55.6 ms, 16 x 2 stages 39.5 ms)
+#ifndef SQOC_GBK
+#define SQOC_GBK 8
+#endif
+#ifndef SQOC_GSTAGES
+#define SQOC_GSTAGES 4
+#endif
+constexpr int GBM = 64, GBN = 64, GBK = SQOC_GBK, GSTAGES = SQOC_GSTAGES, GTHREADS = 128;
 constexpr int LD_KMAJ = GBK + 4;  // tiles stored [row][k]: ld = 12 (== 4 mod 8, conflict-free)
 constexpr int LD_NMAJ = GBM + 2;  // tiles stored [k][col]: ld = 66 (== 2 mod 8, conflict-free)
 constexpr int G_A_ELEMS = (GBM * LD_KMAJ > GBK * LD_NMAJ) ? GBM * LD_KMAJ : GBK * LD_NMAJ;  // 768 vs 528
@@ -292,7 +300,8 @@ __device__ __forceinline__ void g3_mainloop(double (&acc)[4][2][3][2], const Gem
   };
 #pragma unroll
   for (int s = 0; s < GSTAGES - 1; ++s) issue(s);
-  const bool half_tail = (it.k % GBK) != 0 && (it.k % GBK) <= 4;  // last K tile has one k-step
+  constexpr int KS = GBK / 4;                                      // k-steps per stage
+  const int last_steps = (it.k % GBK) ? ((it.k % GBK) + 3) / 4 : KS;  // a segment's last K tile
   int kin = 0;
   for (int kt = 0; kt < kt_total; ++kt) {
     cp_async_wait<GSTAGES - 2>();
@@ -301,13 +310,13 @@ __device__ __forceinline__ void g3_mainloop(double (&acc)[4][2][3][2], const Gem
     const int st = kt % GSTAGES;
     const double2* sA = sAbase + st * G_A_ELEMS;
     const double2* sB = sBbase + st * G_A_ELEMS;
-    const int ksteps = (half_tail && kin == kt_per_seg - 1) ? 1 : 2;
+    const int ksteps = (kin == kt_per_seg - 1) ? last_steps : KS;
     if (++kin == kt_per_seg) kin = 0;
     if constexpr (MC > 0 && NC > 0) {
     // both k-steps of a stage unrolled (loads of the second overlap the first's DMMAs); only the
     // segment's last stage may skip its all-zero second half
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
+    for (int ks = 0; ks < KS; ++ks) {
       if (ks >= ksteps) break;
       const int kk = ks * 4;
       double ar[MC], ai[MC], as[MC], br[NC], bi[NC], bs[NC];
