@@ -72,6 +72,7 @@ struct sqoc_problem {
   double* F_dev = nullptr;      // [max_batch]
   double* w_dev = nullptr;      // [nblocks]
   int* flag_dev = nullptr;      // non-finite flag
+  int* flag_host = nullptr;     // pinned copy (the read-back does not serialise the result copies)
   cudaEvent_t fork = nullptr;
   sqoc::LargeGroup* large = nullptr;  // all blocks with d > kTinyMaxDim, advanced together
   cudaStream_t large_stream = nullptr;
@@ -195,6 +196,7 @@ static void free_problem(sqoc_problem* p) {
   cudaFree(p->F_dev);
   cudaFree(p->w_dev);
   cudaFree(p->flag_dev);
+  cudaFreeHost(p->flag_host);
   if (p->fork) cudaEventDestroy(p->fork);
   if (p->large) {
     large_free(*p->large);
@@ -344,6 +346,7 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
     chk(cudaMalloc(&p->F_dev, max_batch * sizeof(double)), "cudaMalloc F");
     chk(cudaMalloc(&p->w_dev, n_blocks * sizeof(double)), "cudaMalloc w");
     chk(cudaMalloc(&p->flag_dev, sizeof(int)), "cudaMalloc flag");
+    chk(cudaMallocHost(&p->flag_host, sizeof(int)), "cudaMallocHost flag");
     if (rc == SQOC_OK) chk(cudaMemcpy(p->w_dev, w.data(), n_blocks * sizeof(double), cudaMemcpyHostToDevice), "copy w");
     chk(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming), "event");
     for (int b = 0; b < n_blocks; ++b) p->blocks[b].weight = w[b];
@@ -536,8 +539,8 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
     SQOC_CUDA(cudaGetLastError());
     p->launches += 1;
   }
-  int flag = 0;
-  SQOC_CUDA(cudaMemcpyAsync(&flag, p->flag_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
+  *p->flag_host = 0;
+  SQOC_CUDA(cudaMemcpyAsync(p->flag_host, p->flag_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (!dev) {
     if (F) SQOC_CUDA(cudaMemcpyAsync(F, F_dev, batch * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (grad && KN) SQOC_CUDA(cudaMemcpyAsync(grad, grad_dev, batch * KN * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -547,7 +550,7 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
     SQOC_CUDA(cudaMemcpyAsync(tau, p->tau_dev, (size_t)batch * p->nblocks * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   }
   SQOC_CUDA(cudaStreamSynchronize(st));
-  if (flag) return fail(SQOC_ERR_NONFINITE, "objective or gradient became non-finite");
+  if (*p->flag_host) return fail(SQOC_ERR_NONFINITE, "objective or gradient became non-finite");
   return SQOC_OK;
 }
 
