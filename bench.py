@@ -221,6 +221,8 @@ def run_ours(args):
         sub.initial = [s.initial[bdom_]] if s.initial else []
         sub.weights = np.array([s.block_weights()[bdom_]])
         eng1 = GrapeEngine(sub, max_batch=batch, device=local)
+        if len(s.blocks) > 1:
+            eng1.set_tiny_cta_warps(0)  # the CTA size the multi-block step launches it with
         eng1.evaluate_device(u.data_ptr(), batch, F.data_ptr(), g.data_ptr(), stream=stream.cuda_stream)
         alone = []
         for _ in range(max(2, args.steps)):

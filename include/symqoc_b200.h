@@ -108,6 +108,11 @@ int sqoc_last_tiny_schedule(const sqoc_problem* p);
 int sqoc_set_tiny_history(sqoc_problem* p, int mode);
 int sqoc_last_tiny_history(const sqoc_problem* p);
 
+/* Fused tiny kernel: warps per CTA.  -1 auto (default: 4-warp CTAs when the problem has a single
+ * tiny block -- several CTAs per SM, a shorter tail; one CTA filling an SM otherwise, which packs
+ * the concurrent block kernels best), 0 always full, > 0 a cap. */
+int sqoc_set_tiny_cta_warps(sqoc_problem* p, int warps);
+
 /* Propagator plan of the last large-block evaluation: Taylor degree of the product scheme
  * (12: 4 products, 18: 5 products), `squarings` squarings, and the number of
  * augmented-action terms (state-vector). */

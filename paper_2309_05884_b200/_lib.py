@@ -44,6 +44,7 @@ SIGNATURES = {
     "sqoc_last_tiny_schedule": (_I, [_P]),
     "sqoc_set_tiny_history": (_I, [_P, _I]),
     "sqoc_last_tiny_history": (_I, [_P]),
+    "sqoc_set_tiny_cta_warps": (_I, [_P, _I]),
     "sqoc_last_plan": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "sqoc_set_norm_bounds": (_I, [_P, _D]),
     "sqoc_chunk_product": (_I, [_P, _P, _P, _I, _P]),

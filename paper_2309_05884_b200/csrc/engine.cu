@@ -82,6 +82,7 @@ struct sqoc_problem {
   int tiny_mode = -1;  // -1 auto, 0 fused, 1 slice-parallel
   int last_tiny_mode = -1;
   int tiny_hist = -1;  // -1 auto, 0 off, 1 X history, 2 X + chain history
+  int tiny_cta = -1;   // fused-kernel warps per CTA: -1 auto, 0 full (one CTA fills an SM), > 0 cap
   int last_tiny_hist = -1;
   bool hist_planned = false;  // auto levels decided (once, from free memory)
   int launches = 0;
@@ -304,7 +305,8 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
       // SM-ms: SMs partly filled between CTAs), so the concurrent cfg 1 step slows to 212.9 ms.
       bp.nwarps_max = choose_nwarps(d, n_controls, 1 << 30, false);
       const int per_cta = pg * bp.nwarps;
-      bp.park_slots = (size_t)((max_batch + per_cta - 1) / per_cta) * per_cta;
+      // room for any CTA size up to per_cta (sqoc_set_tiny_cta_warps): the last CTA's padding slots
+      bp.park_slots = (size_t)((max_batch + per_cta - 1) / per_cta) * per_cta + per_cta;
       chk(cudaMalloc(&bp.park, bp.park_slots * 2 * d * R * sizeof(double2)), "cudaMalloc park");
     } else {
       LargeBlockSpec ls{};
@@ -457,7 +459,13 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
         p->launches += 3;
       } else {
         const int pg = 32 / tiny_lanes(bp.d, tiny_mma(bp.d));
-        int nw = std::max(1, std::min(bp.nwarps, (batch + pg - 1) / pg));
+        // auto: a problem with a single tiny block launches 4-warp CTAs (several per SM: a shorter
+        // tail -- r01 d = 13 alone 79.0 vs 90.7 ms); with several blocks one CTA fills an SM, which
+        // packs the concurrent sector kernels best (r01 cfg 1: 198 vs 213 ms with 4-warp CTAs)
+        int ntiny = 0;
+        for (auto& ob : p->blocks) ntiny += ob.tiny;
+        const int cap = p->tiny_cta > 0 ? p->tiny_cta : (p->tiny_cta == -1 && ntiny == 1) ? 4 : bp.nwarps;
+        int nw = std::max(1, std::min(std::min(bp.nwarps, cap), (batch + pg - 1) / pg));
         tp.nwarps = nw;
         if (!p->hist_planned) {
           // auto: X histories of all tiny blocks if they fit in 40% of free memory, then chain
@@ -704,6 +712,12 @@ int sqoc_set_tiny_history(sqoc_problem* p, int mode) {
 }
 
 int sqoc_last_tiny_history(const sqoc_problem* p) { return p ? p->last_tiny_hist : -1; }
+
+int sqoc_set_tiny_cta_warps(sqoc_problem* p, int warps) {
+  if (!p || warps < -1 || warps > 32) return fail(SQOC_ERR_ARG, "tiny CTA warps must be -1, 0 or 1..32");
+  p->tiny_cta = warps;
+  return SQOC_OK;
+}
 
 int sqoc_last_plan(const sqoc_problem* p, int* taylor_degree, int* squarings, int* action_terms) {
   if (!p || !taylor_degree || !squarings || !action_terms) return fail(SQOC_ERR_ARG, "NULL argument");

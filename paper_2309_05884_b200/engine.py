@@ -135,6 +135,10 @@ class GrapeEngine:
         'chain' (X and the propagator chain per slice)."""
         _lib.check(self.lib.sqoc_set_tiny_history(self.handle, self.TINY_HISTORY[mode]), "sqoc_set_tiny_history")
 
+    def set_tiny_cta_warps(self, warps: int) -> None:
+        """Fused tiny kernel warps per CTA: -1 auto, 0 full (one CTA per SM), > 0 a cap."""
+        _lib.check(self.lib.sqoc_set_tiny_cta_warps(self.handle, int(warps)), "sqoc_set_tiny_cta_warps")
+
     @property
     def last_tiny_history(self) -> str:
         return {-1: "none", 0: "off", 1: "x", 2: "chain"}[self.lib.sqoc_last_tiny_history(self.handle)]

@@ -191,3 +191,30 @@ def test_batched_device_lbfgs_improves_every_seed():
     assert bool(torch.all(res.F >= F0))
     assert res.history[-1] > res.history[0] + 1e-3
     assert all(b >= a - 1e-12 for a, b in zip(res.history, res.history[1:]))
+
+
+def test_tiny_cta_size_does_not_change_results():
+    """sqoc_set_tiny_cta_warps only regroups problems into CTAs: bit-identical F and gradient."""
+    import copy
+
+    import numpy as np
+
+    from paper_2309_05884_b200 import systems
+    from paper_2309_05884_b200.engine import GrapeEngine
+
+    multi = systems.config(1, n=8, n_slices=40)
+    single = copy.copy(multi)
+    single.blocks, single.targets = [multi.blocks[0]], [multi.targets[0]]
+    for s in (multi, single):
+        u = s.controls(11, batch=75)
+        eng = GrapeEngine(s, max_batch=75)
+        eng.set_tiny_schedule("fused")
+        ref = None
+        for w in (-1, 0, 3, 1):
+            eng.set_tiny_cta_warps(w)
+            F, g = eng.objective(u)
+            if ref is None:
+                ref = (F.copy(), g.copy())
+            else:
+                assert np.array_equal(F, ref[0]) and np.array_equal(g, ref[1])
+        eng.close()
