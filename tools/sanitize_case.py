@@ -13,6 +13,14 @@ from paper_2309_05884_b200.engine import GrapeEngine  # noqa: E402
 lib = _lib.load()
 s = systems.config(1, n=8, n_slices=6)          # S_n sectors d = 9, 7, 5, 3, 1 (tiny, gate)
 GrapeEngine(s, max_batch=3).objective(s.controls(0, batch=3))
+s = systems.config(1, n=12, n_slices=4)         # all S_12 sectors, fused kernel + chain-history backward
+GrapeEngine(s, max_batch=20).objective(s.controls(0, batch=20))
+from paper_2309_05884_b200 import gpu_basis  # noqa: E402
+
+gb = gpu_basis.GpuDnBasis(6)                    # on-GPU D_n basis + compression
+gb.blocks()
+gb.compress(systems.ring_heisenberg(6))
+gb.close()
 s = systems.config(0, n_slices=5)               # d = 13 state (tiny)
 GrapeEngine(s, max_batch=2).objective(s.controls(0, batch=2))
 for mults in (3, 4):
