@@ -23,3 +23,11 @@ x = torch.empty_like(u)
 print("H2D 65MB ms", wall(lambda: x.copy_(pin, non_blocking=True)))
 print("D2H 65MB ms", wall(lambda: gh.copy_(g, non_blocking=True)))
 print("device stream0 wall ms again", wall(lambda: eng.evaluate_device(u.data_ptr(), B, F.data_ptr(), g.data_ptr())))
+# host path emulated with torch copies around the device evaluation (same stream)
+ud = torch.empty_like(u); Fd = torch.empty_like(F); gd = torch.empty_like(g)
+def emul():
+    ud.copy_(pin, non_blocking=True)
+    eng.evaluate_device(ud.data_ptr(), B, Fd.data_ptr(), gd.data_ptr())
+    Fh.copy_(Fd, non_blocking=True); gh.copy_(gd, non_blocking=True)
+print("emulated host path wall ms", wall(emul))
+print("host wall ms again", wall(lambda: eng.evaluate_host_ptr(pin.data_ptr(), B, Fh.data_ptr(), gh.data_ptr())))
