@@ -71,3 +71,28 @@ def test_gpu_built_system_gives_same_objective():
     F2, g2 = e2.objective(u)
     assert np.abs(np.asarray(F1) - np.asarray(F2)).max() <= 1e-12
     assert np.abs(np.asarray(g1) - np.asarray(g2)).max() <= 1e-10 * np.abs(g1).max()
+
+
+def test_gpu_basis_odd_n15_against_host_and_n16_completeness():
+    """Beyond the reference's n <= 10: n = 15 (odd, no B irreps) matches the host restatement
+    column for column; n = 16 (the ABI maximum) spans the 65536-dim space with orthonormal columns."""
+    host = symmetry.dn_full_basis(15)
+    gb = gpu_basis.GpuDnBasis(15)
+    try:
+        dev = gb.blocks()
+        assert [b.label for b in dev] == [b.label for b in host]
+        assert [b.keys for b in dev] == [b.keys for b in host]
+        for bd, bh in zip(dev, host):
+            diff = abs(bd.columns - bh.columns)
+            assert (diff.max() if diff.nnz else 0.0) <= 1e-14
+    finally:
+        gb.close()
+    gb = gpu_basis.GpuDnBasis(16)
+    try:
+        assert sum(gb.dims) == 1 << 16
+        dev = gb.blocks()
+        for b in dev[:4] + dev[-2:]:
+            g = (b.columns.T @ b.columns).toarray()
+            assert np.abs(g - np.eye(b.dim)).max() <= 1e-13
+    finally:
+        gb.close()
