@@ -24,6 +24,8 @@ class OracleEngine:
         return F, g
 
 
+import scipy.optimize  # noqa: E402,F401  (imported before the timed regions: qoc imports it lazily)
+
 s = systems.config(0)
 u0 = s.controls(0)
 out = {"config": "cfg0: n=6 ring, A1 d=13, state transfer, N_t=100; 50 L-BFGS-B iterations"}
