@@ -297,6 +297,33 @@ struct Tile {
       for (int j = 0; j < TSC; ++j) m[j] = nm[j];
     }
   }
+  // t = L M^dag (the backward seed X Lam^dag), pipelined like mulL (r01 v12: the seed's plain
+  // k-loop was the hottest loop of the d = 11 kernel, short-scoreboard waits on its loads)
+  __device__ __forceinline__ void mul_bt(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
+    zero(t);
+    double2 l[TSR], m[TSC];
+#pragma unroll
+    for (int i = 0; i < TSR; ++i) l[i] = L[row(i) * D];
+#pragma unroll
+    for (int j = 0; j < TSC; ++j) m[j] = cconj(M[col(j) * D]);
+#pragma unroll 2
+    for (int k = 0; k < D; ++k) {
+      const int kn = k + 1 < D ? k + 1 : k;
+      double2 nl[TSR], nm[TSC];
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) nl[i] = L[row(i) * D + kn];
+#pragma unroll
+      for (int j = 0; j < TSC; ++j) nm[j] = cconj(M[col(j) * D + kn]);
+#pragma unroll
+      for (int i = 0; i < TSR; ++i)
+#pragma unroll
+        for (int j = 0; j < TSC; ++j) cfma(t[i][j], l[i], m[j]);
+#pragma unroll
+      for (int i = 0; i < TSR; ++i) l[i] = nl[i];
+#pragma unroll
+      for (int j = 0; j < TSC; ++j) m[j] = nm[j];
+    }
+  }
   // (t, dt) = (L, dL)(M, dM) = (L M, L dM + dL M)
   __device__ __forceinline__ void pair(double2 (&t)[TSR][TSC], double2 (&dt)[TSR][TSC], const double2* L,
                                        const double2* dL, const double2* M, const double2* dM) const {
@@ -1017,7 +1044,7 @@ struct TinyCtx {
   // Adot (B3) = 2^-s X Lam^dag with X in B0, Lam in B1 (D x R each)
   __device__ __forceinline__ void seed_c(int s) const {
     T2 t;
-    if constexpr (GATE && MMA) {
+    if constexpr (GATE && (MMA || D <= 9)) {  // r01: pipelined seed d = 9 63.8 -> 52.3 ms alone, d = 11 slower
       tl.mul_bt(t, B0, B1);
     } else {
       tl.zero(t);
