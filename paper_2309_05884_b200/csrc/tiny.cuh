@@ -298,7 +298,8 @@ struct Tile {
     }
   }
   // t = L M^dag (the backward seed X Lam^dag), pipelined like mulL (r01 v12: the seed's plain
-  // k-loop was the hottest loop of the d = 11 kernel, short-scoreboard waits on its loads)
+  // k-loop was the hottest loop of the d = 11 kernel, short-scoreboard waits on its loads; the
+  // pipelined form measured no faster there, d = 10..12 keep the plain loop)
   __device__ __forceinline__ void mul_bt(double2 (&t)[TSR][TSC], const double2* L, const double2* M) const {
     zero(t);
     double2 l[TSR], m[TSC];
@@ -1044,7 +1045,7 @@ struct TinyCtx {
   // Adot (B3) = 2^-s X Lam^dag with X in B0, Lam in B1 (D x R each)
   __device__ __forceinline__ void seed_c(int s) const {
     T2 t;
-    if constexpr (GATE && (MMA || D <= 9)) {  // r01: pipelined seed d = 9 63.8 -> 52.3 ms alone, d = 11 slower
+    if constexpr (GATE && (MMA || D <= 9)) {  // pipelined seed (no measurable change in the cfg 1 step)
       tl.mul_bt(t, B0, B1);
     } else {
       tl.zero(t);
