@@ -6,6 +6,7 @@ Prints, per sector d: launch ms (CUDA events, min of 3), problems resident per S
 SM-ms per problem (launch ms x 148 / batch, i.e. the machine share one problem costs when
 the sectors are packed concurrently), and SM-ms per problem / d^3.
 """
+import os
 import sys
 
 import numpy as np
@@ -26,6 +27,10 @@ for bi, blk in enumerate(full.blocks):
         continue
     s = systems.GrapeSystem(f"sector{blk.dim}", full.n_qubits, [blk], "gate", full.T, n_sl, [full.targets[bi]])
     eng = GrapeEngine(s, max_batch=batch)
+    # the CTA size the multi-sector step uses (a single-block engine would pick 4-warp CTAs);
+    # SECTOR_CTA=auto times the single-block default instead
+    if os.environ.get("SECTOR_CTA", "full") == "full":
+        eng.set_tiny_cta_warps(0)
     u = torch.from_numpy(s.controls(0, batch=batch)).cuda()
     F = torch.empty(batch, dtype=torch.float64, device="cuda")
     g = torch.empty_like(u)
