@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/symqoc_b200.h"
+#include "devonce.h"
 #include "large.cuh"
 #include "tiny.cuh"
 
@@ -118,18 +119,16 @@ enum TinyKernel { TK_FUSED = 0, TK_SP_EXPM = 1, TK_SP_SWEEP = 2, TK_SP_GRAD = 3 
 
 template <int D, bool GATE>
 static int launch_tiny_t(int which, const TinySliceParams& sp, int grid, int nwarps, size_t smem, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    SQOC_CUDA(cudaFuncSetAttribute(grape_tiny_kernel<D, GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kMaxSmem));
-    SQOC_CUDA(cudaFuncSetAttribute(tiny_sp_expm_kernel<D, GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kMaxSmem));
-    SQOC_CUDA(cudaFuncSetAttribute(tiny_sp_sweep_kernel<D, GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kMaxSmem));
-    SQOC_CUDA(cudaFuncSetAttribute(tiny_sp_grad_kernel<D, GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kMaxSmem));
-    attr_set = true;
-  }
+  static std::mutex mu;
+  static uint64_t done = 0;
+  SQOC_CUDA(once_per_device(mu, done, [] {
+    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e = cudaFuncSetAttribute(grape_tiny_kernel<D, GATE>, a, (int)kMaxSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tiny_sp_expm_kernel<D, GATE>, a, (int)kMaxSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tiny_sp_sweep_kernel<D, GATE>, a, (int)kMaxSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tiny_sp_grad_kernel<D, GATE>, a, (int)kMaxSmem);
+    return e;
+  }));
   switch (which) {
     case TK_FUSED: grape_tiny_kernel<D, GATE><<<grid, nwarps * 32, smem, st>>>(sp.p); break;
     case TK_SP_EXPM: tiny_sp_expm_kernel<D, GATE><<<grid, nwarps * 32, smem, st>>>(sp); break;

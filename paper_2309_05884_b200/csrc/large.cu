@@ -8,6 +8,7 @@
 #include <cstdlib>
 
 #include "../../include/symqoc_b200.h"
+#include "devonce.h"
 #include "large.cuh"
 #include "schemes.h"
 
@@ -395,15 +396,16 @@ int large_set_complex_gemm(int mults) {
 
 template <int TA, int TB, int EPI>
 static cudaError_t launch_gemm(const GemmItem* items, int n, int tiles, GemmArgs a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_kernel<TA, TB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static std::mutex mu;
+  static uint64_t done = 0;
+  cudaError_t e = once_per_device(mu, done, [] {
+    cudaError_t r = cudaFuncSetAttribute(zgemm_kernel<TA, TB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)G_SMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(zgemm3m_kernel<TA, TB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(zgemm3m_kernel<TA, TB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+    return r;
+  });
+  if (e != cudaSuccess) return e;
   if (use_3m()) zgemm3m_kernel<TA, TB, EPI><<<tiles, G3THREADS, G_SMEM, st>>>(items, n, a);
   else zgemm_kernel<TA, TB, EPI><<<tiles, GTHREADS, G_SMEM, st>>>(items, n, a);
   return cudaGetLastError();

@@ -65,7 +65,8 @@ def lbfgs_maximize(fun, u0: torch.Tensor, iterations: int = 50, history: int = 1
     Y = torch.zeros(history, B, n, dtype=dt, device=dev)
     rho = torch.zeros(history, B, dtype=dt, device=dev)
     valid = torch.zeros(history, B, dtype=torch.bool, device=dev)
-    res = BatchedResult(u=u, F=-fval, history=[float((-fval).mean())])
+    hist = [(-fval).mean()]  # device scalars: no host sync per iteration (converted at the end)
+    res = BatchedResult(u=u, F=-fval)
     for it in range(iterations):
         # two-loop recursion (per seed; invalid history slots contribute nothing)
         q = g.clone()
@@ -121,9 +122,12 @@ def lbfgs_maximize(fun, u0: torch.Tensor, iterations: int = 50, history: int = 1
         S[slot] = torch.where(good[:, None], s, S[slot])
         Y[slot] = torch.where(good[:, None], y, Y[slot])
         rho[slot] = torch.where(good, 1.0 / sy.clamp_min(1e-300), rho[slot])
-        valid[slot] = valid[slot] | good
+        # a rejected pair invalidates the slot: the pair left there from `history` iterations ago
+        # would otherwise be taken as the newest one (two-loop order, gamma scaling)
+        valid[slot] = good
         u, fval, g = u_new, f_new, g_new
-        res.history.append(float((-fval).mean()))
+        hist.append((-fval).mean())
+    res.history = torch.stack(hist).tolist()
     res.u = u.reshape(shape)
     res.F = -fval
     res.evaluations = evals

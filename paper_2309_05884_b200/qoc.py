@@ -12,7 +12,9 @@ Every evaluation goes through the C ABI; there is no CPU path here.
 
 from __future__ import annotations
 
+import hashlib
 import time
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -49,7 +51,38 @@ class _StateSystem:
         return np.ones(1)
 
 
-_ENGINE_CACHE: dict = {}
+_ENGINE_CACHE_MAX = 8
+_ENGINE_CACHE: OrderedDict = OrderedDict()  # content digest -> (inputs, engine), LRU order
+
+
+def _cached_engine(h0, hx, hy, psi0, psi_f, tau, n):
+    """Engine for exactly these matrices, states and grid.
+
+    The key is a digest of the CONTENTS (not ``id(backend)``: CPython reuses the ids of
+    collected temporaries, so an id key could hand back an engine built for other matrices);
+    a hit is confirmed with ``np.array_equal`` on the stored inputs.  Least-recently-used
+    engines beyond ``_ENGINE_CACHE_MAX`` are closed (their device memory freed) on eviction.
+    """
+    arrays = (h0, hx, hy, psi0, psi_f)
+    h = hashlib.blake2b(digest_size=20)
+    for a in arrays:
+        h.update(repr(a.shape).encode())
+        h.update(np.ascontiguousarray(a).tobytes())
+    h.update(np.float64(tau).tobytes())
+    h.update(np.int64(n).tobytes())
+    key = h.digest()
+    cache = _ENGINE_CACHE
+    hit = cache.get(key)
+    if hit is not None and all(np.array_equal(a, b) for a, b in zip(hit[0], arrays)):
+        cache.move_to_end(key)
+        return hit[1]
+    eng = GrapeEngine(_StateSystem(h0, hx, hy, psi0, psi_f, float(tau), n), max_batch=1)
+    cache[key] = (tuple(a.copy() for a in arrays), eng)
+    cache.move_to_end(key)
+    while len(cache) > _ENGINE_CACHE_MAX:
+        _, (_, old) = cache.popitem(last=False)
+        old.close()
+    return eng
 
 
 def _backend_h0(backend) -> np.ndarray:
@@ -77,13 +110,7 @@ def gradient(psi0, psi_f, bx, by, backend, tau):
     hy = np.asarray(backend.hy, dtype=np.complex128)
     if n == 0:  # empty grid: P = |<psi_f|psi_0>|^2 (test_qoc.py:43-50)
         return np.zeros(0), np.zeros(0), objective(psi0, psi_f)
-    key = (id(backend), float(tau), n, psi0.tobytes(), psi_f.tobytes())
-    eng = _ENGINE_CACHE.get(key)
-    if eng is None:
-        if len(_ENGINE_CACHE) > 16:
-            _ENGINE_CACHE.clear()
-        eng = GrapeEngine(_StateSystem(h0, hx, hy, psi0, psi_f, float(tau), n), max_batch=1)
-        _ENGINE_CACHE[key] = eng
+    eng = _cached_engine(h0, hx, hy, psi0, psi_f, float(tau), n)
     F, g = eng.objective(np.stack([bx, by]))
     return g[0].copy(), g[1].copy(), float(F)
 

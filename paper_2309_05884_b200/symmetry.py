@@ -19,8 +19,10 @@ identical:
   the reference at n=6,8,10 in ``tests/test_symmetry.py``).
 * D_n first block (bracelets) -- ``adjoint.build_bracelet_first_block``
   (``adjoint.py:99-148``), orbits sorted by (weight(min), min).
-* S_n full basis -- ``adjoint._cg_full_sn`` (``adjoint.py:151-195``): iterated
-  spin-1/2 Clebsch-Gordan coupling, multiplets stably sorted by descending 2J.
+* S_n spin sectors -- one multiplet per total spin J, in the reference's descending-J order
+  (``adjoint._cg_full_sn``, ``adjoint.py:151-195``), each built by the lowering-operator
+  ladder from a singlet-paired highest-weight vector (Condon-Shortley phases, so the
+  compressed blocks equal the reference's; ``sn_multiplet``).
 """
 
 from __future__ import annotations
@@ -194,56 +196,51 @@ def bracelet_block(n: int) -> BlockBasis:
 # --------------------------------------------------------------------------- S_n
 
 
-def sn_multiplets(n: int):
-    """Spin multiplets (2J, columns 2^n x (2J+1)) from iterated CG coupling.
+def _lower(v: np.ndarray, n: int) -> np.ndarray:
+    """S_- = sum_i sigma_i^- on a 2^n Fock vector (up = bit 0, site i <-> bit n - i)."""
+    x = np.arange(1 << n)
+    out = np.zeros_like(v)
+    for bit in range(n):
+        src = x[(x >> bit) & 1 == 0]  # spin up on this site -> flip it down
+        out[src | (1 << bit)] += v[src]
+    return out
 
-    Restates ``adjoint._cg_full_sn`` (adjoint.py:151-195): the J = j + 1/2 branch
-    precedes the J = j - 1/2 branch of every parent, and the final list is stably
-    sorted by descending 2J.  Columns run over 2M = 2J, 2J-2, ..., -2J.
+
+def sn_multiplet(n: int, two_j: int) -> np.ndarray:
+    """One spin-J multiplet |J, M>, 2M = 2J, 2J-2, ..., -2J, as 2^n x (2J+1) real columns.
+
+    Construction (lowering-operator ladder, Condon-Shortley phases): the highest-weight vector
+    is |up>^(2J) on the first 2J sites times a singlet (|ud> - |du>)/sqrt(2) on each remaining
+    site pair -- total spin J, M = J -- and |J, M-1> = S_- |J, M> / sqrt((J+M)(J-M+1)).
+    Every S_n-invariant operator and every global control compresses to the same matrix on any
+    multiplet of a given J with these phases, so the blocks equal the reference's CG-coupled
+    multiplets (adjoint.py:151-195; pinned by the ``sn12_d*`` goldens).
     """
-    up = np.array([1.0, 0.0])
-    down = np.array([0.0, 1.0])
-    mult = [(1, [up, down])]
-    for _ in range(n - 1):
-        nxt = []
-        for two_j, vecs in mult:
-            norm = 2.0 * (two_j + 1)
-            plus = []
-            for idx in range(two_j + 2):
-                two_m = two_j + 1 - 2 * idx
-                v = np.zeros(2 * vecs[0].shape[0])
-                if idx <= two_j:
-                    v += math.sqrt((two_j + two_m + 1) / norm) * np.kron(vecs[idx], up)
-                if idx >= 1:
-                    v += math.sqrt((two_j - two_m + 1) / norm) * np.kron(vecs[idx - 1], down)
-                plus.append(v)
-            nxt.append((two_j + 1, plus))
-            if two_j >= 1:
-                minus = []
-                for idx in range(two_j):
-                    two_m = two_j - 1 - 2 * idx
-                    v = -math.sqrt((two_j - two_m + 1) / norm) * np.kron(vecs[idx + 1], up)
-                    v += math.sqrt((two_j + two_m + 1) / norm) * np.kron(vecs[idx], down)
-                    minus.append(v)
-                nxt.append((two_j - 1, minus))
-        mult = nxt
-    mult.sort(key=lambda t: -t[0])
-    return [(tj, np.column_stack(v)) for tj, v in mult]
+    if (n - two_j) % 2 or not 0 <= two_j <= n:
+        raise ValueError(f"no spin 2J={two_j} multiplet for n={n}")
+    pairs = (n - two_j) // 2
+    v = np.zeros(1 << n)
+    v[0] = 1.0  # all up
+    for p in range(pairs):  # singlet on sites (2J + 2p + 1, 2J + 2p + 2)
+        a, b = n - (two_j + 2 * p + 1), n - (two_j + 2 * p + 2)  # their bits
+        w = np.zeros_like(v)
+        nz = np.nonzero(v)[0]
+        w[nz | (1 << b)] += v[nz] / math.sqrt(2.0)
+        w[nz | (1 << a)] -= v[nz] / math.sqrt(2.0)
+        v = w
+    cols = [v]
+    for k in range(two_j):  # 2M = 2J - 2k  ->  2J - 2k - 2
+        two_m = two_j - 2 * k
+        c = math.sqrt((two_j + two_m) * (two_j - two_m + 2)) / 2.0  # sqrt((J+M)(J-M+1))
+        cols.append(_lower(cols[-1], n) / c)
+    return np.column_stack(cols)
 
 
 def sn_sector_blocks(n: int):
-    """One representative block per total spin J (first multiplet of that 2J).
-
-    Returns blocks ordered by descending J, i.e. the reference's multiplet order
-    with duplicates of a J dropped (same-J multiplets give identical compressed
-    matrices for S_n-invariant Hamiltonians).
-    """
-    seen = set()
+    """One block per total spin J, ordered by descending J (the reference's multiplet order,
+    adjoint.py:186, with the identical same-J multiplets dropped: S_n-invariant Hamiltonians
+    compress identically on each of them)."""
     blocks = []
-    for two_j, cols in sn_multiplets(n):
-        if two_j in seen:
-            continue
-        seen.add(two_j)
-        label = f"J={two_j / 2:g}"
-        blocks.append(BlockBasis(label, sp.csc_matrix(cols), [two_j]))
+    for two_j in range(n, -1, -2):
+        blocks.append(BlockBasis(f"J={two_j / 2:g}", sp.csc_matrix(sn_multiplet(n, two_j)), [two_j]))
     return blocks

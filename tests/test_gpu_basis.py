@@ -1,9 +1,12 @@
-"""On-GPU D_n basis construction and compression against the host restatement.
+"""On-GPU D_n basis construction and compression against the host restatement
+and the reference.
 
 The host restatement (symmetry.dn_full_basis) is pinned to the reference's own
-adjoint._dn_full_projected at n = 6, 8, 10 in tests/test_symmetry.py; here the GPU
-builder must give the same blocks in the same order with the same column order
-(bit-exact keys) and the same column values / compressed generators to rounding.
+adjoint._dn_full_projected: block sizes at n = 6, 8, 10 and every column at n = 8, 10
+(tests/test_symmetry.py, fixture tests/golden/r02_adjoint.npz).  Here the GPU builder must
+give the same blocks in the same order with the same column order (bit-exact keys) and the
+same column values / compressed generators to rounding -- and, at n = 8, 10, the reference's
+columns directly.
 """
 
 import time
@@ -40,6 +43,26 @@ def test_gpu_basis_matches_host_restatement(n):
             for m, bh in zip(mats, host):
                 ref = bh.compress(full)
                 assert np.abs(m - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+    finally:
+        gb.close()
+
+
+@pytest.mark.parametrize("n", [8, 10])
+def test_gpu_basis_columns_match_reference(n):
+    """GPU-built columns against the reference's build_full_adjoint(n, 'dn') (adjoint.py:198-220)."""
+    import os
+
+    import scipy.sparse as sp
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "r02_adjoint.npz"))
+    dim = 1 << n
+    ref = sp.csc_matrix((z[f"dn{n}_data"], z[f"dn{n}_indices"], z[f"dn{n}_indptr"]), shape=(dim, dim)).toarray()
+    gb = gpu_basis.GpuDnBasis(n)
+    try:
+        dev = gb.blocks()
+        assert [b.dim for b in dev] == list(z[f"dn{n}_sizes"])
+        ours = np.hstack([b.columns.toarray() for b in dev])
+        assert np.abs(ours - ref).max() <= 1e-14
     finally:
         gb.close()
 

@@ -69,3 +69,25 @@ def test_state_dtau_consistent_with_state_gradient(golden):
     grad = 2 * np.real(np.conj(o) * dtau)
     np.testing.assert_allclose(grad[0], gx, atol=1e-12)
     np.testing.assert_allclose(grad[1], gy, atol=1e-12)
+
+
+def test_r02_cfg1_fixture_reproduces_with_current_systems():
+    """The cfg 1 fixture (tests/golden/make_fixtures_r02.py) is reproducible from the current host
+    systems: same inputs (checksum) and the same oracle output on its first row."""
+    import os
+
+    from paper_2309_05884_b200 import systems
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "r02_cfg1.npz"))
+    s = systems.config(1)
+    ub = s.controls(0, batch=4096)
+    rows = list(z["cfg1_rows"])
+    chk = []
+    for a in (ub[rows], *s.targets, *[b.h0 for b in s.blocks]):
+        a = np.asarray(a).astype(np.complex128).ravel()
+        w = np.arange(1, a.size + 1, dtype=np.float64)
+        chk += [a.sum(), (w * a).sum() / a.size]
+    np.testing.assert_allclose(np.array(chk), z["cfg1_check"], rtol=1e-10, atol=1e-12)
+    F, g, _ = O.objective(s, ub[rows[0]])
+    assert abs(F - z["cfg1_F"][0]) <= 1e-12
+    assert np.abs(g - z["cfg1_grad"][0]).max() <= 1e-10 * np.abs(g).max()

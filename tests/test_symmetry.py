@@ -78,3 +78,51 @@ def test_pauli_term_encoding_for_gpu_compression():
                 par = bin(x & int(sg)).count("1") & 1
                 dense[x ^ int(f), x] += (cr + 1j * ci) * (-1.0 if par else 1.0)
         assert np.abs(dense - pauli.realize(op).toarray()).max() <= 1e-15
+
+
+def _reference_adjoint(n):
+    """Reference ``build_full_adjoint(n, 'dn')`` columns (tests/golden/make_fixtures_r02.py)."""
+    import os
+
+    import scipy.sparse as sp
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "r02_adjoint.npz"))
+    dim = 1 << n
+    m = sp.csc_matrix((z[f"dn{n}_data"], z[f"dn{n}_indices"], z[f"dn{n}_indptr"]), shape=(dim, dim))
+    return m.toarray(), list(z[f"dn{n}_sizes"])
+
+
+@pytest.mark.parametrize("n", [8, 10])
+def test_dn_columns_match_reference(n):
+    """Block order AND column order/values of the full D_n basis equal the reference's
+    (adjoint.py:198-220; the indexing contract), not just the sizes."""
+    ref, sizes = _reference_adjoint(n)
+    blocks = symmetry.dn_full_basis(n)
+    assert [b.dim for b in blocks] == sizes
+    ours = np.hstack([b.columns.toarray() for b in blocks])
+    assert np.abs(ours - ref).max() <= 1e-14
+    # the generating Fock index of each column is its smallest-(weight, index) support state
+    s = 0
+    for b in blocks:
+        for c, key in enumerate(b.keys):
+            assert ref[key[1], s + c] != 0.0
+        s += b.dim
+
+
+def test_sn_multiplets_are_spin_eigenvectors():
+    """sn_multiplet columns: orthonormal, S_z = M, S^2 = J(J+1) (n = 8, every J)."""
+    n = 8
+    sz = np.array([(n - 2 * bin(x).count("1")) / 2 for x in range(1 << n)])
+    hx, hy = (pauli.realize(o).toarray() for o in systems.global_controls(n))
+    sx, sy = hx / 2, hy / 2
+    szm = np.diag(sz)
+    s2 = sx @ sx + sy @ sy + szm @ szm
+    for two_j in range(n, -1, -2):
+        cols = symmetry.sn_multiplet(n, two_j)
+        assert np.abs(cols.T @ cols - np.eye(two_j + 1)).max() <= 1e-13
+        j = two_j / 2
+        for k in range(two_j + 1):
+            m = j - k
+            v = cols[:, k]
+            assert np.abs(sz * v - m * v).max() <= 1e-13
+            assert np.abs(s2 @ v - j * (j + 1) * v).max() <= 1e-12
