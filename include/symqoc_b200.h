@@ -154,6 +154,14 @@ int sqoc_state_gradient(int device, int d, const double* h0, const double* hx, c
 int sqoc_set_timing(sqoc_problem* p, int on);
 int sqoc_block_time_ms(const sqoc_problem* p, int block, double* ms);
 
+/* Large-block GEMMs of the last sqoc_eval: device time of their launches (summed CUDA-event
+ * pairs around every GEMM launch on the launching stream; 0 unless sqoc_set_timing was on),
+ * complex multiply-adds issued (sum m n k over the work lists; tile padding not counted) and
+ * the number of GEMM launches.  The DMMA pipe executes sqoc_complex_gemm_mults() real FMAs
+ * (3 for Gauss/3M, 4 for 4M) per complex MAC. */
+int sqoc_last_gemm_stats(sqoc_problem* p, double* gemm_ms, double* complex_macs, int* launches);
+int sqoc_complex_gemm_mults(void);
+
 /* Device kernel launches issued by the last sqoc_eval on this problem. */
 int sqoc_last_launch_count(const sqoc_problem* p);
 

@@ -734,8 +734,27 @@ int sqoc_set_complex_gemm(int mults) {
 int sqoc_set_timing(sqoc_problem* p, int on) {
   if (!p) return fail(SQOC_ERR_ARG, "problem is NULL");
   p->timing = on != 0;
+  if (p->large) p->large->timing = p->timing;
   return SQOC_OK;
 }
+
+int sqoc_last_gemm_stats(sqoc_problem* p, double* gemm_ms, double* complex_macs, int* launches) {
+  if (!p || !gemm_ms || !complex_macs || !launches) return fail(SQOC_ERR_ARG, "NULL argument");
+  *gemm_ms = 0.0;
+  *complex_macs = 0.0;
+  *launches = 0;
+  if (!p->large) return SQOC_OK;
+  SQOC_CUDA(cudaSetDevice(p->device));
+  *complex_macs = p->large->gemm_macs;
+  *launches = p->large->gemm_launches;
+  if (p->large->timing) {
+    int rc = large_gemm_time(*p->large, gemm_ms);
+    if (rc != SQOC_OK) return fail(rc, p->large->err);
+  }
+  return SQOC_OK;
+}
+
+int sqoc_complex_gemm_mults(void) { return large_complex_mults(); }
 
 int sqoc_block_time_ms(const sqoc_problem* p, int block, double* ms) {
   if (!p || !ms || block < 0 || block >= p->nblocks) return fail(SQOC_ERR_ARG, "bad block index");

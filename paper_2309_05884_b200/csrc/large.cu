@@ -376,6 +376,15 @@ __global__ void sv_dot_kernel(int K, int N, int nblk, const int* __restrict__ di
   if (threadIdx.x < K) g[((size_t)i * nblk + b) * K + threadIdx.x] = red[threadIdx.x][0];
 }
 
+#define LCHK(x)                                                  \
+  do {                                                           \
+    cudaError_t e_ = (x);                                        \
+    if (e_ != cudaSuccess) {                                     \
+      g.err = std::string(#x) + ": " + cudaGetErrorString(e_);   \
+      return SQOC_ERR_CUDA;                                      \
+    }                                                            \
+  } while (0)
+
 // ------------------------------------------------------------------ host side
 // Complex product algorithm for the large path: 3M (Gauss, 3 DMMAs per complex k-step) by
 // default, 4M with SQOC_GEMM_4M=1 in the environment (checked once per process).
@@ -387,6 +396,8 @@ static bool use_3m() {
   }
   return g_gemm_mode == 3;
 }
+
+int large_complex_mults() { return use_3m() ? 3 : 4; }
 
 int large_set_complex_gemm(int mults) {
   if (mults != 3 && mults != 4) return SQOC_ERR_ARG;
@@ -411,9 +422,57 @@ static cudaError_t launch_gemm(const GemmItem* items, int n, int tiles, GemmArgs
   return cudaGetLastError();
 }
 
-enum Op { F_STEP, F_S, F_X, B_C, B_STEP, B_S, B_D, B_XL };
-
 static int tiles_of(int m, int n) { return ((m + GBM - 1) / GBM) * ((n + GBN - 1) / GBN); }
+
+// GEMM timing / accounting around every launch (event pairs only when g.timing is on)
+static void gemm_begin(LargeGroup& g, const ListRef& l, cudaStream_t st) {
+  g.gemm_macs += l.macs;
+  g.gemm_launches++;
+  if (!g.timing) return;
+  while (g.tev.size() < g.tev_used + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    g.tev.push_back(e);
+  }
+  cudaEventRecord(g.tev[g.tev_used], st);
+}
+static void gemm_end(LargeGroup& g, cudaStream_t st) {
+  if (!g.timing || g.tev.size() < g.tev_used + 2) return;
+  cudaEventRecord(g.tev[g.tev_used + 1], st);
+  g.tev_used += 2;
+}
+
+int large_gemm_time(LargeGroup& g, double* ms) {
+  double t = 0.0;
+  for (size_t i = 0; i + 1 < g.tev_used; i += 2) {
+    float x = 0.f;
+    LCHK(cudaEventElapsedTime(&x, g.tev[i], g.tev[i + 1]));
+    t += x;
+  }
+  *ms = t;
+  return SQOC_OK;
+}
+
+static ListRef upload_list(std::vector<GemmItem>& v, std::vector<void*>& mem) {
+  ListRef ref;
+  int t = 0;
+  for (auto& x : v) {
+    x.tile_start = t;
+    t += tiles_of(x.m, x.n);
+    ref.macs += (double)x.m * x.n * x.k * x.nseg;
+  }
+  if (v.empty()) return ref;
+  if (cudaMalloc(&ref.dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return ListRef{};
+  cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
+  ref.n = (int)v.size();
+  ref.tiles = t;
+  mem.push_back(ref.dev);
+  return ref;
+}
+
+// Sequential schedule ops.  Gate objective: B_UC = [M = U^dag Ad | trace Tr(U^dag dT E_k)] in one
+// launch, B_CU: Ad = M U.  State objective: B_C, B_D, B_XL (vector X / Lam).
+enum Op { F_STEP, F_S, F_X, B_C, B_STEP, B_S, B_D, B_XL, B_UC, B_CU };
 
 static GemmItem mk(const double2* A0, const double2* B0, const double2* A1, const double2* B1, double2* C,
                    const double2* E0, const double2* E1, int m, int n, int k, int nseg, int lda, int ldb, int ldc,
@@ -455,99 +514,88 @@ static void push_step(std::vector<GemmItem>& v, const PolyScheme& sc, int k, int
 }
 
 // Sequential schedule lists.  F_STEP / B_STEP: p = step index, q = scheme degree.
-static std::pair<GemmItem*, int> get_list(LargeGroup& g, int op, int p, int q, int r, int* tiles_out) {
+static ListRef get_list(LargeGroup& g, int op, int p, int q, int r) {
   auto key = std::make_tuple(op, p, q, r);
   auto found = g.lists.find(key);
+  if (found != g.lists.end()) return found->second;
   std::vector<GemmItem> v;
-  if (found == g.lists.end()) {
-    for (int b = 0; b < g.nblk; ++b) {
-      const int d = g.blocks[b].d, R = g.gate ? d : 1;
-      const size_t o = g.off[b], orr = g.offr[b];
-      double2 *Ad = g.Ad + o;
-      double2 *Tp = g.T[p] + o, *Tn = g.T[1 - p] + o, *dTp = g.dT[p] + o, *dTn = g.dT[1 - p] + o;
-      double2 *Xq = g.X[q] + orr, *Xn = g.X[1 - q] + orr, *Lr = g.L[r] + orr, *Ln = g.L[1 - r] + orr;
-      auto slot = [&](int c) -> double2* {
-        switch (c) {
-          case 0: return g.A + o;
-          case 1: return g.A2 + o;
-          case 2: return g.A3 + o;
-          case kSlotY: return g.T[0] + o;
-          default: return g.xs[c - 3] + o;
-        }
-      };
-      auto dslot = [&](int c) -> double2* {
-        switch (c) {
-          case 0: return g.Ad + o;
-          case 1: return g.dA2 + o;
-          case 2: return g.dA3 + o;
-          case kSlotY: return g.dT[0] + o;
-          default: return g.dxs[c - 3] + o;
-        }
-      };
-      switch (op) {
-        case F_STEP: push_step(v, scheme_of(q), p, d, slot, dslot, true, false); break;
-        case B_STEP: push_step(v, scheme_of(q), p, d, slot, dslot, true, true); break;
-        case F_S: v.push_back(mk(Tp, Tp, 0, 0, Tn, 0, 0, d, d, d, 1, d, d, d, 0)); break;
-        case F_X: v.push_back(mk(Tp, Xq, 0, 0, Xn, 0, 0, d, R, d, 1, d, R, R, 0)); break;
-        case B_C: v.push_back(mk(Xq, Lr, 0, 0, Ad, 0, 0, d, d, R, 1, R, R, d, 0)); break;
-        case B_S:
-          v.push_back(mk(Tp, Tp, 0, 0, Tn, 0, 0, d, d, d, 1, d, d, d, 0));
-          v.push_back(mk(Tp, dTp, dTp, Tp, dTn, 0, 0, d, d, d, 2, d, d, d, 0));
-          break;
-        case B_D: {
-          GemmItem it = mk(Tp, dTp, 0, 0, nullptr, 0, 0, d, d, d, 1, d, d, d, 0);
-          it.F = g.blocks[b].gen + (size_t)d * d;
-          it.fstride = (long)d * d;
-          it.nF = g.K;
-          it.tr_out = g.trace_part + (size_t)g.trace_tile_off[b] * g.K;
-          v.push_back(it);
-          break;
-        }
-        case B_XL:
-          v.push_back(mk(Tp, Xq, 0, 0, Xn, 0, 0, d, R, d, 1, d, R, R, 0));
-          v.push_back(mk(Tp, Lr, 0, 0, Ln, 0, 0, d, R, d, 1, d, R, R, 0));
-          break;
+  for (int b = 0; b < g.nblk; ++b) {
+    const int d = g.blocks[b].d, R = g.gate ? d : 1;
+    const size_t o = g.off[b], orr = g.offr[b];
+    double2* Ad = g.Ad + o;
+    double2 *Tp = g.T[p] + o, *Tn = g.T[1 - p] + o, *dTp = g.dT[p] + o, *dTn = g.dT[1 - p] + o;
+    double2 *Xq = g.X[q] + orr, *Xn = g.X[1 - q] + orr, *Lr = g.L[r] + orr, *Ln = g.L[1 - r] + orr;
+    auto slot = [&](int c) -> double2* {
+      switch (c) {
+        case 0: return g.A + o;
+        case 1: return g.A2 + o;
+        case 2: return g.A3 + o;
+        case kSlotY: return g.T[0] + o;
+        default: return g.xs[c - 3] + o;
       }
+    };
+    auto dslot = [&](int c) -> double2* {
+      switch (c) {
+        case 0: return g.Ad + o;
+        case 1: return g.dA2 + o;
+        case 2: return g.dA3 + o;
+        case kSlotY: return g.dT[0] + o;
+        default: return g.dxs[c - 3] + o;
+      }
+    };
+    auto trace_item = [&]() {
+      GemmItem it = mk(Tp, dTp, 0, 0, nullptr, 0, 0, d, d, d, 1, d, d, d, 0);
+      it.F = g.blocks[b].gen + (size_t)d * d;
+      it.fstride = (long)d * d;
+      it.nF = g.K;
+      it.tr_out = g.trace_part + (size_t)g.trace_tile_off[b] * g.K;
+      return it;
+    };
+    switch (op) {
+      case F_STEP: push_step(v, scheme_of(q), p, d, slot, dslot, true, false); break;
+      case B_STEP: push_step(v, scheme_of(q), p, d, slot, dslot, true, true); break;
+      case F_S: v.push_back(mk(Tp, Tp, 0, 0, Tn, 0, 0, d, d, d, 1, d, d, d, 0)); break;
+      case F_X: v.push_back(mk(Tp, Xq, 0, 0, Xn, 0, 0, d, R, d, 1, d, R, R, 0)); break;
+      case B_C: v.push_back(mk(Xq, Lr, 0, 0, Ad, 0, 0, d, d, R, 1, R, R, d, 0)); break;
+      case B_S:
+        v.push_back(mk(Tp, Tp, 0, 0, Tn, 0, 0, d, d, d, 1, d, d, d, 0));
+        v.push_back(mk(Tp, dTp, dTp, Tp, dTn, 0, 0, d, d, d, 2, d, d, d, 0));
+        break;
+      case B_D: v.push_back(trace_item()); break;
+      case B_XL:
+        v.push_back(mk(Tp, Xq, 0, 0, Xn, 0, 0, d, R, d, 1, d, R, R, 0));
+        v.push_back(mk(Tp, Lr, 0, 0, Ln, 0, 0, d, R, d, 1, d, R, R, 0));
+        break;
+      case B_UC:  // gate: M (in X[0]) = U^dag Ad, and the trace item
+        v.push_back(mk(Tp, Ad, 0, 0, g.X[0] + orr, 0, 0, d, d, d, 1, d, d, d, 0));
+        v.push_back(trace_item());
+        break;
+      case B_CU:  // gate: Ad = M U
+        v.push_back(mk(g.X[0] + orr, Tp, 0, 0, Ad, 0, 0, d, d, d, 1, d, d, d, 0));
+        break;
     }
-    int t = 0;
-    for (auto& it : v) {
-      it.tile_start = t;
-      t += tiles_of(it.m, it.n);
-    }
-    GemmItem* dev = nullptr;
-    if (cudaMalloc(&dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return {nullptr, 0};
-    cudaMemcpy(dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
-    g.list_mem.push_back(dev);
-    found = g.lists.emplace(key, std::make_pair(dev, (int)v.size())).first;
-    g.list_tiles[key] = t;
   }
-  *tiles_out = g.list_tiles[key];
-  return found->second;
+  ListRef ref = upload_list(v, g.list_mem);
+  if (ref.dev) g.lists.emplace(key, ref);
+  return ref;
 }
 
-#define LCHK(x)                                                  \
-  do {                                                           \
-    cudaError_t e_ = (x);                                        \
-    if (e_ != cudaSuccess) {                                     \
-      g.err = std::string(#x) + ": " + cudaGetErrorString(e_);   \
-      return SQOC_ERR_CUDA;                                      \
-    }                                                            \
-  } while (0)
-
 static int gemm(LargeGroup& g, int op, int p, int q, int r, GemmArgs a, cudaStream_t st) {
-  int tiles = 0;
-  auto lst = get_list(g, op, p, q, r, &tiles);
-  if (!lst.first) {
+  ListRef l = get_list(g, op, p, q, r);
+  if (!l.dev) {
     g.err = "work list allocation failed";
     return SQOC_ERR_CUDA;
   }
+  gemm_begin(g, l, st);
   cudaError_t e;
   switch (op) {
-    case B_C: e = launch_gemm<OP_N, OP_C, EPI_STORE>(lst.first, lst.second, tiles, a, st); break;
-    case B_D: e = launch_gemm<OP_C, OP_N, EPI_TRACE>(lst.first, lst.second, tiles, a, st); break;
-    case B_XL: e = launch_gemm<OP_C, OP_N, EPI_STORE>(lst.first, lst.second, tiles, a, st); break;
-    default: e = launch_gemm<OP_N, OP_N, EPI_STORE>(lst.first, lst.second, tiles, a, st); break;
+    case B_C: e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.n, l.tiles, a, st); break;
+    case B_D: e = launch_gemm<OP_C, OP_N, EPI_TRACE>(l.dev, l.n, l.tiles, a, st); break;
+    case B_XL: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st); break;
+    case B_UC: e = launch_gemm<OP_C, OP_N, EPI_MIXED>(l.dev, l.n, l.tiles, a, st); break;
+    default: e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st); break;
   }
+  gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
     return SQOC_ERR_CUDA;
@@ -697,7 +745,8 @@ void large_free(LargeGroup& g) {
   for (auto m : g.list_mem) cudaFree(m);
   g.list_mem.clear();
   g.lists.clear();
-  g.list_tiles.clear();
+  for (auto e : g.tev) cudaEventDestroy(e);
+  g.tev.clear();
 }
 
 // ------------------------------------------------------------------ boundary conditions
@@ -815,18 +864,8 @@ static ListRef hist_list(LargeGroup& g, int op, int idx, int p, int i0, int i1) 
         }
       }
     }
-  int t = 0;
-  for (auto& x : v) {
-    x.tile_start = t;
-    t += tiles_of(x.m, x.n);
-  }
-  ListRef ref;
-  if (cudaMalloc(&ref.dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return ListRef{};
-  cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
-  ref.n = (int)v.size();
-  ref.tiles = t;
-  g.hlist_mem.push_back(ref.dev);
-  g.hlists[key] = ref;
+  ListRef ref = upload_list(v, g.hlist_mem);
+  if (ref.dev) g.hlists[key] = ref;
   return ref;
 }
 
@@ -837,9 +876,11 @@ static int hgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArgs
     return SQOC_ERR_CUDA;
   }
   cudaError_t e;
+  gemm_begin(g, l, st);
   if (op == H_L) e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
   else if (op == H_B) e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
   else e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
+  gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
     return SQOC_ERR_CUDA;
@@ -905,22 +946,8 @@ static ListRef scan_list(LargeGroup& g, int op, int idx, int Lc, int C) {
         break;
     }
   }
-  int t = 0;
-  for (auto& x : v) {
-    x.tile_start = t;
-    t += tiles_of(x.m, x.n);
-  }
-  ListRef ref;
-  if (v.empty()) {
-    g.hlists[key] = ref;
-    return ref;
-  }
-  if (cudaMalloc(&ref.dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return ListRef{};
-  cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
-  ref.n = (int)v.size();
-  ref.tiles = t;
-  g.hlist_mem.push_back(ref.dev);
-  g.hlists[key] = ref;
+  ListRef ref = upload_list(v, g.hlist_mem);
+  if (ref.dev || v.empty()) g.hlists[key] = ref;
   return ref;
 }
 
@@ -928,8 +955,10 @@ static int scan_gemm(LargeGroup& g, int op, int idx, int Lc, int C, cudaStream_t
   ListRef l = scan_list(g, op, idx, Lc, C);
   if (!l.n) return SQOC_OK;
   const GemmArgs one{1.0, 0.0, 0.0, 0.0};
+  gemm_begin(g, l, st);
   cudaError_t e = (op == H_LP1) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, one, st)
                                 : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, one, st);
+  gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
     return SQOC_ERR_CUDA;
@@ -1085,18 +1114,8 @@ static ListRef sv_list(LargeGroup& g, int op, int idx, int p, int i0, int i1) {
         }
       }
   }
-  int t = 0;
-  for (auto& x : v) {
-    x.tile_start = t;
-    t += tiles_of(x.m, x.n);
-  }
-  ListRef ref;
-  if (cudaMalloc(&ref.dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return ListRef{};
-  cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
-  ref.n = (int)v.size();
-  ref.tiles = t;
-  g.hlist_mem.push_back(ref.dev);
-  g.hlists[key] = ref;
+  ListRef ref = upload_list(v, g.hlist_mem);
+  if (ref.dev) g.hlists[key] = ref;
   return ref;
 }
 
@@ -1106,8 +1125,10 @@ static int svgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArg
     g.err = "state-vector work list allocation failed";
     return SQOC_ERR_CUDA;
   }
+  gemm_begin(g, l, st);
   cudaError_t e = (op == SV_CHI) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st)
                                  : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
+  gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
     return SQOC_ERR_CUDA;
@@ -1313,6 +1334,9 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
   const dim3 ew_grid((unsigned)std::min<size_t>(((size_t)maxd * maxd + 255) / 256, 4096), nblk);
   const int* toff = g.tile_off_dev;
   g.launches = 0;
+  g.tev_used = 0;
+  g.gemm_macs = 0.0;
+  g.gemm_launches = 0;
   for (int s = 0; s < a.batch; ++s) {
     const double* u = a.u + (size_t)s * K * N;
     // ---- plan (scheme, s) from the norm bound over all slices and blocks ----
@@ -1401,12 +1425,16 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
       if (done) continue;
     }
     // ---- backward sweep ----
+    if (g.gate) {  // one carry: Ad = 2^-s C_N, C_N = X_N Lam_N^dag (Lam_N = V or the chunk's Lam_end in L[0])
+      int rc;
+      if ((rc = gemm(g, B_C, 0, q, 0, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
+    }
     for (int j = N - 1; j >= 0; --j) {
       build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
       LCHK(cudaGetLastError());
       g.launches++;
       int rc;
-      if ((rc = gemm(g, B_C, 0, q, r, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
+      if (!g.gate && (rc = gemm(g, B_C, 0, q, r, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
       for (int k = 0; k < sc.nsteps; ++k)
         if ((rc = gemm(g, B_STEP, k, sc.degree, 0, step_args(sc.step[k]), st))) return rc;
       int p = 0;
@@ -1414,14 +1442,18 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
         if ((rc = gemm(g, B_S, p, 0, 0, one, st))) return rc;
         p ^= 1;
       }
-      if ((rc = gemm(g, B_D, p, 0, 0, one, st))) return rc;
+      if ((rc = gemm(g, g.gate ? B_UC : B_D, p, 0, 0, one, st))) return rc;
       trace_reduce_kernel<<<nblk, 256, 0, st>>>(j, K, N, toff, g.trace_part, g.tau_dev, g.w_dev, g.gidx_dev,
                                                 a.gradb + (size_t)s * K * N, a.gradb_block_stride);
       LCHK(cudaGetLastError());
       g.launches++;
-      if ((rc = gemm(g, B_XL, p, q, r, one, st))) return rc;
-      q ^= 1;
-      r ^= 1;
+      if (g.gate) {  // C_{j-1} = U^dag C_j U
+        if (j > 0 && (rc = gemm(g, B_CU, p, 0, 0, one, st))) return rc;
+      } else {
+        if ((rc = gemm(g, B_XL, p, q, r, one, st))) return rc;
+        q ^= 1;
+        r ^= 1;
+      }
     }
   }
   return SQOC_OK;

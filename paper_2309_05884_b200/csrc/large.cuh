@@ -9,9 +9,12 @@
 // ||A_j|| <= ||a_0|| + sum_k |u_kj| ||a_k||, large.cu "propagator schemes"):
 //
 //   forward : A, scheme steps (P products) -> Y, T <- T T (s x), X <- U X
-//   backward: Ad = 2^-s X Lam^dag, scheme steps as forward-mode pairs, squaring pairs
-//             -> (U, N = L_R(A, X Lam^dag)); trace epilogue dtau_k = Tr(U^dag N E_k)
-//             (no D stored); X <- U^dag X, Lam <- U^dag Lam.
+//   backward: gate objective -- one d x d carry Ad = 2^-s C_j, C_j = X_j Lam_j^dag (formed once
+//             from X_N and Lam_N); scheme steps as forward-mode pairs seeded with Ad, squaring
+//             pairs -> (U, N = L_R(A, C_j)); one launch forms M = U^dag Ad and the trace
+//             dtau_k = Tr(U^dag N E_k); then Ad <- M U (C_{j-1} = U^dag C_j U).
+//             State objective (vector X, Lam): Ad = 2^-s X Lam^dag per slice, the same pairs
+//             and trace, X <- U^dag X, Lam <- U^dag Lam.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -46,6 +49,7 @@ struct LargeBlockSpec {
 struct ListRef {
   GemmItem* dev = nullptr;
   int n = 0, tiles = 0;
+  double macs = 0.0;  // complex multiply-adds of the list (sum m n k nseg), for the executed-FLOP count
 };
 
 struct LargeGroup {
@@ -75,9 +79,14 @@ struct LargeGroup {
   double* w_dev = nullptr;
   int* gidx_dev = nullptr;
   // GEMM work lists, built once (device), keyed by op + buffer parities
-  std::map<std::tuple<int, int, int, int>, std::pair<GemmItem*, int>> lists;  // (items, count)
-  std::map<std::tuple<int, int, int, int>, int> list_tiles;
+  std::map<std::tuple<int, int, int, int>, ListRef> lists;
   std::vector<void*> list_mem;
+  // GEMM timing (sqoc_set_timing): an event pair around every GEMM launch of the last evaluation
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;
+  size_t tev_used = 0;
+  double gemm_macs = 0.0;  // complex MACs issued by the last evaluation's GEMMs
+  int gemm_launches = 0;
   int* tile_off_dev = nullptr;    // [nblk + 1] trace tile offsets
   // ---- history schedule: every slice resident, slice-batched GEMMs (chosen when memory allows) ----
   int h_deg = -1, h_s = -1, h_C = 0;
@@ -122,6 +131,9 @@ int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, 
 int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st);
 int large_set_norms(LargeGroup& g, const std::vector<double>& gnorm);
 int large_set_complex_gemm(int mults);
+int large_complex_mults();  // 3 (Gauss) or 4
+// Device time of the last evaluation's GEMM launches (needs g.timing during it).
+int large_gemm_time(LargeGroup& g, double* ms);
 void large_free(LargeGroup& g);
 
 }  // namespace sqoc

@@ -10,7 +10,8 @@
 // K segments C = A0 B0 + A1 B1), tiles mapped by a prefix sum so blocks of
 // different sizes share one launch.  Operands may be conjugate-transposed.
 // Epilogues: C = alpha acc + beta0 E0 + beta1 E1 + gamma [diag] I, or a fused
-// trace sum_pq acc[p][q] F_k[q][p] written as per-tile partials (no C store).
+// trace sum_pq acc[p][q] F_k[q][p] written as per-tile partials (no C store); EPI_MIXED
+// lets one launch hold both kinds of items (trace iff the item has nF > 0).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -18,7 +19,7 @@
 namespace sqoc {
 
 enum { OP_N = 0, OP_C = 1 };
-enum { EPI_STORE = 0, EPI_TRACE = 1 };
+enum { EPI_STORE = 0, EPI_TRACE = 1, EPI_MIXED = 2 };  // MIXED: per item, trace iff it.nF > 0
 
 struct GemmItem {
   const double2* A0;
@@ -222,7 +223,8 @@ __global__ void __launch_bounds__(GTHREADS) zgemm_kernel(const GemmItem* __restr
   }
   cp_async_wait<0>();
 
-  if (EPI == EPI_STORE) {
+  const bool trace = EPI == EPI_TRACE || (EPI == EPI_MIXED && it.nF > 0);  // uniform per CTA
+  if (!trace) {
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -394,7 +396,8 @@ __global__ void __launch_bounds__(G3THREADS, 2) zgemm3m_kernel(const GemmItem* _
   }
   cp_async_wait<0>();
 
-  if (EPI == EPI_STORE) {
+  const bool trace = EPI == EPI_TRACE || (EPI == EPI_MIXED && it.nF > 0);  // uniform per CTA
+  if (!trace) {
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll

@@ -162,6 +162,15 @@ class GrapeEngine:
             out.append(ms.value)
         return out
 
+    def gemm_stats(self) -> dict:
+        """Large-block GEMMs of the last evaluation: device ms (needs set_timing(True)), complex
+        MACs issued, launches, and the real FMAs per complex MAC of the GEMM algorithm (3M / 4M)."""
+        ms, macs, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        _lib.check(self.lib.sqoc_last_gemm_stats(self.handle, ctypes.byref(ms), ctypes.byref(macs), ctypes.byref(n)),
+                   "sqoc_last_gemm_stats")
+        return {"ms": ms.value, "complex_macs": macs.value, "launches": n.value,
+                "real_fma_per_complex_mac": self.lib.sqoc_complex_gemm_mults()}
+
     @property
     def last_launches(self) -> int:
         return self.lib.sqoc_last_launch_count(self.handle)

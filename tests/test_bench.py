@@ -47,3 +47,51 @@ def test_clock_sampler_parses_nvidia_smi_lines():
     c.proc = FakeProc()
     r = c.stop()
     assert r["sm_max_mhz"] == 1965 and r["reasons"] == ["sw_power_cap"] and r["samples"] == 2
+
+
+def test_launcher_spawns_ranks_on_cpu():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with two ranks (gloo here)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--selftest-launcher"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["rank_sum"] == 3.0
+
+
+def test_reference_arm_prints_the_same_config_as_ours():
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2309_05884_b200 import systems
+
+    s = systems.config(0)
+    c = bench.config_dict(0, s, 1, 1)
+    assert c["workload"] == bench.CONFIG_NAMES[0] and c["blocks"] == [13] and c["n_slices"] == 100
+    env = dict(os.environ, SQOC_CPU_BUDGET_S="0.3", SQOC_CPU_WARM_BUDGET_S="0.1")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "0",
+                          "--steps", "2", "--warmup", "1"], capture_output=True, text=True, env=env, timeout=600,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["config"] == c and line["warmup"] == 1 and line["steps"] == 2
+
+
+def test_default_config_is_the_largest_single_gpu_config():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert bench.DEFAULT_CONFIG == 3
+
+
+def test_gate_compare_raises_on_mismatch():
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import pytest
+
+    import bench
+
+    rep = {"cases": []}
+    bench._compare(0.5, np.ones(3), 0.5 + 1e-12, np.ones(3) * (1 + 1e-10), "ok", rep)
+    with pytest.raises(bench.CorrectnessGateError):
+        bench._compare(0.5, np.ones(3), 0.5 + 1e-9, np.ones(3), "F off", rep)
+    with pytest.raises(bench.CorrectnessGateError):
+        bench._compare(0.5, np.ones(3), 0.5, np.ones(3) * (1 + 1e-6), "grad off", rep)
