@@ -493,10 +493,11 @@ def run_ours(args):
 
 
 def run_sharded(args):
-    """cfg 2-4 on N > 1 GPUs: slice-chunk sharding of ONE evaluation (parallel.ShardedObjective):
-    per-rank chunk products, one all-gather of the chunk products (the scan carry), carries on the
-    device, local backward sweeps, an all-gather of the gradient.  Total work fixed -> "strong".
-    Timed on the device (CUDA events), max over ranks."""
+    """cfg 2-4 on N > 1 GPUs: ONE evaluation split over a (block groups x slice chunks) grid of ranks
+    (parallel.ShardedObjective): per-rank chunk products, one NCCL all-gather of the chunk products
+    per block group (the scan carry, device to device), boundary values formed on each device,
+    local backward sweeps, one all-gather of the 8 KB gradient rows.  Total work fixed -> "strong".
+    Timed on the device (CUDA events on torch's current stream), max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -505,49 +506,127 @@ def run_sharded(args):
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
     cfg = args.config
     s = build_system(cfg, gpu_basis=True)
-    dev = torch.device("cuda", local)
-    comm = parallel.Comm(device=dev)
-    obj = parallel.ShardedObjective(s, comm, lambda sys_: GrapeEngine(sys_, max_batch=1, device=local))
-    # gate: the sharded evaluation of the cfg's fixture controls (cfg 2 only has a full-size fixture)
-    gate = {"cases": []}
-    if cfg == 2:
-        z = _fixture("cfg2")
-        Fz, gz = obj.objective(s.controls(11))
-        _compare(Fz, gz, float(z["cfg2_F"]), z["cfg2_grad"], f"cfg2 slice-chunk{ws} vs oracle", gate)
+    # default grid: cfg 2 by blocks only (its ~100-dim blocks run the slice-batched history schedule;
+    # chunking would force the slice-sequential one); cfg 3 and cfg 4 by slice chunks only -- block
+    # groups halve each GEMM launch's work list and lose more than they save (cfg 3, 8 emulated ranks,
+    # profiles/r02_chunk_emulate_cfg3.jsonl: 1x8 critical path 7.00 s, 2x4 7.51 s, 4x2 7.63 s)
+    groups = args.block_groups or {2: ws}.get(cfg, 1)
+    comm = parallel.Comm()
+    factory = lambda sys_: GrapeEngine(sys_, max_batch=1, device=local)  # noqa: E731
+    # ---- correctness gate: the sharded path on the committed fixture's system ----
+    gate = {"tol_F_abs": GATE_F_TOL, "tol_grad_rel": GATE_G_TOL, "cases": []}
+    if cfg in (2, 3, 4):
+        if cfg == 2:
+            z, gsys, gu = _fixture("cfg2"), s, s.controls(11)
+            fz, gz = float(z["cfg2_F"]), z["cfg2_grad"]
+        elif cfg == 3:
+            z = _fixture("cfg3")
+            gsys = parallel.local_system(s, 0, 4)
+            gu, fz, gz = gsys.controls(11), float(z["cfg3_F"]), z["cfg3_grad"]
+        else:
+            z = _fixture("cfg4")
+            gsys = parallel.local_system(s, 0, 2)
+            gu, fz, gz = gsys.controls(11), float(z["cfg4_full_F"]), z["cfg4_full_grad"]
+        gobj = parallel.ShardedObjective(gsys, comm, factory, n_block_groups=groups)
+        Fz, gzz = gobj.objective(gu)
+        gobj.eng.close()
+        del gobj
+        torch.cuda.empty_cache()
+        _compare(Fz, gzz, fz, gz, f"cfg{cfg} sharded {groups}x{ws // groups} vs fixture", gate)
+    obj = parallel.ShardedObjective(s, comm, factory, n_block_groups=groups)
     u = s.controls(0)
-    for _ in range(args.warmup):
-        obj.objective(u)
+    u_t = torch.as_tensor(u).to(dev)
+    pinned = torch.from_numpy(u).pin_memory()
+    gh = torch.empty_like(pinned).pin_memory()
+    Fh = torch.empty(1, dtype=torch.float64).pin_memory()
+
+    def e2e_call():
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        uu = pinned.to(dev, non_blocking=True)
+        F_, g_ = obj.objective_t(uu)
+        gh.copy_(g_, non_blocking=True)
+        Fh.copy_(F_.reshape(1), non_blocking=True)
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0
+
+    t_first = time.perf_counter()
+    obj.objective_t(u_t)
+    torch.cuda.synchronize()
+    first_s = time.perf_counter() - t_first
+    e2e = []
+    for _ in range(1, args.warmup):
+        if first_s > 2.0 and len(e2e) < 3:
+            e2e.append(e2e_call())
+        else:
+            obj.objective_t(u_t)
+    torch.cuda.synchronize()
+    obj.timing = True
+    obj.eng.set_timing(True)
+    clocks = ClockSampler(local, period_ms=200 if first_s < 5 else 1000)
+    clocks.start()
     stream = torch.cuda.current_stream()
-    times = []
+    times, stages, carries, launches = [], [], [], 0
     for _ in range(args.steps):
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        F, g = obj.objective(u)
+        F, g = obj.objective_t(u_t)
         e1.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         times.append(float(t.item()))
+        stages.append(dict(obj.stage_ms))
+        carries.append(obj.eng.carry_stats())
+        launches += obj.last_launches
+    clk = clocks.stop()
+    obj.timing = False
+    obj.eng.set_timing(False)
+    if not e2e:
+        for _ in range(max(3, args.steps)):
+            e2e.append(e2e_call())
+    te = torch.tensor([float(np.median(e2e))], dtype=torch.float64, device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    # per-rank stage shares (medians), gathered to rank 0
+    med = {k: float(np.median([x[k] for x in stages])) for k in stages[0]}
+    med["carry"] = float(np.median([c["ms"] for c in carries]))
+    row = torch.tensor([med["forward"], med["exchange"], med["backward"], med["reduce"], med["carry"]],
+                       dtype=torch.float64, device=dev)
+    rows = comm.all_gather(row).cpu().numpy()
     if rank == 0:
         ms = float(np.median(times))
         flops = s.flops_per_eval()
         conf = config_dict(cfg, s, 1, ws)
-        conf["slice_chunks"] = parallel.chunk_bounds(s.n_slices, ws)
+        conf["parallelism"] = f"block-groups{groups} x slice-chunks{ws // groups}"
+        conf["slice_chunks"] = parallel.chunk_bounds(s.n_slices, ws // groups)
+        conf["block_groups"] = parallel.block_groups([b.dim for b in s.blocks], groups)
         conf["steps_ms"] = [round(x, 2) for x in times]
+        per_rank = [{"forward_ms": r[0], "exchange_ms": r[1], "backward_ms": r[2], "reduce_ms": r[3],
+                     "carry_ms": r[4], "carry_plus_comm_share": (r[1] + r[3] + r[4]) / ms} for r in rows]
+        peak = FP64_PEAK_TFLOPS * ws
         print(json.dumps({
             "metric": METRIC, "value": 1e3 / ms, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded)", "config": conf,
-            "roofline": {"bound": "tensor", "achieved": flops / (ms / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS * ws,
-                         "unit": "TFLOP/s", "frac": flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * ws),
-                         "traffic": None},
-            "gate": gate, "F": F,
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded u ~ U[-1,1], seeded Haar/QR targets)",
+            "config": conf,
+            "roofline": {"bound": "tensor", "kernel": "zgemm3m_kernel (all ranks)",
+                         "achieved": flops / (ms / 1e3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                         "frac": flops / (ms / 1e3) / 1e12 / peak, "traffic": None,
+                         "peak_source": f"{ws} x measured FP64 DMMA peak (profiles/r01_fp64_peak.txt)"},
+            "per_rank": per_rank,
+            "e2e": {"value": 1.0 / float(te.item()), "unit": UNIT, "h2d_bytes_per_step": int(u.nbytes),
+                    "d2h_bytes_per_step": int(gh.numel() * 8 + 8), "calls_ms": [round(x * 1e3, 2) for x in e2e]},
+            "gate": gate, "gpu_launches": int(launches), "clocks": clk,
+            "cpu_baseline": {"value": None, "unit": UNIT, "cores": None, "kind": "port",
+                             "sample": "timed on rank 0 at N=1 only"},
         }), flush=True)
+    obj.eng.close()
     dist.destroy_process_group()
 
 
@@ -631,7 +710,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-alone", action="store_true", help="skip the tiny kernel timed-alone pass")
+    ap.add_argument("--block-groups", type=int, default=None,
+                    help="cfg 2-4 on N GPUs: block groups G (N/G slice chunks each); default N for cfg 2, else 1")
     ap.add_argument("--selftest-launcher", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--sharded", action="store_true", help="cfg 2-4: the sharded path even on one rank")
     args = ap.parse_args()
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
@@ -640,8 +722,15 @@ def main():
         sys.exit(relaunch(args))
     elif args.selftest_launcher:
         launcher_selftest()
-    elif args.config in (2, 3, 4) and ws > 1:
-        run_sharded(args)
+    elif args.config in (2, 3, 4) and (ws > 1 or args.sharded):
+        if "WORLD_SIZE" not in os.environ:  # one rank without torchrun: a local rendezvous
+            os.environ.update({"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0", "MASTER_ADDR": "127.0.0.1",
+                               "MASTER_PORT": str(_free_port())})
+        try:
+            run_sharded(args)
+        except CorrectnessGateError as e:
+            print(f"CorrectnessGateError: {e}", file=sys.stderr, flush=True)
+            sys.exit(3)
     else:
         try:
             run_ours(args)

@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define SQOC_ABI_VERSION 1
+#define SQOC_ABI_VERSION 2
 
 enum sqoc_status {
   SQOC_OK = 0,
@@ -118,20 +118,30 @@ int sqoc_set_tiny_cta_warps(sqoc_problem* p, int warps);
  * augmented-action terms (state-vector). */
 int sqoc_last_plan(const sqoc_problem* p, int* taylor_degree, int* squarings, int* action_terms);
 
-/* Slice-chunk sharding (multi-GPU scan carry).  A rank builds
- * the problem for its own contiguous slice range [s, e) (n_slices = e - s, the same
- * dt), then:
- *   sqoc_chunk_product : out[b] (d_b x d_b) = U_{e-1} ... U_s for every block
- *                        (gate-objective problem; batch 1);
- *   sqoc_eval_chunk    : gradient of this rank's slices from the full-grid boundary
- *                        values: x_start[b] = X before slice s (gate d x d, state d),
- *                        lam_end[b] = Lambda after slice e-1 ((U_{N-1}..U_e)^dag V),
- *                        tau[b] = full-grid tau_b (2 doubles each); F = sum_b w_b |tau_b|^2,
- *                        grad [K][e - s].
- * Both need every block to be large (d > 16); tiny blocks shard by batch instead. */
-int sqoc_chunk_product(sqoc_problem* p, const double* u, double* const* out, int memory, void* stream);
-int sqoc_eval_chunk(sqoc_problem* p, const double* u, const double* const* x_start, const double* const* lam_end,
-                    const double* tau, double* F, double* grad, int memory, void* stream);
+/* Slice-chunk sharding of ONE evaluation over ranks (multi-GPU scan carry).
+ * Replaces the reference's strictly sequential slice loops (qoc.py:128-134 forward, :156-167
+ * backward) by P contiguous chunks.  A rank builds the problem for its own slice range [s, e)
+ * (n_slices = e - s, the same dt; any subset of the blocks, weights of the full problem), then:
+ *   sqoc_chunk_size     : length in doubles of one packed chunk product (sum_b 2 d_b^2);
+ *   sqoc_chunk_forward  : packed[...] = C_b = U_{e-1} ... U_s of every block, block order,
+ *                         each d_b x d_b complex row-major (the forward sweep of the chunk);
+ *   (the caller all-gathers the packed products of the P chunks into gathered[P][...],
+ *    e.g. ncclAllGather on device buffers -- the only data that crosses GPUs)
+ *   sqoc_chunk_backward : on the device, the boundary values of chunk c from gathered:
+ *                         gate  X_end = C_c .. C_0, Lam_end = C_{c+1}^dag .. C_{P-1}^dag V_b,
+ *                         state psi_start = C_{c-1} .. C_0 psi_0, chi_end = C_{c+1}^dag .. psi_f,
+ *                         the full-grid tau_b, then the backward sweep of the chunk's slices only
+ *                         (the forward is not repeated): F = sum_b w_b |tau_b|^2 over this
+ *                         problem's blocks, grad [K][e - s], tau [n_blocks][2] (any may be NULL).
+ * Call sqoc_chunk_backward after sqoc_chunk_forward with the same u.  Every block must be large
+ * (d > 16); tiny blocks shard by batch instead (seed-DP).  `memory` applies to every array. */
+int sqoc_chunk_size(const sqoc_problem* p, long long* n_doubles);
+int sqoc_chunk_forward(sqoc_problem* p, const double* u, double* packed, int memory, void* stream);
+int sqoc_chunk_backward(sqoc_problem* p, const double* u, const double* gathered, int n_chunks, int chunk, double* F,
+                        double* grad, double* tau, int memory, void* stream);
+/* Last sqoc_chunk_backward: device time of the boundary-value formation (carry GEMMs + tau; needs
+ * sqoc_set_timing) and the number of carry GEMM launches (each batched over the blocks). */
+int sqoc_last_carry_stats(sqoc_problem* p, double* carry_ms, int* carry_gemms);
 
 /* Complex GEMM algorithm of the large-block path (process-wide): 3 = Gauss/3M (three
  * real DMMA products per complex product, default), 4 = 4M (four).  Both are exact
@@ -189,6 +199,28 @@ int sqoc_basis_columns(const sqoc_basis* b, int block, int* keys, int* col_nnz, 
 int sqoc_basis_compress(const sqoc_basis* b, int n_terms, const int* flip, const int* sign, const double* coef,
                         double* const* out);
 int sqoc_basis_destroy(sqoc_basis* b);
+
+/* Trotterised per-qubit propagator (reference trotter.py:68-225).
+ * Model (model.py:59-92, per-qubit controls): H = sum_i bz/2 Z_i + sum_k c_k/4 sum_i Z_i Z_{i+k}
+ * + sum_i (bx_i X_i + by_i Y_i)/2 on n <= 12 spins, site 1 = most significant bit.
+ *   sqoc_trotter_create  : PerQubitPlan(cfg, tau, strang) (trotter.py:77-114): coupling phases and
+ *                          the exact-H diagonal precomputed on the device
+ *   sqoc_trotter_apply   : n_steps Trotter steps (PerQubitPlan.apply_step, trotter.py:138-152) on the
+ *                          rows of arr [2^n][cols] complex row-major (a state: cols = 1), in place;
+ *                          controls bx, by [n_steps][n]
+ *   sqoc_trotter_replay  : fidelity_replay (trotter.py:196-225): W <- U_trotter (W U_exact^dag) per
+ *                          step from W = I, fids[r] = |Tr W|^2 / 4^n after every record_every-th step
+ *                          and the last (ceil(n_steps / record_every) values)
+ * `memory` applies to arr / bx / by / fids. */
+typedef struct sqoc_trotter sqoc_trotter;
+int sqoc_trotter_create(sqoc_trotter** out, int device, int n, double bz, const double* couplings, int n_couplings,
+                        double tau, int strang);
+int sqoc_trotter_apply(sqoc_trotter* t, double* arr, int cols, const double* bx, const double* by, int n_steps,
+                       int memory, void* stream);
+int sqoc_trotter_replay(sqoc_trotter* t, const double* bx, const double* by, int n_steps, int record_every,
+                        double* fids, int memory, void* stream);
+int sqoc_trotter_last_launches(const sqoc_trotter* t);
+int sqoc_trotter_destroy(sqoc_trotter* t);
 
 /* Largest block dimension the fused on-chip (tiny) path handles. */
 int sqoc_tiny_max_dim(void);

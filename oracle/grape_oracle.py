@@ -159,29 +159,69 @@ def objective(system, u, blocks=None):
 
 
 class OracleChunkEngine:
-    """CPU stand-in for GrapeEngine's slice-chunk interface (tests of parallel.py)."""
+    """CPU stand-in for GrapeEngine's slice-chunk interface (tests of parallel.py): the same packed
+    products and boundary values, restated with numpy on the eigh propagators (qoc.py:128-134)."""
 
     def __init__(self, system):
-        self.system = system
+        import torch
 
-    def chunk_product(self, u):
-        out = []
+        self.system = system
+        self.torch_device = torch.device("cpu")
+
+    def close(self):
+        pass
+
+    def _unpack(self, flat):
+        out, o = [], 0
+        for blk in self.system.blocks:
+            d = blk.dim
+            out.append(flat[o:o + d * d].reshape(d, d))
+            o += d * d
+        return out
+
+    def objective_t(self, u_t):
+        import torch
+
+        F, g, _ = objective(self.system, u_t.numpy())
+        return torch.tensor([F], dtype=torch.float64), torch.from_numpy(g)
+
+    def chunk_forward_t(self, u_t):
+        import torch
+
+        u = u_t.numpy()
+        parts = []
         for blk in self.system.blocks:
             x = np.eye(blk.dim, dtype=np.complex128)
             for j in range(u.shape[1]):
                 uj, _ = expm_hermitian(hamiltonian(blk.h0, blk.hk, u[:, j]), self.system.dt)
                 x = uj @ x
-            out.append(x)
-        return out
+            parts.append(x.reshape(-1))
+        return torch.from_numpy(np.concatenate(parts).view(np.float64).copy())
 
-    def eval_chunk(self, u, x_start, lam_end, tau):
+    def chunk_backward_t(self, u_t, gathered, n_chunks, chunk):
+        import torch
+
+        u = u_t.numpy()
+        prods = [self._unpack(gathered[i].numpy().view(np.complex128)) for i in range(n_chunks)]
         w = self.system.block_weights()
-        F = float(np.sum(w * np.abs(tau) ** 2))
+        F = 0.0
         grad = np.zeros(np.shape(u))
         for b, blk in enumerate(self.system.blocks):
+            left = np.eye(blk.dim, dtype=np.complex128)
+            for i in range(chunk):
+                left = prods[i][b] @ left
+            right = np.eye(blk.dim, dtype=np.complex128)
+            for i in range(chunk + 1, n_chunks):
+                right = prods[i][b] @ right
+            tgt = np.asarray(self.system.targets[b], dtype=np.complex128)
+            lam_end = right.conj().T @ tgt
             if self.system.objective == "gate":
-                _, dt = gate_dtau(lam_end[b], u, blk.h0, blk.hk, self.system.dt, x0=x_start[b], lam_end=lam_end[b])
+                tau = np.vdot(lam_end, prods[chunk][b] @ left)
+                _, dt = gate_dtau(lam_end, u, blk.h0, blk.hk, self.system.dt, x0=left, lam_end=lam_end)
             else:
-                _, dt = state_dtau(x_start[b], lam_end[b], u, blk.h0, blk.hk, self.system.dt)
-            grad += 2.0 * w[b] * np.real(np.conj(tau[b]) * dt)
-        return F, grad
+                psi_start = left @ np.asarray(self.system.initial[b], dtype=np.complex128)
+                tau = np.vdot(lam_end, prods[chunk][b] @ psi_start)
+                _, dt = state_dtau(psi_start, lam_end, u, blk.h0, blk.hk, self.system.dt)
+            F += w[b] * abs(tau) ** 2
+            grad += 2.0 * w[b] * np.real(np.conj(tau) * dt)
+        return torch.tensor([F], dtype=torch.float64), torch.from_numpy(grad)

@@ -47,8 +47,10 @@ SIGNATURES = {
     "sqoc_set_tiny_cta_warps": (_I, [_P, _I]),
     "sqoc_last_plan": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "sqoc_set_norm_bounds": (_I, [_P, _D]),
-    "sqoc_chunk_product": (_I, [_P, _P, _P, _I, _P]),
-    "sqoc_eval_chunk": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _P]),
+    "sqoc_chunk_size": (_I, [_P, ctypes.POINTER(ctypes.c_longlong)]),
+    "sqoc_chunk_forward": (_I, [_P, _P, _P, _I, _P]),
+    "sqoc_chunk_backward": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _I, _P]),
+    "sqoc_last_carry_stats": (_I, [_P, _D, ctypes.POINTER(_I)]),
     "sqoc_block_time_ms": (_I, [_P, _I, _D]),
     "sqoc_last_gemm_stats": (_I, [_P, _D, _D, ctypes.POINTER(_I)]),
     "sqoc_complex_gemm_mults": (_I, []),
@@ -59,6 +61,11 @@ SIGNATURES = {
     "sqoc_basis_columns": (_I, [_P, _I, _P, _P, _P, _P]),
     "sqoc_basis_compress": (_I, [_P, _I, _P, _P, _P, _P]),
     "sqoc_basis_destroy": (_I, [_P]),
+    "sqoc_trotter_create": (_I, [ctypes.POINTER(_P), _I, _I, ctypes.c_double, _P, _I, ctypes.c_double, _I]),
+    "sqoc_trotter_apply": (_I, [_P, _P, _I, _P, _P, _I, _I, _P]),
+    "sqoc_trotter_replay": (_I, [_P, _P, _P, _I, _I, _P, _I, _P]),
+    "sqoc_trotter_last_launches": (_I, [_P]),
+    "sqoc_trotter_destroy": (_I, [_P]),
     "sqoc_last_error": (ctypes.c_char_p, []),
     "sqoc_abi_version": (_I, []),
 }

@@ -7,7 +7,7 @@ import re
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "large.cu", "basis.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "large.cu", "basis.cu", "trotter.cu")]
 DEPS = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + [
     os.path.join(HERE, "..", "include", "symqoc_b200.h")
 ]

@@ -562,55 +562,37 @@ int sqoc_eval(sqoc_problem* p, const double* u, int batch, double* F, double* gr
 }
 
 // ---------------------------------------------------------------- slice-chunk sharding
-static int bc_stage(sqoc_problem* p, const double* const* src, int memory, double2** dev_bufs,
-                    std::vector<double2*>& keep, cudaStream_t st) {
-  // copy per-block d x R boundary matrices to device scratch; fill dev_bufs[b]
-  const bool gate = p->objective == SQOC_OBJ_GATE;
-  for (int b = 0; b < p->nblocks; ++b) {
-    const size_t n = (size_t)p->blocks[b].d * (gate ? p->blocks[b].d : 1);
-    double2* d = nullptr;
-    SQOC_CUDA(cudaMalloc(&d, n * sizeof(double2)));
-    keep.push_back(d);
-    SQOC_CUDA(cudaMemcpyAsync(d, src[b], n * sizeof(double2),
-                              memory == SQOC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
-    dev_bufs[b] = d;
-  }
-  return SQOC_OK;
-}
-
-static int chunk_checks(sqoc_problem* p) {
+static int chunk_checks(sqoc_problem* p, int memory) {
   if (!p) return fail(SQOC_ERR_ARG, "problem is NULL");
+  if (memory != SQOC_MEM_HOST && memory != SQOC_MEM_DEVICE) return fail(SQOC_ERR_ARG, "unknown memory kind");
   if (!p->large) return fail(SQOC_ERR_UNSUPPORTED, "slice-chunk sharding needs large blocks (d > 16)");
   for (auto& b : p->blocks)
     if (b.tiny) return fail(SQOC_ERR_UNSUPPORTED, "slice-chunk sharding is not built for tiny blocks (use seed-DP)");
   return SQOC_OK;
 }
 
-int sqoc_chunk_product(sqoc_problem* p, const double* u, double* const* out, int memory, void* stream) {
-  int rc = chunk_checks(p);
+int sqoc_chunk_size(const sqoc_problem* p, long long* n_doubles) {
+  if (!p || !n_doubles) return fail(SQOC_ERR_ARG, "problem or n_doubles is NULL");
+  long long n = 0;
+  for (auto& b : p->blocks) n += 2LL * b.d * b.d;
+  *n_doubles = n;
+  return SQOC_OK;
+}
+
+int sqoc_chunk_forward(sqoc_problem* p, const double* u, double* packed, int memory, void* stream) {
+  int rc = chunk_checks(p, memory);
   if (rc != SQOC_OK) return rc;
-  if (p->objective != SQOC_OBJ_GATE) return fail(SQOC_ERR_ARG, "chunk products need a gate-objective problem");
-  if (!out) return fail(SQOC_ERR_ARG, "out is NULL");
+  if (!packed || (!u && p->N > 0)) return fail(SQOC_ERR_ARG, "u or packed is NULL");
   SQOC_CUDA(cudaSetDevice(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t KN = (size_t)p->K * p->N;
+  const size_t total = p->large->total;
   const double* u_dev = u;
+  double2* out = reinterpret_cast<double2*>(packed);
   if (memory == SQOC_MEM_HOST) {
-    SQOC_CUDA(cudaMemcpyAsync(p->u_dev, u, KN * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (KN) SQOC_CUDA(cudaMemcpyAsync(p->u_dev, u, KN * sizeof(double), cudaMemcpyHostToDevice, st));
     u_dev = p->u_dev;
-  }
-  std::vector<double2*> tmp;
-  p->large->fwd_out.assign(p->nblocks, nullptr);
-  for (int b = 0; b < p->nblocks; ++b) {
-    const size_t n = (size_t)p->blocks[b].d * p->blocks[b].d;
-    if (memory == SQOC_MEM_HOST) {
-      double2* d = nullptr;
-      SQOC_CUDA(cudaMalloc(&d, n * sizeof(double2)));
-      tmp.push_back(d);
-      p->large->fwd_out[b] = d;
-    } else {
-      p->large->fwd_out[b] = reinterpret_cast<double2*>(out[b]);
-    }
+    SQOC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out), total * sizeof(double2), st));
   }
   LargeArgs la;
   la.u = u_dev;
@@ -619,57 +601,59 @@ int sqoc_chunk_product(sqoc_problem* p, const double* u, double* const* out, int
   la.tau_stride = p->nblocks;
   la.gradb = p->gradb;
   la.gradb_block_stride = (size_t)p->max_batch * KN;
+  p->large->chunk_phase = 1;
+  p->large->chunk_out = out;
   rc = large_eval(*p->large, la, st);
-  p->large->fwd_out.clear();
-  if (rc != SQOC_OK) {
-    for (auto d : tmp) cudaFree(d);
-    return fail(rc, p->large->err);
-  }
+  p->large->chunk_phase = 0;
+  p->large->chunk_out = nullptr;
   p->launches = p->large->launches;
-  if (memory == SQOC_MEM_HOST)
-    for (int b = 0; b < p->nblocks; ++b) {
-      const size_t n = (size_t)p->blocks[b].d * p->blocks[b].d;
-      SQOC_CUDA(cudaMemcpyAsync(out[b], tmp[b], n * sizeof(double2), cudaMemcpyDeviceToHost, st));
-    }
+  if (rc == SQOC_OK && memory == SQOC_MEM_HOST)
+    SQOC_CUDA(cudaMemcpyAsync(packed, out, total * sizeof(double2), cudaMemcpyDeviceToHost, st));
+  if (memory == SQOC_MEM_HOST) cudaFreeAsync(out, st);
+  if (rc != SQOC_OK) return fail(rc, p->large->err);
   SQOC_CUDA(cudaStreamSynchronize(st));
-  for (auto d : tmp) cudaFree(d);
   return SQOC_OK;
 }
 
-int sqoc_eval_chunk(sqoc_problem* p, const double* u, const double* const* x_start, const double* const* lam_end,
-                    const double* tau, double* F, double* grad, int memory, void* stream) {
-  int rc = chunk_checks(p);
+int sqoc_chunk_backward(sqoc_problem* p, const double* u, const double* gathered, int n_chunks, int chunk, double* F,
+                        double* grad, double* tau, int memory, void* stream) {
+  int rc = chunk_checks(p, memory);
   if (rc != SQOC_OK) return rc;
-  if (!x_start || !lam_end || !tau) return fail(SQOC_ERR_ARG, "boundary arrays are NULL");
+  if (!gathered) return fail(SQOC_ERR_ARG, "gathered is NULL");
+  if (n_chunks < 1 || chunk < 0 || chunk >= n_chunks) return fail(SQOC_ERR_ARG, "chunk outside 0..n_chunks-1");
   SQOC_CUDA(cudaSetDevice(p->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  std::vector<double2*> keep;
-  std::vector<double2*> xb(p->nblocks), lb(p->nblocks);
-  rc = bc_stage(p, x_start, memory, xb.data(), keep, st);
-  if (rc == SQOC_OK) rc = bc_stage(p, lam_end, memory, lb.data(), keep, st);
-  double2 *xptrs = nullptr, *lptrs = nullptr, *taud = nullptr;
-  if (rc == SQOC_OK) {
-    SQOC_CUDA(cudaMalloc(&xptrs, p->nblocks * sizeof(double2*)));
-    SQOC_CUDA(cudaMalloc(&lptrs, p->nblocks * sizeof(double2*)));
-    SQOC_CUDA(cudaMalloc(&taud, p->nblocks * sizeof(double2)));
-    SQOC_CUDA(cudaMemcpyAsync(xptrs, xb.data(), p->nblocks * sizeof(double2*), cudaMemcpyHostToDevice, st));
-    SQOC_CUDA(cudaMemcpyAsync(lptrs, lb.data(), p->nblocks * sizeof(double2*), cudaMemcpyHostToDevice, st));
-    SQOC_CUDA(cudaMemcpyAsync(taud, tau, p->nblocks * sizeof(double2),
-                              memory == SQOC_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
-    SQOC_CUDA(cudaStreamSynchronize(st));
-    p->large->bc_x_dev = reinterpret_cast<const double2**>(xptrs);
-    p->large->bc_l_dev = reinterpret_cast<const double2**>(lptrs);
-    p->large->bc_tau = taud;
-    rc = sqoc_eval(p, u, 1, F, grad, nullptr, memory, stream);
-    p->large->bc_x_dev = nullptr;
-    p->large->bc_l_dev = nullptr;
-    p->large->bc_tau = nullptr;
+  const size_t total = p->large->total;
+  const double2* in = reinterpret_cast<const double2*>(gathered);
+  double2* staged = nullptr;
+  if (memory == SQOC_MEM_HOST) {
+    SQOC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&staged), (size_t)n_chunks * total * sizeof(double2), st));
+    SQOC_CUDA(cudaMemcpyAsync(staged, gathered, (size_t)n_chunks * total * sizeof(double2), cudaMemcpyHostToDevice,
+                              st));
+    in = staged;
   }
-  cudaFree(xptrs);
-  cudaFree(lptrs);
-  cudaFree(taud);
-  for (auto d : keep) cudaFree(d);
+  p->large->chunk_phase = 2;
+  p->large->chunk_in = in;
+  p->large->chunk_P = n_chunks;
+  p->large->chunk_c = chunk;
+  rc = sqoc_eval(p, u, 1, F, grad, tau, memory, stream);
+  p->large->chunk_phase = 0;
+  p->large->chunk_in = nullptr;
+  if (staged) {
+    cudaFreeAsync(staged, st);
+    cudaStreamSynchronize(st);
+  }
   return rc;
+}
+
+int sqoc_last_carry_stats(sqoc_problem* p, double* carry_ms, int* carry_gemms) {
+  if (!p || !carry_ms || !carry_gemms) return fail(SQOC_ERR_ARG, "NULL argument");
+  *carry_ms = 0.0;
+  *carry_gemms = 0;
+  if (!p->large) return SQOC_OK;
+  *carry_gemms = p->large->carry_gemms;
+  if (p->timing) large_carry_time(*p->large, carry_ms);
+  return SQOC_OK;
 }
 
 int sqoc_set_norm_bounds(sqoc_problem* p, const double* bounds) {

@@ -738,6 +738,11 @@ void large_free(LargeGroup& g) {
   cudaFree(g.gentall_dev);
   double2* sv[] = {g.sv_U, g.sv_chunk, g.sv_psi, g.sv_chi, g.sv_V, g.sv_W, g.sv_acc, g.sv_g, g.mf_t};
   for (auto x : sv) cudaFree(x);
+  cudaFree(g.chunk_vec);
+  cudaFree(g.chunk_tau);
+  cudaFree(g.chunk_ptrs);
+  for (auto e : g.carry_ev)
+    if (e) cudaEventDestroy(e);
   cudaFree(g.gent_dev);
   for (auto m : g.hlist_mem) cudaFree(m);
   g.hlist_mem.clear();
@@ -759,17 +764,8 @@ static int bc_init(LargeGroup& g, double2* X, double2* L, dim3 grid, cudaStream_
   return SQOC_OK;
 }
 
-// tau from X_N (or the given full-grid tau); forward-only calls copy X_N out and stop (*done)
-static int bc_tau(LargeGroup& g, const double2* XN, const LargeArgs& a, int s_idx, cudaStream_t st, bool* done) {
-  *done = false;
-  if (!g.fwd_out.empty()) {
-    for (int b = 0; b < g.nblk; ++b) {
-      const size_t n = (size_t)g.blocks[b].d * (g.gate ? g.blocks[b].d : 1);
-      LCHK(cudaMemcpyAsync(g.fwd_out[b], XN + g.offr[b], n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
-    }
-    *done = true;
-    return SQOC_OK;
-  }
+// tau from X_N (or the full-grid tau a chunk's phase 2 formed from the gathered products)
+static int bc_tau(LargeGroup& g, const double2* XN, const LargeArgs& a, int s_idx, cudaStream_t st) {
   if (g.bc_tau) {
     set_tau_kernel<<<(g.nblk + 127) / 128, 128, 0, st>>>(g.nblk, g.bc_tau, g.tau_dev,
                                                           a.tau_out + (size_t)s_idx * a.tau_stride, g.gidx_dev);
@@ -1019,9 +1015,7 @@ static int large_eval_history(LargeGroup& g, const LargeArgs& a, int s_idx, cons
     for (int i = 0; i < N; ++i)
       if ((rc = hgemm(g, H_X, 0, 0, i, i + 1, one, st))) return rc;
   }
-  bool done = false;
-  if ((rc = bc_tau(g, g.h_X + (size_t)N * g.totalr, a, s_idx, st, &done))) return rc;
-  if (done) return SQOC_OK;
+  if ((rc = bc_tau(g, g.h_X + (size_t)N * g.totalr, a, s_idx, st))) return rc;
   if (chunked) {
     if ((rc = history_scans(g, false, true, st))) return rc;
   } else {
@@ -1150,18 +1144,21 @@ static int taylor_terms(double beta) {
 
 static int sv_gradient(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, double bound, cudaStream_t st);
 
-static int large_eval_state_vector(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, int sq,
-                                   double bound, cudaStream_t st) {
-  const int K = g.K, N = g.N, nblk = g.nblk;
-  const PolyScheme& sc = scheme_of(g.last_degree);
+static unsigned sv_ew_x(const LargeGroup& g) {
   int maxd = 0;
   for (auto& b : g.blocks) maxd = std::max(maxd, b.d);
-  const unsigned ew_x = (unsigned)std::max<size_t>(1, std::min<size_t>(((size_t)maxd * maxd + 255) / 256, 256));
+  return (unsigned)std::max<size_t>(1, std::min<size_t>(((size_t)maxd * maxd + 255) / 256, 256));
+}
+
+// propagators U_i of every slice, S slices per launch, kept in sv_U for both vector sweeps
+static int sv_propagators(LargeGroup& g, const double* u, int sq, cudaStream_t st) {
+  const int K = g.K, N = g.N, nblk = g.nblk;
+  const PolyScheme& sc = scheme_of(g.last_degree);
+  const unsigned ew_x = sv_ew_x(g);
   const double scale = std::ldexp(1.0, -sq);
   const size_t S = g.sv_S, sl = g.total;
   GemmArgs one{1.0, 0.0, 0.0, 0.0};
   int rc;
-  // ---- propagators U_i, chunk by chunk, kept for both vector sweeps ----
   for (int i0 = 0; i0 < N; i0 += (int)S) {
     const int n_here = std::min<int>((int)S, N - i0);
     const dim3 grid(ew_x, nblk, n_here);
@@ -1178,14 +1175,19 @@ static int large_eval_state_vector(LargeGroup& g, const LargeArgs& a, int s_idx,
     LCHK(cudaMemcpyAsync(g.sv_U + (size_t)i0 * sl, g.sv_chunk + (size_t)(kSlotY + p) * S * sl,
                          (size_t)n_here * sl * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   }
-  // ---- psi / chi sweeps (sequential over slices, batched over blocks) ----
-  const dim3 ew_grid(ew_x, nblk);
+  return SQOC_OK;
+}
+
+// psi / chi sweeps over the U_i in sv_U (sequential over slices, batched over blocks) + gradient
+static int sv_sweeps(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, double bound, cudaStream_t st) {
+  const int N = g.N;
+  GemmArgs one{1.0, 0.0, 0.0, 0.0};
+  int rc;
+  const dim3 ew_grid(sv_ew_x(g), g.nblk);
   if ((rc = bc_init(g, g.sv_psi, g.sv_chi + (size_t)N * g.totalr, ew_grid, st))) return rc;
   for (int i = 0; i < N; ++i)
     if ((rc = svgemm(g, SV_PSI, 0, 0, i, i + 1, one, st))) return rc;
-  bool done = false;
-  if ((rc = bc_tau(g, g.sv_psi + (size_t)N * g.totalr, a, s_idx, st, &done))) return rc;
-  if (done) return SQOC_OK;
+  if ((rc = bc_tau(g, g.sv_psi + (size_t)N * g.totalr, a, s_idx, st))) return rc;
   for (int i = N - 1; i >= 0; --i)
     if ((rc = svgemm(g, SV_CHI, 0, 0, i, i + 1, one, st))) return rc;
   return sv_gradient(g, a, s_idx, u, bound, st);
@@ -1314,9 +1316,7 @@ static int large_eval_matrix_free(LargeGroup& g, const LargeArgs& a, int s_idx, 
     if ((rc = mf_action(g, 1.0, m, sigma, g.sv_psi + (size_t)j * g.totalr, g.sv_psi + (size_t)(j + 1) * g.totalr, st)))
       return rc;
   }
-  bool done = false;
-  if ((rc = bc_tau(g, g.sv_psi + (size_t)N * g.totalr, a, s_idx, st, &done))) return rc;
-  if (done) return SQOC_OK;
+  if ((rc = bc_tau(g, g.sv_psi + (size_t)N * g.totalr, a, s_idx, st))) return rc;
   for (int j = N - 1; j >= 0; --j) {  // chi_j = exp(A_j)^dag chi_{j+1} = exp(-A_j) chi_{j+1} (A anti-Hermitian)
     build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, 1.0, g.A, 0);
     LCHK(cudaGetLastError());
@@ -1327,12 +1327,285 @@ static int large_eval_matrix_free(LargeGroup& g, const LargeArgs& a, int s_idx, 
   return sv_gradient(g, a, s_idx, u, bound, st);
 }
 
-int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
+
+// ------------------------------------------------------------------ slice-sequential schedule
+// forward sweep from the boundary X_0 (I / psi_0 / a chunk's X_start); returns the parity q of X_N
+static int seq_forward(LargeGroup& g, const double* u, const PolyScheme& sc, int sq, dim3 ew_grid, cudaStream_t st,
+                       int* q_out) {
+  const int K = g.K, N = g.N;
+  const double scale = std::ldexp(1.0, -sq);
+  int rc;
+  if ((rc = bc_init(g, g.X[0], g.L[0], ew_grid, st))) return rc;
+  int q = 0;
+  GemmArgs one{1.0, 0.0, 0.0, 0.0};
+  for (int j = 0; j < N; ++j) {
+    build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
+    LCHK(cudaGetLastError());
+    g.launches++;
+    for (int k = 0; k < sc.nsteps; ++k)
+      if ((rc = gemm(g, F_STEP, k, sc.degree, 0, step_args(sc.step[k]), st))) return rc;
+    int p = 0;
+    for (int i = 0; i < sq; ++i) {
+      if ((rc = gemm(g, F_S, p, 0, 0, one, st))) return rc;
+      p ^= 1;
+    }
+    if ((rc = gemm(g, F_X, p, q, 0, one, st))) return rc;
+    q ^= 1;
+  }
+  *q_out = q;
+  return SQOC_OK;
+}
+
+// backward sweep from X_N (X[q]) and Lam_N (L[0]); tau must already be set
+static int seq_backward(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, const PolyScheme& sc, int sq,
+                        int q, dim3 ew_grid, cudaStream_t st) {
   const int K = g.K, N = g.N, nblk = g.nblk;
+  const double scale = std::ldexp(1.0, -sq);
+  GemmArgs one{1.0, 0.0, 0.0, 0.0};
+  int rc, r = 0;
+  if (g.gate) {  // one carry: Ad = 2^-s C_N, C_N = X_N Lam_N^dag
+    if ((rc = gemm(g, B_C, 0, q, 0, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
+  }
+  for (int j = N - 1; j >= 0; --j) {
+    build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
+    LCHK(cudaGetLastError());
+    g.launches++;
+    if (!g.gate && (rc = gemm(g, B_C, 0, q, r, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
+    for (int k = 0; k < sc.nsteps; ++k)
+      if ((rc = gemm(g, B_STEP, k, sc.degree, 0, step_args(sc.step[k]), st))) return rc;
+    int p = 0;
+    for (int i = 0; i < sq; ++i) {
+      if ((rc = gemm(g, B_S, p, 0, 0, one, st))) return rc;
+      p ^= 1;
+    }
+    if ((rc = gemm(g, g.gate ? B_UC : B_D, p, 0, 0, one, st))) return rc;
+    trace_reduce_kernel<<<nblk, 256, 0, st>>>(j, K, N, g.tile_off_dev, g.trace_part, g.tau_dev, g.w_dev, g.gidx_dev,
+                                              a.gradb + (size_t)s_idx * K * N, a.gradb_block_stride);
+    LCHK(cudaGetLastError());
+    g.launches++;
+    if (g.gate) {  // C_{j-1} = U^dag C_j U
+      if (j > 0 && (rc = gemm(g, B_CU, p, 0, 0, one, st))) return rc;
+    } else {
+      if ((rc = gemm(g, B_XL, p, q, r, one, st))) return rc;
+      q ^= 1;
+      r ^= 1;
+    }
+  }
+  return SQOC_OK;
+}
+
+// ------------------------------------------------------------------ slice-chunk sharding
+__global__ void eye_kernel(const int* __restrict__ dims, const size_t* __restrict__ off, double2* __restrict__ out) {
+  const int b = blockIdx.y;
+  const int d = dims[b];
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)d * d; i += (size_t)gridDim.x * blockDim.x)
+    out[off[b] + i] = make_double2((i / d == i % d) ? 1.0 : 0.0, 0.0);
+}
+
+// One launch per carry step, each batched over the blocks; all lists uploaded in one stream-ordered
+// allocation (freed in stream order after the last launch).
+struct CarryStep {
+  int ta;          // OP_N or OP_C on the chunk product
+  size_t first, n; // items
+};
+
+static int run_carry_steps(LargeGroup& g, std::vector<GemmItem>& items, const std::vector<CarryStep>& steps,
+                           cudaStream_t st) {
+  if (items.empty()) return SQOC_OK;
+  for (auto& s : steps) {  // tile offsets restart per launch
+    int t = 0;
+    for (size_t i = s.first; i < s.first + s.n; ++i) {
+      items[i].tile_start = t;
+      t += tiles_of(items[i].m, items[i].n);
+    }
+  }
+  GemmItem* dev = nullptr;
+  LCHK(cudaMallocAsync(reinterpret_cast<void**>(&dev), items.size() * sizeof(GemmItem), st));
+  LCHK(cudaMemcpyAsync(dev, items.data(), items.size() * sizeof(GemmItem), cudaMemcpyHostToDevice, st));
+  GemmArgs one{1.0, 0.0, 0.0, 0.0};
+  for (auto& s : steps) {
+    int tiles = 0;
+    ListRef l;
+    for (size_t i = s.first; i < s.first + s.n; ++i) {
+      tiles += tiles_of(items[i].m, items[i].n);
+      l.macs += (double)items[i].m * items[i].n * items[i].k;
+    }
+    gemm_begin(g, l, st);
+    cudaError_t e = s.ta == OP_C ? launch_gemm<OP_C, OP_N, EPI_STORE>(dev + s.first, (int)s.n, tiles, one, st)
+                                 : launch_gemm<OP_N, OP_N, EPI_STORE>(dev + s.first, (int)s.n, tiles, one, st);
+    gemm_end(g, st);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(dev, st);
+      g.err = std::string("carry zgemm launch: ") + cudaGetErrorString(e);
+      return SQOC_ERR_CUDA;
+    }
+    g.launches++;
+    g.carry_gemms++;
+  }
+  LCHK(cudaFreeAsync(dev, st));
+  return SQOC_OK;
+}
+
+// Boundary values of chunk c from the gathered products (chunk_in).  Gate: X_end -> X[0],
+// Lam_end -> L[0]; state: psi_start / chi_end in chunk_vec; tau of every block -> chunk_tau.
+static int chunk_carries(LargeGroup& g, cudaStream_t st) {
+  const int P = g.chunk_P, c = g.chunk_c, nb = g.nblk;
+  const size_t tot = g.total;
+  auto Cp = [&](int i, int b) { return g.chunk_in + (size_t)i * tot + g.off[b]; };
+  std::vector<GemmItem> items;
+  std::vector<CarryStep> steps;
+  std::vector<const double2*> xs(nb), ls(nb);
+  if (!g.chunk_vec) {
+    LCHK(cudaMalloc(&g.chunk_vec, 5 * g.totalr * sizeof(double2)));
+    LCHK(cudaMalloc(&g.chunk_tau, nb * sizeof(double2)));
+    LCHK(cudaMalloc(reinterpret_cast<void**>(&g.chunk_ptrs), 2 * nb * sizeof(double2*)));
+  }
+  auto add_step = [&](int ta, auto item_of) {
+    CarryStep s{ta, items.size(), (size_t)nb};
+    for (int b = 0; b < nb; ++b) items.push_back(item_of(b, g.blocks[b].d));
+    steps.push_back(s);
+  };
+  const double2* X_tau = nullptr;  // the matrix / vector tau is read against Lam_end / chi_end
+  if (g.gate) {
+    // left: M_1 = C_1 C_0, M_i = C_i M_{i-1}, X_end = M_c (T[0] / T[1] ping-pong, last into X[0])
+    for (int i = 1; i <= c; ++i)
+      add_step(OP_N, [&](int b, int d) {
+        const double2* B = i == 1 ? Cp(0, b) : g.T[(i - 2) & 1] + g.off[b];
+        double2* C = i == c ? g.X[0] + g.off[b] : g.T[(i - 1) & 1] + g.off[b];
+        return mk(Cp(i, b), B, 0, 0, C, 0, 0, d, d, d, 1, d, d, d, 0);
+      });
+    if (c == 0) LCHK(cudaMemcpyAsync(g.X[0], Cp(0, 0), tot * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    // right: R_1 = C_{P-1}^dag V, R_i = C_{P-i}^dag R_{i-1}, Lam_end = R_{P-1-c} (dT ping-pong, last into L[0])
+    const int nr = P - 1 - c;
+    for (int i = 1; i <= nr; ++i)
+      add_step(OP_C, [&](int b, int d) {
+        const double2* B = i == 1 ? g.blocks[b].target : g.dT[(i - 2) & 1] + g.off[b];
+        double2* C = i == nr ? g.L[0] + g.off[b] : g.dT[(i - 1) & 1] + g.off[b];
+        return mk(Cp(P - i, b), B, 0, 0, C, 0, 0, d, d, d, 1, d, d, d, 0);
+      });
+    if (nr == 0)
+      for (int b = 0; b < nb; ++b)
+        LCHK(cudaMemcpyAsync(g.L[0] + g.off[b], g.blocks[b].target, (size_t)g.blocks[b].d * g.blocks[b].d *
+                             sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    for (int b = 0; b < nb; ++b) {
+      xs[b] = g.X[0] + g.off[b];
+      ls[b] = g.L[0] + g.off[b];
+    }
+    X_tau = g.X[0];
+  } else {
+    // vectors: chunk_vec slots 0/1 left ping-pong, 2/3 right ping-pong, 4 = C_c psi_start
+    auto V = [&](int slot, int b) { return g.chunk_vec + (size_t)slot * g.totalr + g.offr[b]; };
+    for (int i = 1; i <= c; ++i)  // v_i = C_{i-1} v_{i-1}, v_0 = psi_0
+      add_step(OP_N, [&](int b, int d) {
+        const double2* x = i == 1 ? g.blocks[b].x0 : V((i - 2) & 1, b);
+        return mk(Cp(i - 1, b), x, 0, 0, V((i - 1) & 1, b), 0, 0, d, 1, d, 1, d, 1, 1, 0);
+      });
+    for (int b = 0; b < nb; ++b) xs[b] = c == 0 ? g.blocks[b].x0 : V((c - 1) & 1, b);
+    add_step(OP_N, [&](int b, int d) { return mk(Cp(c, b), xs[b], 0, 0, V(4, b), 0, 0, d, 1, d, 1, d, 1, 1, 0); });
+    const int nr = P - 1 - c;
+    for (int i = 1; i <= nr; ++i)  // w_i = C_{P-i}^dag w_{i-1}, w_0 = psi_f
+      add_step(OP_C, [&](int b, int d) {
+        const double2* x = i == 1 ? g.blocks[b].target : V(2 + ((i - 2) & 1), b);
+        return mk(Cp(P - i, b), x, 0, 0, V(2 + ((i - 1) & 1), b), 0, 0, d, 1, d, 1, d, 1, 1, 0);
+      });
+    for (int b = 0; b < nb; ++b) ls[b] = nr == 0 ? g.blocks[b].target : V(2 + ((nr - 1) & 1), b);
+    X_tau = g.chunk_vec + 4 * g.totalr;
+  }
+  int rc = run_carry_steps(g, items, steps, st);
+  if (rc) return rc;
+  std::vector<const double2*> ptrs(xs);
+  ptrs.insert(ptrs.end(), ls.begin(), ls.end());
+  LCHK(cudaMemcpyAsync(g.chunk_ptrs, ptrs.data(), 2 * nb * sizeof(double2*), cudaMemcpyHostToDevice, st));
+  // tau_b = <Lam_end, X_end> (gate, = Tr(V^dag X_N)) or <chi_end, C_c psi_start> (state, = <psi_f|X_N|psi_0>)
+  tau_kernel<<<nb, 256, 0, st>>>(g.gate, 1, g.d_dev, g.offr_dev, X_tau, g.chunk_ptrs + nb, g.chunk_tau, g.chunk_tau,
+                                 g.gidx_dev);
+  LCHK(cudaGetLastError());  // (chunk problems hold large blocks only: global index == local index)
+  g.launches++;
+  return SQOC_OK;
+}
+
+static int chunk_eval(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, const PolyScheme& sc, int sq,
+                      double bound, dim3 ew_grid, cudaStream_t st) {
+  int rc;
+  if (g.chunk_phase == 1) {
+    if (g.gate) {  // forward sweep from X = I; X_N is the chunk product
+      g.mode = 0;
+      int q = 0;
+      if ((rc = seq_forward(g, u, sc, sq, ew_grid, st, &q))) return rc;
+      LCHK(cudaMemcpyAsync(g.chunk_out, g.X[q], g.total * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    } else {  // every U_j kept (the sweeps of phase 2 reuse them); product by one GEMM per slice
+      g.mode = 2;
+      if ((rc = sv_alloc(g, true))) return rc;
+      if ((rc = sv_propagators(g, u, sq, st))) return rc;
+      const int N = g.N;
+      if (N == 0) {
+        eye_kernel<<<ew_grid, 256, 0, st>>>(g.d_dev, g.off_dev, g.chunk_out);
+        LCHK(cudaGetLastError());
+      } else if (N == 1) {
+        LCHK(cudaMemcpyAsync(g.chunk_out, g.sv_U, g.total * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+      }
+      std::vector<GemmItem> items;
+      std::vector<CarryStep> steps;
+      for (int i = 1; i < N; ++i) {  // M_i = U_i M_{i-1}, M_0 = U_0 (T ping-pong, last into chunk_out)
+        CarryStep s{OP_N, items.size(), (size_t)g.nblk};
+        for (int b = 0; b < g.nblk; ++b) {
+          const int d = g.blocks[b].d;
+          const double2* B = i == 1 ? g.sv_U + g.off[b] : g.T[(i - 2) & 1] + g.off[b];
+          double2* C = i == N - 1 ? g.chunk_out + g.off[b] : g.T[(i - 1) & 1] + g.off[b];
+          items.push_back(mk(g.sv_U + (size_t)i * g.total + g.off[b], B, 0, 0, C, 0, 0, d, d, d, 1, d, d, d, 0));
+        }
+        steps.push_back(s);
+      }
+      g.carry_gemms = 0;
+      if ((rc = run_carry_steps(g, items, steps, st))) return rc;
+    }
+    g.chunk_fwd_valid = true;
+    return SQOC_OK;
+  }
+  // ---- phase 2 ----
+  if (!g.gate && !g.chunk_fwd_valid) {
+    g.err = "sqoc_chunk_backward needs sqoc_chunk_forward on the same problem and controls first";
+    return SQOC_ERR_ARG;
+  }
+  g.carry_gemms = 0;
+  if (g.timing) {
+    for (auto& e : g.carry_ev)
+      if (!e) LCHK(cudaEventCreate(&e));
+    LCHK(cudaEventRecord(g.carry_ev[0], st));
+  }
+  if ((rc = chunk_carries(g, st))) return rc;
+  if (g.timing) LCHK(cudaEventRecord(g.carry_ev[1], st));
+  g.bc_tau = g.chunk_tau;
+  if (g.gate) {
+    g.mode = 0;
+    rc = bc_tau(g, nullptr, a, s_idx, st);  // tau_dev and tau_out from the carries
+    if (rc == SQOC_OK) rc = seq_backward(g, a, s_idx, u, sc, sq, 0, ew_grid, st);
+  } else {
+    g.mode = 2;
+    g.bc_x_dev = g.chunk_ptrs;
+    g.bc_l_dev = g.chunk_ptrs + g.nblk;
+    rc = sv_sweeps(g, a, s_idx, u, bound, st);
+  }
+  g.bc_tau = nullptr;
+  g.bc_x_dev = g.bc_l_dev = nullptr;
+  return rc;
+}
+
+int large_carry_time(LargeGroup& g, double* ms) {
+  *ms = 0.0;
+  if (!g.carry_ev[0] || !g.carry_ev[1]) return SQOC_OK;
+  float x = 0.f;
+  if (cudaEventElapsedTime(&x, g.carry_ev[0], g.carry_ev[1]) == cudaSuccess) *ms = x;
+  else (void)cudaGetLastError();
+  return SQOC_OK;
+}
+
+// ------------------------------------------------------------------ evaluation
+int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
+  const int N = g.N, K = g.K, nblk = g.nblk;
   int maxd = 0;
   for (auto& b : g.blocks) maxd = std::max(maxd, b.d);
   const dim3 ew_grid((unsigned)std::min<size_t>(((size_t)maxd * maxd + 255) / 256, 4096), nblk);
-  const int* toff = g.tile_off_dev;
   g.launches = 0;
   g.tev_used = 0;
   g.gemm_macs = 0.0;
@@ -1352,12 +1625,15 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
     const PolyScheme& sc = *choose_scheme(bound, sq);
     g.last_degree = sc.degree;
     g.last_s = sq;
+    int rc;
+    if (g.chunk_phase) {
+      if ((rc = chunk_eval(g, a, s, u, sc, sq, bound, ew_grid, st))) return rc;
+      continue;
+    }
     if (!g.gate && N > 0 && g.force_mode == 3) {  // matrix-free state schedule (opt-in)
-      int rc = sv_alloc(g, false);
-      if (rc != SQOC_OK) return rc;
+      if ((rc = sv_alloc(g, false))) return rc;
       g.mode = 3;
-      rc = large_eval_matrix_free(g, a, s, u, bound, st);
-      if (rc != SQOC_OK) return rc;
+      if ((rc = large_eval_matrix_free(g, a, s, u, bound, st))) return rc;
       continue;
     }
     if (!g.gate && N > 0 && g.force_mode != 0 && g.force_mode != 1) {  // state-vector schedule
@@ -1369,11 +1645,11 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
         use_sv = sv_fixed_bytes(g) + 5 * g.total * sizeof(double2) <= (size_t)(0.7 * (double)(free_b + have));
       }
       if (use_sv) {
-        int rc = sv_alloc(g, true);
-        if (rc != SQOC_OK) return rc;
+        if ((rc = sv_alloc(g, true))) return rc;
         g.mode = 2;
-        rc = large_eval_state_vector(g, a, s, u, sq, bound, st);
-        if (rc != SQOC_OK) return rc;
+        g.chunk_fwd_valid = false;  // sv_U now holds this evaluation's propagators
+        if ((rc = sv_propagators(g, u, sq, st))) return rc;
+        if ((rc = sv_sweeps(g, a, s, u, bound, st))) return rc;
         continue;
       }
     }
@@ -1386,75 +1662,17 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
         use_hist = history_bytes(g, kSlots + sq) <= (size_t)(0.6 * (double)(free_b + have));
       }
       if (use_hist && N > 0) {
-        int rc = hist_alloc(g, sc.degree, sq);
-        if (rc != SQOC_OK) return rc;
+        if ((rc = hist_alloc(g, sc.degree, sq))) return rc;
         g.mode = 1;
-        rc = large_eval_history(g, a, s, u, sq, st);
-        if (rc != SQOC_OK) return rc;
+        if ((rc = large_eval_history(g, a, s, u, sq, st))) return rc;
         continue;
       }
       g.mode = 0;
     }
-    const double scale = std::ldexp(1.0, -sq);
-    // ---- forward sweep ----
-    {
-      int rc0 = bc_init(g, g.X[0], g.L[0], ew_grid, st);
-      if (rc0) return rc0;
-    }
-    int q = 0, r = 0;
-    GemmArgs one{1.0, 0.0, 0.0, 0.0};
-    for (int j = 0; j < N; ++j) {
-      build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
-      LCHK(cudaGetLastError());
-      g.launches++;
-      int rc;
-      for (int k = 0; k < sc.nsteps; ++k)
-        if ((rc = gemm(g, F_STEP, k, sc.degree, 0, step_args(sc.step[k]), st))) return rc;
-      int p = 0;
-      for (int i = 0; i < sq; ++i) {
-        if ((rc = gemm(g, F_S, p, 0, 0, one, st))) return rc;
-        p ^= 1;
-      }
-      if ((rc = gemm(g, F_X, p, q, 0, one, st))) return rc;
-      q ^= 1;
-    }
-    {
-      bool done = false;
-      int rc0 = bc_tau(g, g.X[q], a, s, st, &done);
-      if (rc0) return rc0;
-      if (done) continue;
-    }
-    // ---- backward sweep ----
-    if (g.gate) {  // one carry: Ad = 2^-s C_N, C_N = X_N Lam_N^dag (Lam_N = V or the chunk's Lam_end in L[0])
-      int rc;
-      if ((rc = gemm(g, B_C, 0, q, 0, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
-    }
-    for (int j = N - 1; j >= 0; --j) {
-      build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
-      LCHK(cudaGetLastError());
-      g.launches++;
-      int rc;
-      if (!g.gate && (rc = gemm(g, B_C, 0, q, r, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
-      for (int k = 0; k < sc.nsteps; ++k)
-        if ((rc = gemm(g, B_STEP, k, sc.degree, 0, step_args(sc.step[k]), st))) return rc;
-      int p = 0;
-      for (int i = 0; i < sq; ++i) {
-        if ((rc = gemm(g, B_S, p, 0, 0, one, st))) return rc;
-        p ^= 1;
-      }
-      if ((rc = gemm(g, g.gate ? B_UC : B_D, p, 0, 0, one, st))) return rc;
-      trace_reduce_kernel<<<nblk, 256, 0, st>>>(j, K, N, toff, g.trace_part, g.tau_dev, g.w_dev, g.gidx_dev,
-                                                a.gradb + (size_t)s * K * N, a.gradb_block_stride);
-      LCHK(cudaGetLastError());
-      g.launches++;
-      if (g.gate) {  // C_{j-1} = U^dag C_j U
-        if (j > 0 && (rc = gemm(g, B_CU, p, 0, 0, one, st))) return rc;
-      } else {
-        if ((rc = gemm(g, B_XL, p, q, r, one, st))) return rc;
-        q ^= 1;
-        r ^= 1;
-      }
-    }
+    int q = 0;
+    if ((rc = seq_forward(g, u, sc, sq, ew_grid, st, &q))) return rc;
+    if ((rc = bc_tau(g, g.X[q], a, s, st))) return rc;
+    if ((rc = seq_backward(g, a, s, u, sc, sq, q, ew_grid, st))) return rc;
   }
   return SQOC_OK;
 }

@@ -15,6 +15,9 @@
 //             dtau_k = Tr(U^dag N E_k); then Ad <- M U (C_{j-1} = U^dag C_j U).
 //             State objective (vector X, Lam): Ad = 2^-s X Lam^dag per slice, the same pairs
 //             and trace, X <- U^dag X, Lam <- U^dag Lam.
+//
+// Slice-chunk sharding runs the same sweeps on one rank's slices, split in two phases around the
+// exchange of the chunk products (LargeGroup::chunk_phase).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -115,12 +118,29 @@ struct LargeGroup {
   const double2** gentall_dev = nullptr;  // per block a_k^T for k = 0..K
   std::vector<void*> gentall_mem;
   int last_degree = 0, last_s = 0, last_taylor_terms = 0;
-  // boundary conditions for slice-chunk sharding (set by the engine for one sqoc_eval_chunk /
-  // sqoc_chunk_product call, cleared afterwards)
-  const double2** bc_x_dev = nullptr;     // device array of per-block X_start pointers, or null
-  const double2** bc_l_dev = nullptr;     // device array of per-block Lam_end pointers, or null
-  const double2* bc_tau = nullptr;        // device [nblk] full-grid tau_b, or null
-  std::vector<double2*> fwd_out;          // forward-only: X_N of each block copied here
+  // ---- slice-chunk sharding (sqoc_chunk_forward / sqoc_chunk_backward) ----
+  // phase 1 writes this chunk's product C = U_{N-1} .. U_0 of every block, packed in block order
+  // (block b at off[b], d_b x d_b row-major), to chunk_out.  Phase 2 reads the products of all P
+  // chunks (chunk_in, [P][total], chunk order) and forms the boundary values on the device:
+  //   gate : X_end = C_c C_{c-1} .. C_0, Lam_end = C_{c+1}^dag .. C_{P-1}^dag V, tau = <Lam_end, X_end>
+  //          -> the slice-sequential backward sweep only (the forward ran in phase 1);
+  //   state: psi_start = C_{c-1} .. C_0 psi_0, chi_end = C_{c+1}^dag .. C_{P-1}^dag psi_f,
+  //          tau = <chi_end, C_c psi_start> -> vector sweeps + gradient over the U_j phase 1 kept.
+  int chunk_phase = 0;                // 0 ordinary evaluation, 1 chunk forward, 2 chunk backward
+  double2* chunk_out = nullptr;       // phase 1 output [total]
+  const double2* chunk_in = nullptr;  // phase 2 input [P][total]
+  int chunk_P = 0, chunk_c = 0;
+  bool chunk_fwd_valid = false;       // state: sv_U holds the propagators of the last phase 1
+  double2* chunk_vec = nullptr;       // state carries: [5][totalr]
+  double2* chunk_tau = nullptr;       // [nblk]
+  const double2** chunk_ptrs = nullptr;  // device [2][nblk]: X_start / Lam_end block pointers
+  cudaEvent_t carry_ev[2] = {nullptr, nullptr};
+  float carry_ms = 0.f;               // device time of the last phase 2's carries (timing on)
+  int carry_gemms = 0;                // carry GEMM launches of the last phase 2
+  // boundary values consumed by bc_init / bc_tau (set only inside a phase 2 evaluation)
+  const double2** bc_x_dev = nullptr;
+  const double2** bc_l_dev = nullptr;
+  const double2* bc_tau = nullptr;
   int mode = -1;                    // last schedule used: 0 sequential, 1 history, 2 state-vector, 3 matrix-free
   int force_mode = -1;              // -1 auto, 0 sequential, 1 history, 2 state-vector, 3 matrix-free
   int launches = 0;
@@ -134,6 +154,8 @@ int large_set_complex_gemm(int mults);
 int large_complex_mults();  // 3 (Gauss) or 4
 // Device time of the last evaluation's GEMM launches (needs g.timing during it).
 int large_gemm_time(LargeGroup& g, double* ms);
+// Device time of the last chunk phase 2's boundary-value formation (needs g.timing during it).
+int large_carry_time(LargeGroup& g, double* ms);
 void large_free(LargeGroup& g);
 
 }  // namespace sqoc

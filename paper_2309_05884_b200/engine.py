@@ -16,16 +16,29 @@ from . import _lib
 def spectral_norm_bound(h: np.ndarray) -> float:
     """Upper bound of ||H||_2 for a Hermitian generator (host setup, not the hot path).
 
-    Dense eigvalsh up to d = 512, Lanczos (ARPACK, largest magnitude) above; a
+    Dense eigvalsh up to d = 2048, Lanczos (ARPACK, largest magnitude) above; a
     relative margin of 1e-6 covers the iteration tolerance.
     """
     h = np.asarray(h)
-    if h.shape[0] <= 512:
+    if h.shape[0] <= 2048:  # dense tridiagonalisation: 0.25 s at d = 1161 against 0.4-0.8 s for Lanczos
         return float(np.abs(np.linalg.eigvalsh(h)).max()) * (1 + 1e-12) + 1e-300
     from scipy.sparse.linalg import eigsh
 
     lam = eigsh(h, k=1, which="LM", return_eigenvectors=False, tol=1e-10)
     return float(np.abs(lam).max()) * (1 + 1e-6)
+
+
+def block_norm_bounds(blk) -> tuple:
+    """(||H0||_2, ||H_1||_2, ...) bounds of one block, computed once and kept on the block object
+    (the engines of sharded ranks and of the correctness gate share the system's blocks)."""
+    cached = getattr(blk, "_sqoc_norm_bounds", None)
+    if cached is None:
+        cached = tuple(spectral_norm_bound(m) for m in (blk.h0, *blk.hk))
+        try:
+            blk._sqoc_norm_bounds = cached
+        except AttributeError:
+            pass
+    return cached
 
 
 def _cplx(a) -> np.ndarray:
@@ -87,7 +100,7 @@ class GrapeEngine:
         _lib.check(rc, "sqoc_create")
         self.handle = handle
         if spectral_bounds and max(dims) > self.lib.sqoc_tiny_max_dim():
-            bounds = np.array([[spectral_norm_bound(m) for m in (blk.h0, *blk.hk)] for blk in system.blocks])
+            bounds = np.array([block_norm_bounds(blk) for blk in system.blocks])
             _lib.check(self.lib.sqoc_set_norm_bounds(self.handle, np.ascontiguousarray(bounds).ctypes.data_as(
                 ctypes.POINTER(ctypes.c_double))), "sqoc_set_norm_bounds")
 
@@ -199,29 +212,63 @@ class GrapeEngine:
         """objective(u) -> (F, grad): the BASELINE host API."""
         return self.evaluate(u)
 
-    # ---- slice-chunk sharding (DESIGN.md section 6) ----
-    def chunk_product(self, u) -> list:
-        """[U_{N-1} ... U_0 per block] for this problem's slices (gate-objective problem)."""
-        u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
-        outs = [np.empty((d, d), dtype=np.complex128) for d in self.dims]
-        arr = (ctypes.c_void_p * self.nblocks)(*[o.ctypes.data for o in outs])
-        _lib.check(self.lib.sqoc_chunk_product(self.handle, u.ctypes.data, arr, _lib.MEM_HOST, None),
-                   "sqoc_chunk_product")
-        return outs
+    # ---- slice-chunk sharding (parallel.py, DESIGN.md section 6): torch tensors on this device ----
+    @property
+    def torch_device(self):
+        import torch
 
-    def eval_chunk(self, u, x_start, lam_end, tau):
-        """(F, grad (K, N_local)) of this rank's slices given full-grid boundary values."""
-        u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
-        xs = [np.ascontiguousarray(x, dtype=np.complex128) for x in x_start]
-        ls = [np.ascontiguousarray(x, dtype=np.complex128) for x in lam_end]
-        t = np.ascontiguousarray(np.asarray(tau, dtype=np.complex128).reshape(-1))
-        xa = (ctypes.c_void_p * self.nblocks)(*[x.ctypes.data for x in xs])
-        la = (ctypes.c_void_p * self.nblocks)(*[x.ctypes.data for x in ls])
-        F = np.empty(1)
-        grad = np.empty_like(u)
-        _lib.check(self.lib.sqoc_eval_chunk(self.handle, u.ctypes.data, xa, la, t.ctypes.data, F.ctypes.data,
-                                            grad.ctypes.data, _lib.MEM_HOST, None), "sqoc_eval_chunk")
-        return float(F[0]), grad
+        return torch.device("cuda", self.device)
+
+    def objective_t(self, u_t):
+        """Ordinary evaluation on device tensors: u_t (K, N) -> (F (1,), grad (K, N)) on this device."""
+        import torch
+
+        u_t = u_t.to(self.torch_device, torch.float64).contiguous()
+        F = torch.empty(1, dtype=torch.float64, device=self.torch_device)
+        grad = torch.empty_like(u_t)
+        st = torch.cuda.current_stream(self.torch_device).cuda_stream
+        self.evaluate_device(u_t.data_ptr(), 1, F.data_ptr(), grad.data_ptr(), stream=st)
+        return F, grad
+
+    def chunk_size(self) -> int:
+        """Doubles in one packed chunk product (sum_b 2 d_b^2)."""
+        n = ctypes.c_longlong()
+        _lib.check(self.lib.sqoc_chunk_size(self.handle, ctypes.byref(n)), "sqoc_chunk_size")
+        return n.value
+
+    def chunk_forward_t(self, u_t):
+        """Packed U_{N-1} ... U_0 of every block (float64 [2 sum d^2] on this device) for this problem's
+        slices; u_t (K, N) float64 on this device.  Runs on torch's current stream."""
+        import torch
+
+        u_t = u_t.to(self.torch_device, torch.float64).contiguous()
+        out = torch.empty(self.chunk_size(), dtype=torch.float64, device=self.torch_device)
+        st = torch.cuda.current_stream(self.torch_device).cuda_stream
+        _lib.check(self.lib.sqoc_chunk_forward(self.handle, u_t.data_ptr(), out.data_ptr(), _lib.MEM_DEVICE,
+                                               st or None), "sqoc_chunk_forward")
+        return out
+
+    def chunk_backward_t(self, u_t, gathered, n_chunks: int, chunk: int):
+        """(F (1,), grad (K, N_local)) device tensors of this chunk from the gathered products
+        [n_chunks, 2 sum d^2] (boundary values formed on the device)."""
+        import torch
+
+        u_t = u_t.to(self.torch_device, torch.float64).contiguous()
+        gathered = gathered.contiguous()
+        F = torch.empty(1, dtype=torch.float64, device=self.torch_device)
+        grad = torch.empty_like(u_t)
+        st = torch.cuda.current_stream(self.torch_device).cuda_stream
+        _lib.check(self.lib.sqoc_chunk_backward(self.handle, u_t.data_ptr(), gathered.data_ptr(), int(n_chunks),
+                                                int(chunk), F.data_ptr(), grad.data_ptr(), None, _lib.MEM_DEVICE,
+                                                st or None), "sqoc_chunk_backward")
+        return F, grad
+
+    def carry_stats(self) -> dict:
+        """Last chunk backward: device ms of the boundary values (needs set_timing(True)) and carry launches."""
+        ms, n = ctypes.c_double(), ctypes.c_int()
+        _lib.check(self.lib.sqoc_last_carry_stats(self.handle, ctypes.byref(ms), ctypes.byref(n)),
+                   "sqoc_last_carry_stats")
+        return {"ms": ms.value, "launches": n.value}
 
     def evaluate_host_ptr(self, u_ptr: int, batch: int, F_ptr: int, grad_ptr: int):
         """Host pointers (e.g. pinned torch tensors); copies happen inside the call."""

@@ -19,7 +19,7 @@ def test_header_symbols_exported():
 
 def test_abi_version_and_limits():
     lib = _lib.load()
-    assert lib.sqoc_abi_version() == 1
+    assert lib.sqoc_abi_version() == 2
     assert lib.sqoc_tiny_max_dim() == 16
 
 
@@ -31,3 +31,20 @@ def test_create_rejects_bad_arguments():
     rc = lib.sqoc_create(ctypes.byref(h), 0, 0, None, 2, None, None, 1, None, None, None, 10, 0.1, 1)
     assert rc == _lib.SQOC_ERR_ARG
     assert b"missing" in lib.sqoc_last_error()
+
+
+def test_trotter_and_chunk_entry_points_reject_bad_arguments_without_a_gpu():
+    import ctypes
+
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    assert lib.sqoc_trotter_create(ctypes.byref(h), 0, 13, 1.0, None, 0, 0.05, 0) == _lib.SQOC_ERR_ARG
+    assert b"n <= 12" in lib.sqoc_last_error()
+    cpl = (ctypes.c_double * 3)(0.2, 0.1, 0.1)
+    assert lib.sqoc_trotter_create(ctypes.byref(h), 0, 4, 1.0, cpl, 3, 0.05, 0) == _lib.SQOC_ERR_ARG
+    assert lib.sqoc_trotter_apply(None, None, 1, None, None, 1, 0, None) == _lib.SQOC_ERR_ARG
+    assert lib.sqoc_trotter_replay(None, None, None, 1, 1, None, 0, None) == _lib.SQOC_ERR_ARG
+    assert lib.sqoc_chunk_forward(None, None, None, 0, None) == _lib.SQOC_ERR_ARG
+    assert lib.sqoc_chunk_backward(None, None, None, 1, 0, None, None, None, 0, None) == _lib.SQOC_ERR_ARG
+    n = ctypes.c_longlong()
+    assert lib.sqoc_chunk_size(None, ctypes.byref(n)) == _lib.SQOC_ERR_ARG

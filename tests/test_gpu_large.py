@@ -123,18 +123,66 @@ def test_cfg4_short_grid_schedules_agree():
     assert rel(g1, g3) <= G_TOL
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_slice_chunk_sharding_emulated_on_one_gpu(world):
-    """The multi-GPU scan-carry algorithm (parallel.py) run as `world` emulated ranks through
-    sqoc_chunk_product / sqoc_eval_chunk equals the unsharded evaluation."""
+@pytest.mark.parametrize("world,groups", [(2, 1), (3, 1), (4, 2)])
+def test_slice_chunk_sharding_emulated_on_one_gpu(world, groups):
+    """The multi-GPU algorithm (parallel.py: block groups x slice chunks) run as `world` emulated ranks
+    through sqoc_chunk_forward / sqoc_chunk_backward -- carries formed on the device from the
+    stacked chunk products -- equals the unsharded evaluation (gate: sequential backward only;
+    state: the state-vector sweeps over the U_j the forward phase kept)."""
     from paper_2309_05884_b200 import parallel
 
     for s in (systems.config(2, n_slices=24), systems.state_transfer_ring(8, 10.0 * 12 / 200, 12, seed=4, full=True)):
+        if groups > len(s.blocks):
+            continue
         u = s.controls(6)
         F0, g0 = GrapeEngine(s, max_batch=1).objective(u)
-        F, g = parallel.emulate_ranks(s, world, lambda sys_: GrapeEngine(sys_, max_batch=1), u)
+        F, g = parallel.emulate_ranks(s, world, lambda sys_: GrapeEngine(sys_, max_batch=1), u, n_block_groups=groups)
         assert abs(F - F0) <= F_TOL
         assert rel(g, g0) <= G_TOL
+
+
+def test_cfg3_eight_chunk_carries_on_device_against_oracle():
+    """cfg 3's 16 GPU-built D_14 blocks on 8 slices as 8 emulated ranks (one slice each: the P = 8
+    carry chains of every rank at full block size) and as 2 block groups x 4 chunks, against the
+    unsharded GPU evaluation (itself pinned to the oracle at all 16 blocks by
+    test_gpu_baseline.test_cfg3_all_16_blocks_against_oracle)."""
+    from paper_2309_05884_b200 import parallel
+
+    s = systems.config(3, n_slices=8, builder="gpu")
+    u = s.controls(5)
+    eng = GrapeEngine(s, max_batch=1)
+    eng.set_schedule("sequential")
+    F0, g0 = eng.objective(u)
+    eng.close()
+    for world, groups in ((8, 1), (8, 2)):
+        F, g = parallel.emulate_ranks(s, world, lambda sys_: GrapeEngine(sys_, max_batch=1), u, n_block_groups=groups)
+        assert abs(F - F0) <= F_TOL, (world, groups)
+        assert rel(g, g0) <= G_TOL, (world, groups)
+
+
+def test_chunk_carry_stats_and_errors():
+    import torch
+
+    s = systems.config(2, n_slices=6)
+    eng = GrapeEngine(s, max_batch=1)
+    u = torch.as_tensor(s.controls(2)).cuda()
+    packed = eng.chunk_forward_t(u)
+    assert packed.numel() == eng.chunk_size() == 2 * sum(b.dim ** 2 for b in s.blocks)
+    eng.set_timing(True)
+    gathered = torch.stack([packed, packed, packed])
+    eng.chunk_backward_t(u, gathered, 3, 1)
+    st = eng.carry_stats()
+    assert st["launches"] == 2 and st["ms"] > 0.0  # one left + one right carry GEMM launch at c = 1 of 3
+    with pytest.raises(ValueError):
+        eng.chunk_backward_t(u, gathered, 3, 3)
+    eng.close()
+    # state objectives need the forward phase (it keeps the U_j) before the backward phase
+    st_sys = systems.state_transfer_ring(8, 10.0 * 4 / 200, 4, seed=4, full=True)
+    e2 = GrapeEngine(st_sys, max_batch=1)
+    u2 = torch.as_tensor(st_sys.controls(1)).cuda()
+    with pytest.raises(ValueError):
+        e2.chunk_backward_t(u2, torch.zeros(1, e2.chunk_size(), dtype=torch.float64, device="cuda"), 1, 0)
+    e2.close()
 
 
 @pytest.mark.parametrize("mults", [4, 3])

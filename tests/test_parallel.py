@@ -28,40 +28,55 @@ def _systems():
     }
 
 
-def _worker(rank, world, port, kind, out_dir):
+def _worker(rank, world, port, kind, groups, out_dir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         s = _systems()[kind]
         u = s.controls(3)
-        obj = parallel.ShardedObjective(s, parallel.Comm(), O.OracleChunkEngine)
+        obj = parallel.ShardedObjective(s, parallel.Comm(), O.OracleChunkEngine, n_block_groups=groups)
         F, g = obj.objective(u)
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), F=F, g=g)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["gate", "state"])
-def test_two_rank_gloo_matches_unsharded_oracle(kind):
+@pytest.mark.parametrize("kind,world,groups", [("gate", 2, 1), ("state", 2, 1), ("gate", 4, 2), ("gate", 2, 2)])
+def test_gloo_ranks_match_unsharded_oracle(kind, world, groups):
+    """world ranks over gloo (block groups x slice chunks): every rank ends with the full F and gradient."""
     with tempfile.TemporaryDirectory() as tmp:
-        mp.spawn(_worker, args=(2, _free_port(), kind, tmp), nprocs=2, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), kind, groups, tmp), nprocs=world, join=True)
         s = _systems()[kind]
         Fo, go, _ = O.objective(s, s.controls(3))
-        for r in range(2):
+        for r in range(world):
             res = np.load(os.path.join(tmp, f"r{r}.npz"))
             assert abs(float(res["F"]) - Fo) <= 1e-12
             np.testing.assert_allclose(res["g"], go, atol=1e-12 * np.abs(go).max())
 
 
-@pytest.mark.parametrize("world", [1, 3, 4])
-def test_emulated_ranks_match_unsharded_oracle(world):
-    for s in _systems().values():
+@pytest.mark.parametrize("world,groups", [(1, 1), (3, 1), (4, 1), (4, 2), (6, 3), (2, 2)])
+def test_emulated_ranks_match_unsharded_oracle(world, groups):
+    for kind, s in _systems().items():
+        if groups > len(s.blocks):
+            continue
         u = s.controls(7)
-        F, g = parallel.emulate_ranks(s, world, O.OracleChunkEngine, u)
+        F, g = parallel.emulate_ranks(s, world, O.OracleChunkEngine, u, n_block_groups=groups)
         Fo, go, _ = O.objective(s, u)
-        assert abs(F - Fo) <= 1e-12
+        assert abs(F - Fo) <= 1e-12, kind
         np.testing.assert_allclose(g, go, atol=1e-12 * np.abs(go).max())
+
+
+def test_block_groups_balance_cfg3_dims():
+    dims = [687, 495, 549, 613] + [1161, 1161, 1179, 1179] * 3
+    for n in (1, 2, 4, 8):
+        gr = parallel.block_groups(dims, n)
+        assert sorted(b for g in gr for b in g) == list(range(16))
+        loads = [sum(dims[b] ** 3 for b in g) for g in gr]
+        if n <= 4:  # 12 blocks of ~1170 over 8 groups cannot balance: block groups stay <= 4 at cfg 3
+            assert max(loads) / min(loads) <= {1: 1.0, 2: 1.01, 4: 1.03}[n]
+    with pytest.raises(ValueError):
+        parallel.block_groups(dims, 17)
 
 
 def test_chunk_bounds_cover_grid():
