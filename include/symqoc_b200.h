@@ -148,6 +148,13 @@ int sqoc_last_carry_stats(sqoc_problem* p, double* carry_ms, int* carry_gemms);
  * algorithms; 3M rounds slightly differently (still ~1e-15 relative). */
 int sqoc_set_complex_gemm(int mults);
 
+/* Large-block 3M GEMM kernel (process-wide): 1 = persistent warp-specialised kernel, one CTA per SM,
+ * a producer warp streaming TMA tensor-map loads into a 12-stage 128B-swizzled shared-memory ring
+ * with full/empty mbarriers across tile boundaries (default); 0 = the per-tile kernel with per-thread
+ * cp.async staging and a block barrier per K stage.  SQOC_GEMM_TMA=0/1 sets the initial mode. */
+int sqoc_set_gemm_staging(int tma);
+int sqoc_gemm_staging(void);
+
 /* Free all device memory of the problem. */
 int sqoc_destroy(sqoc_problem* p);
 

@@ -54,6 +54,8 @@ SIGNATURES = {
     "sqoc_block_time_ms": (_I, [_P, _I, _D]),
     "sqoc_last_gemm_stats": (_I, [_P, _D, _D, ctypes.POINTER(_I)]),
     "sqoc_complex_gemm_mults": (_I, []),
+    "sqoc_set_gemm_staging": (_I, [_I]),
+    "sqoc_gemm_staging": (_I, []),
     "sqoc_tiny_max_dim": (_I, []),
     "sqoc_dn_basis_create": (_I, [ctypes.POINTER(_P), _I, _I]),
     "sqoc_basis_info": (_I, [_P, ctypes.POINTER(_I), _P, _P]),

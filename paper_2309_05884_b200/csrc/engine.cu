@@ -740,6 +740,12 @@ int sqoc_last_gemm_stats(sqoc_problem* p, double* gemm_ms, double* complex_macs,
 
 int sqoc_complex_gemm_mults(void) { return large_complex_mults(); }
 
+int sqoc_set_gemm_staging(int tma) {
+  if (large_set_staging(tma) != SQOC_OK) return fail(SQOC_ERR_ARG, "staging must be 0 (cp.async), 1 or 2 (TMA)");
+  return SQOC_OK;
+}
+int sqoc_gemm_staging(void) { return large_staging(); }
+
 int sqoc_block_time_ms(const sqoc_problem* p, int block, double* ms) {
   if (!p || !ms || block < 0 || block >= p->nblocks) return fail(SQOC_ERR_ARG, "bad block index");
   const BlockPlan& bp = p->blocks[block];

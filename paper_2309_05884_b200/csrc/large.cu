@@ -405,8 +405,110 @@ int large_set_complex_gemm(int mults) {
   return SQOC_OK;
 }
 
+// Large-path 3M GEMM: the persistent warp-specialised TMA kernel (zgemm_tma.cuh, default) or the
+// per-tile cp.async kernel (zgemm3m_kernel); SQOC_GEMM_TMA=0/1 in the environment or
+// sqoc_set_gemm_staging selects it.
+static int g_staging = -1;  // -1 unset, 0 cp.async, 1 persistent TMA
+static int staging() {
+  if (g_staging < 0) {
+    const char* e = getenv("SQOC_GEMM_TMA");
+    g_staging = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_staging;
+}
+int large_set_staging(int mode) {
+  if (mode < 0 || mode > 1) return SQOC_ERR_ARG;
+  g_staging = mode;
+  return SQOC_OK;
+}
+int large_staging() { return staging(); }
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    else
+      (void)cudaGetLastError();
+  });
+  return fn;
+}
+
+// rows x cols complex matrix (row stride ld complex) as FP64 pairs; boxes of box_rows x 8 complex, 128B swizzle
+static bool make_map(CUtensorMap* out, const double2* base, int rows, int cols, int ld, int box_rows) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || !base) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)2 * cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double2)};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Tensor maps of every item in both staging orientations (host); false if the driver cannot encode.
+static bool build_maps(const std::vector<GemmItem>& v, std::vector<ItemMaps>& maps) {
+  maps.assign(v.size(), ItemMaps{});
+  for (size_t i = 0; i < v.size(); ++i) {
+    const GemmItem& it = v[i];
+    for (int seg = 0; seg < it.nseg; ++seg) {
+      const double2* A = seg ? it.A1 : it.A0;
+      const double2* B = seg ? it.B1 : it.B0;
+      CUtensorMap* m = maps[i].m + 4 * seg;
+      if (!make_map(m + 0, A, it.m, it.k, it.lda, GBM) || !make_map(m + 1, A, it.k, it.m, it.lda, 8) ||
+          !make_map(m + 2, B, it.k, it.n, it.ldb, 8) || !make_map(m + 3, B, it.n, it.k, it.ldb, GBN))
+        return false;
+    }
+  }
+  return true;
+}
+
+// The persistent kernel's tiles, most expensive first (K stages x the busiest warp's DMMA sub-tiles;
+// dealt round-robin over the CTAs this balances full, edge and 2-segment tiles).
+constexpr double kPersistentMinK = 256.0;  // mean K (x segments) from which a list uses the persistent kernel
+
+static void build_tiles(const std::vector<GemmItem>& v, std::vector<TileRef>& out) {
+  std::vector<std::pair<double, TileRef>> all;
+  for (size_t i = 0; i < v.size(); ++i) {
+    const GemmItem& it = v[i];
+    const int tm = (it.m + GBM - 1) / GBM, tn = (it.n + GBN - 1) / GBN;
+    const double kt = (double)((it.k + GBK - 1) / GBK) * it.nseg;
+    for (int a = 0; a < tm; ++a)
+      for (int b = 0; b < tn; ++b) {
+        const int rows = std::min(GBM, it.m - a * GBM), cols = std::min(GBN, it.n - b * GBN);
+        const int mc = std::min(4, (std::min(rows, 32) + 7) / 8), nc = std::min(2, (std::min(cols, 16) + 7) / 8);
+        all.push_back({kt * (mc * nc + 1), TileRef{(int)i, a * GBM, b * GBN, a * tn + b}});
+      }
+  }
+  std::stable_sort(all.begin(), all.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+  out.clear();
+  for (auto& x : all) out.push_back(x.second);
+}
+
+static int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
 template <int TA, int TB, int EPI>
-static cudaError_t launch_gemm(const GemmItem* items, int n, int tiles, GemmArgs a, cudaStream_t st) {
+static cudaError_t launch_gemm(const GemmItem* items, const ItemMaps* maps, const TileRef* tref, int n, int tiles,
+                              GemmArgs a, cudaStream_t st) {
   static std::mutex mu;
   static uint64_t done = 0;
   cudaError_t e = once_per_device(mu, done, [] {
@@ -414,10 +516,16 @@ static cudaError_t launch_gemm(const GemmItem* items, int n, int tiles, GemmArgs
                                          (int)G_SMEM);
     if (r == cudaSuccess)
       r = cudaFuncSetAttribute(zgemm3m_kernel<TA, TB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(zgemm3m_pt_kernel<TA, TB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)PT_SMEM);
     return r;
   });
   if (e != cudaSuccess) return e;
-  if (use_3m()) zgemm3m_kernel<TA, TB, EPI><<<tiles, G3THREADS, G_SMEM, st>>>(items, n, a);
+  if (use_3m() && maps && tref && staging() == 1)
+    zgemm3m_pt_kernel<TA, TB, EPI><<<std::min(tiles, sm_count()), PT_THREADS, PT_SMEM, st>>>(items, maps, tref,
+                                                                                             tiles, a);
+  else if (use_3m()) zgemm3m_kernel<TA, TB, EPI><<<tiles, G3THREADS, G_SMEM, st>>>(items, n, a);
   else zgemm_kernel<TA, TB, EPI><<<tiles, GTHREADS, G_SMEM, st>>>(items, n, a);
   return cudaGetLastError();
 }
@@ -464,9 +572,29 @@ static ListRef upload_list(std::vector<GemmItem>& v, std::vector<void*>& mem) {
   if (v.empty()) return ref;
   if (cudaMalloc(&ref.dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return ListRef{};
   cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
+  mem.push_back(ref.dev);
+  std::vector<ItemMaps> maps;
+  std::vector<TileRef> tref;
+  build_tiles(v, tref);
+  // short-K lists (cfg 2's ~100-dim blocks: ~13 K stages a tile) keep the per-tile kernel, whose two
+  // CTAs per SM hide each other's epilogues (r02 same-box A/B: cfg 2 41.1 vs 48.6 ms)
+  double kmean = 0.0;
+  for (auto& x : v) kmean += (double)x.k * x.nseg / v.size();
+  if (kmean >= kPersistentMinK && build_maps(v, maps) &&
+      cudaMalloc(&ref.maps, maps.size() * sizeof(ItemMaps)) == cudaSuccess &&
+      cudaMalloc(&ref.tref, tref.size() * sizeof(TileRef)) == cudaSuccess) {
+    cudaMemcpy(ref.maps, maps.data(), maps.size() * sizeof(ItemMaps), cudaMemcpyHostToDevice);
+    cudaMemcpy(ref.tref, tref.data(), tref.size() * sizeof(TileRef), cudaMemcpyHostToDevice);
+    mem.push_back(ref.maps);
+    mem.push_back(ref.tref);
+  } else {
+    (void)cudaGetLastError();
+    cudaFree(ref.maps);
+    ref.maps = nullptr;  // cp.async kernel for this list
+    ref.tref = nullptr;
+  }
   ref.n = (int)v.size();
   ref.tiles = t;
-  mem.push_back(ref.dev);
   return ref;
 }
 
@@ -589,11 +717,11 @@ static int gemm(LargeGroup& g, int op, int p, int q, int r, GemmArgs a, cudaStre
   gemm_begin(g, l, st);
   cudaError_t e;
   switch (op) {
-    case B_C: e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.n, l.tiles, a, st); break;
-    case B_D: e = launch_gemm<OP_C, OP_N, EPI_TRACE>(l.dev, l.n, l.tiles, a, st); break;
-    case B_XL: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st); break;
-    case B_UC: e = launch_gemm<OP_C, OP_N, EPI_MIXED>(l.dev, l.n, l.tiles, a, st); break;
-    default: e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st); break;
+    case B_C: e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st); break;
+    case B_D: e = launch_gemm<OP_C, OP_N, EPI_TRACE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st); break;
+    case B_XL: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st); break;
+    case B_UC: e = launch_gemm<OP_C, OP_N, EPI_MIXED>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st); break;
+    default: e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st); break;
   }
   gemm_end(g, st);
   if (e != cudaSuccess) {
@@ -873,9 +1001,9 @@ static int hgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArgs
   }
   cudaError_t e;
   gemm_begin(g, l, st);
-  if (op == H_L) e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
-  else if (op == H_B) e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
-  else e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
+  if (op == H_L) e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st);
+  else if (op == H_B) e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st);
+  else e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st);
   gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
@@ -952,8 +1080,8 @@ static int scan_gemm(LargeGroup& g, int op, int idx, int Lc, int C, cudaStream_t
   if (!l.n) return SQOC_OK;
   const GemmArgs one{1.0, 0.0, 0.0, 0.0};
   gemm_begin(g, l, st);
-  cudaError_t e = (op == H_LP1) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, one, st)
-                                : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, one, st);
+  cudaError_t e = (op == H_LP1) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, one, st)
+                                : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, one, st);
   gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
@@ -1120,8 +1248,8 @@ static int svgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArg
     return SQOC_ERR_CUDA;
   }
   gemm_begin(g, l, st);
-  cudaError_t e = (op == SV_CHI) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st)
-                                 : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.n, l.tiles, a, st);
+  cudaError_t e = (op == SV_CHI) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st)
+                                 : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st);
   gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
@@ -1420,8 +1548,27 @@ static int run_carry_steps(LargeGroup& g, std::vector<GemmItem>& items, const st
     }
   }
   GemmItem* dev = nullptr;
+  ItemMaps* maps = nullptr;
   LCHK(cudaMallocAsync(reinterpret_cast<void**>(&dev), items.size() * sizeof(GemmItem), st));
   LCHK(cudaMemcpyAsync(dev, items.data(), items.size() * sizeof(GemmItem), cudaMemcpyHostToDevice, st));
+  std::vector<ItemMaps> hmaps;
+  TileRef* trefs = nullptr;
+  std::vector<std::vector<TileRef>> step_tiles(steps.size());
+  size_t ntref = 0;
+  for (size_t q = 0; q < steps.size(); ++q) {  // tile lists per launch (items relative to the launch's first)
+    std::vector<GemmItem> sub(items.begin() + steps[q].first, items.begin() + steps[q].first + steps[q].n);
+    build_tiles(sub, step_tiles[q]);
+    ntref += step_tiles[q].size();
+  }
+  if (build_maps(items, hmaps)) {
+    LCHK(cudaMallocAsync(reinterpret_cast<void**>(&maps), hmaps.size() * sizeof(ItemMaps), st));
+    LCHK(cudaMemcpyAsync(maps, hmaps.data(), hmaps.size() * sizeof(ItemMaps), cudaMemcpyHostToDevice, st));
+    std::vector<TileRef> flat;
+    for (auto& t : step_tiles) flat.insert(flat.end(), t.begin(), t.end());
+    LCHK(cudaMallocAsync(reinterpret_cast<void**>(&trefs), ntref * sizeof(TileRef), st));
+    LCHK(cudaMemcpyAsync(trefs, flat.data(), ntref * sizeof(TileRef), cudaMemcpyHostToDevice, st));
+  }
+  size_t tref_off = 0;
   GemmArgs one{1.0, 0.0, 0.0, 0.0};
   for (auto& s : steps) {
     int tiles = 0;
@@ -1431,11 +1578,17 @@ static int run_carry_steps(LargeGroup& g, std::vector<GemmItem>& items, const st
       l.macs += (double)items[i].m * items[i].n * items[i].k;
     }
     gemm_begin(g, l, st);
-    cudaError_t e = s.ta == OP_C ? launch_gemm<OP_C, OP_N, EPI_STORE>(dev + s.first, (int)s.n, tiles, one, st)
-                                 : launch_gemm<OP_N, OP_N, EPI_STORE>(dev + s.first, (int)s.n, tiles, one, st);
+    const ItemMaps* mp = maps ? maps + s.first : nullptr;
+    const TileRef* tp = trefs ? trefs + tref_off : nullptr;
+    tref_off += (size_t)tiles;
+    cudaError_t e = s.ta == OP_C
+                        ? launch_gemm<OP_C, OP_N, EPI_STORE>(dev + s.first, mp, tp, (int)s.n, tiles, one, st)
+                        : launch_gemm<OP_N, OP_N, EPI_STORE>(dev + s.first, mp, tp, (int)s.n, tiles, one, st);
     gemm_end(g, st);
     if (e != cudaSuccess) {
       cudaFreeAsync(dev, st);
+      if (maps) cudaFreeAsync(maps, st);
+      if (trefs) cudaFreeAsync(trefs, st);
       g.err = std::string("carry zgemm launch: ") + cudaGetErrorString(e);
       return SQOC_ERR_CUDA;
     }
@@ -1443,6 +1596,8 @@ static int run_carry_steps(LargeGroup& g, std::vector<GemmItem>& items, const st
     g.carry_gemms++;
   }
   LCHK(cudaFreeAsync(dev, st));
+  if (maps) LCHK(cudaFreeAsync(maps, st));
+  if (trefs) LCHK(cudaFreeAsync(trefs, st));
   return SQOC_OK;
 }
 

@@ -26,7 +26,7 @@
 #include <tuple>
 #include <vector>
 
-#include "zgemm.cuh"
+#include "zgemm_tma.cuh"
 
 namespace sqoc {
 
@@ -51,6 +51,8 @@ struct LargeBlockSpec {
 
 struct ListRef {
   GemmItem* dev = nullptr;
+  ItemMaps* maps = nullptr;  // TMA tensor maps per item (null: cp.async staging)
+  TileRef* tref = nullptr;   // persistent kernel's tile list (cost-ordered)
   int n = 0, tiles = 0;
   double macs = 0.0;  // complex multiply-adds of the list (sum m n k nseg), for the executed-FLOP count
 };
@@ -152,6 +154,8 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st);
 int large_set_norms(LargeGroup& g, const std::vector<double>& gnorm);
 int large_set_complex_gemm(int mults);
 int large_complex_mults();  // 3 (Gauss) or 4
+int large_set_staging(int mode);  // 3M GEMM: 1 persistent TMA + mbarrier ring (default), 0 cp.async
+int large_staging();
 // Device time of the last evaluation's GEMM launches (needs g.timing during it).
 int large_gemm_time(LargeGroup& g, double* ms);
 // Device time of the last chunk phase 2's boundary-value formation (needs g.timing during it).

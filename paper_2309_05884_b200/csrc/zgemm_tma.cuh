@@ -1,0 +1,328 @@
+// Persistent, warp-specialised 3M complex FP64 GEMM with TMA staging (sm_100a).
+//
+// Same work lists, warp tiling (8 MMA warps of 32 x 16 on a 64 x 64 CTA tile), Gauss products
+// (T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi) on DMMA.8x8x4), sub-tile skipping at ragged
+// edges and epilogues as zgemm3m_kernel (zgemm.cuh); the operand staging and scheduling differ:
+//
+//   * one CTA per SM (grid = min(tiles, SMs)) walks a static tile list ordered by cost (largest
+//     first, dealt round-robin over the CTAs: an LPT-like balance of the 2-segment, full and edge
+//     tiles of all blocks of the launch);
+//   * one producer lane (thread 0, between its own MMA work) streams every K stage (8 complex k) of
+//     op(A) and op(B) of all the CTA's tiles into a ring of S stages by TMA (cp.async.bulk.tensor)
+//     from per-item tensor maps --
+//     out-of-range rows, columns and k are zero-filled by the TMA unit, so ragged edges need no
+//     predication -- running up to S - 2 stages ahead across tile boundaries, so the next tile's
+//     operands land while the MMA warps run the current tile's epilogue (8 warps, 2 per SM
+//     sub-partition: up to 255 registers, room for a two-deep fragment pipeline);
+//   * a "full" mbarrier per stage (armed with the 16 KB byte count) and an "empty" mbarrier (one
+//     arrival per MMA warp): no block-wide barrier in the main loop, warps drift within the ring;
+//   * dense 128-byte rows with the 128B swizzle (16-byte chunk c of row r stored at c ^ (r & 7)).
+//     Row-major operands ([m][k], op(B) = B^dag as [n][k]) are one 64-row box; k-major operands
+//     ([k][n], op(A) = A^dag as [k][m]) are eight 8 x 8 boxes, one per 8-column block.  With the
+//     swizzle, lane (r, c) of a DMMA fragment reads k = 2c + s for k-step s: every 8-lane phase
+//     of an LDS.128 touches 8 distinct 16-byte bank groups (conflict-free), for both layouts.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "zgemm.cuh"
+
+namespace sqoc {
+
+constexpr int PT_STAGES = 12;
+constexpr int TMA_STAGE_BYTES = 2 * GBM * 8 * 16;  // A + B tiles: 64 x 8 complex each
+constexpr size_t PT_SMEM = (size_t)PT_STAGES * TMA_STAGE_BYTES + 2 * PT_STAGES * 8 + 1024;  // ring + barriers + align
+
+// per work-list item and K segment: tensor maps of A and B in both staging orientations
+// (m[4 seg + 0] A as [m][k], + 1 A as [k][m] (op = conj-transpose), + 2 B as [k][n], + 3 B as [n][k]);
+// unused ones zero
+struct alignas(64) ItemMaps {
+  CUtensorMap m[8];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Issue the TMA copies of K stage kt (segment and k0 from kt) into ring slot `st`.
+template <int TA, int TB>
+__device__ __forceinline__ void tma_issue_stage(const ItemMaps* mp, const GemmItem& it, int kt, int kt_per_seg,
+                                                int m0, int n0, uint8_t* slot, uint64_t* full) {
+  const int seg = kt / kt_per_seg;
+  const int k0 = (kt - seg * kt_per_seg) * GBK;
+  const CUtensorMap* ma = &mp->m[4 * seg + (TA == OP_N ? 0 : 1)];
+  const CUtensorMap* mb = &mp->m[4 * seg + (TB == OP_N ? 2 : 3)];
+  uint8_t* sA = slot;
+  uint8_t* sB = slot + GBM * 8 * 16;
+  mbar_arrive_expect(full, TMA_STAGE_BYTES);
+  if (TA == OP_N) tma_load_2d(sA, ma, 2 * k0, m0, full);  // [m][k]: one 64-row box
+  else
+#pragma unroll
+    for (int b = 0; b < GBM / 8; ++b) tma_load_2d(sA + b * 1024, ma, 2 * (m0 + 8 * b), k0, full);  // [k][m] blocks
+  if (TB == OP_N)
+#pragma unroll
+    for (int b = 0; b < GBN / 8; ++b) tma_load_2d(sB + b * 1024, mb, 2 * (n0 + 8 * b), k0, full);  // [k][n] blocks
+  else tma_load_2d(sB, mb, 2 * k0, n0, full);  // [n][k]: one 64-row box
+}
+
+
+struct TileRef {
+  int item, m0, n0, local;  // work-list item, tile origin, tile index inside the item (trace partials)
+};
+
+// The producer's cursor over (tile, K stage) of this CTA's tile sequence; lives in thread 0 only.
+struct Producer {
+  const GemmItem* items;
+  const ItemMaps* maps;
+  const TileRef* tiles;
+  int ntiles;
+  int t, kt, kt_total, kt_per_seg, m0, n0;
+  const GemmItem* it;
+  const ItemMaps* mp;
+  uint32_t g;  // stages issued so far
+
+  __device__ __forceinline__ void load_tile() {
+    if (t >= ntiles) return;
+    const TileRef tr = tiles[t];
+    it = items + tr.item;
+    mp = maps + tr.item;
+    m0 = tr.m0;
+    n0 = tr.n0;
+    kt_per_seg = (it->k + GBK - 1) / GBK;
+    kt_total = kt_per_seg * it->nseg;
+    kt = 0;
+  }
+  // issue stages until `upto` stages have been issued (or the tiles run out), waiting for each slot's
+  // release by the 8 MMA warps PT_STAGES stages earlier
+  template <int TA, int TB>
+  __device__ __forceinline__ void advance(uint32_t upto, uint8_t* ring, uint64_t* full, uint64_t* empty) {
+    while (g < upto && t < ntiles) {
+      const uint32_t slot = g % PT_STAGES;
+      if (g >= PT_STAGES) mbar_wait(&empty[slot], ((g / PT_STAGES) - 1) & 1);
+      tma_issue_stage<TA, TB>(mp, *it, kt, kt_per_seg, m0, n0, ring + slot * TMA_STAGE_BYTES, &full[slot]);
+      ++g;
+      if (++kt == kt_total) {
+        t += gridDim.x;
+        load_tile();
+      }
+    }
+  }
+};
+
+// One k-step's fragments (k = 2 lc + s of a stage) with the Gauss operand sums precomputed.
+template <int MC, int NC>
+struct Frag {
+  double ar[MC > 0 ? MC : 1], ai[MC > 0 ? MC : 1], as[MC > 0 ? MC : 1];
+  double br[NC > 0 ? NC : 1], bi[NC > 0 ? NC : 1], bs[NC > 0 ? NC : 1];
+};
+
+template <int TA, int TB, int MC, int NC>
+__device__ __forceinline__ void frag_load(Frag<MC, NC>& f, const uint8_t* stage, int oa, int ob) {
+  constexpr int A_MI = (TA == OP_N) ? 8 * 128 : 1024;  // byte stride between the warp's 8-row sub-tiles
+  constexpr int B_NI = (TB == OP_N) ? 1024 : 8 * 128;
+  const uint8_t* sA = stage;
+  const uint8_t* sB = stage + GBM * 8 * 16;
+#pragma unroll
+  for (int mi = 0; mi < MC; ++mi) {
+    double2 a = *reinterpret_cast<const double2*>(sA + oa + mi * A_MI);
+    if (TA == OP_C) a.y = -a.y;
+    f.ar[mi] = a.x; f.ai[mi] = a.y; f.as[mi] = a.x + a.y;
+  }
+#pragma unroll
+  for (int ni = 0; ni < NC; ++ni) {
+    double2 b = *reinterpret_cast<const double2*>(sB + ob + ni * B_NI);
+    if (TB == OP_C) b.y = -b.y;
+    f.br[ni] = b.x; f.bi[ni] = b.y; f.bs[ni] = b.x + b.y;
+  }
+}
+
+template <int MC, int NC>
+__device__ __forceinline__ void frag_mma(double (&acc)[4][2][3][2], const Frag<MC, NC>& f) {
+#pragma unroll
+  for (int mi = 0; mi < MC; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NC; ++ni) {
+      dmma(acc[mi][ni][0][0], acc[mi][ni][0][1], f.ar[mi], f.br[ni]);
+      dmma(acc[mi][ni][1][0], acc[mi][ni][1][1], f.ai[mi], f.bi[ni]);
+      dmma(acc[mi][ni][2][0], acc[mi][ni][2][1], f.as[mi], f.bs[ni]);
+    }
+}
+
+// kt_total K stages of one tile for a warp whose valid output is MC x NC DMMA sub-tiles; every warp
+// waits for and releases every stage (8 releases per slot).  r02 same-box A/B (cfg 3 / cfg 4 ms per
+// slice): this plain loop 102.1 / 83.0; a two-deep register pipeline of the fragments 106.2 / 87.0
+// (the 168-register cap of 9 warps spills); the producer fused into thread 0 (256 threads) 142 / 112.
+template <int TA, int TB, int MC, int NC>
+__device__ __forceinline__ void pt_mainloop(double (&acc)[4][2][3][2], const uint8_t* ring, uint64_t* full,
+                                            uint64_t* empty, uint32_t& g, int kt_total, const int (&offa)[2],
+                                            const int (&offb)[2], int lane) {
+  for (int kt = 0; kt < kt_total; ++kt, ++g) {
+    const uint32_t slot = g % PT_STAGES;
+    mbar_wait(&full[slot], (g / PT_STAGES) & 1);
+    if constexpr (MC > 0 && NC > 0) {
+      Frag<MC, NC> f;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        frag_load<TA, TB>(f, ring + slot * TMA_STAGE_BYTES, offa[s], offb[s]);
+        frag_mma(acc, f);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+}
+
+constexpr int PT_THREADS = G3THREADS + 32;  // 8 MMA warps + 1 producer warp
+
+template <int TA, int TB, int EPI>
+__global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmItem* __restrict__ items,
+                                                                   const ItemMaps* __restrict__ maps,
+                                                                   const TileRef* __restrict__ tiles, int ntiles,
+                                                                   GemmArgs args) {
+  extern __shared__ uint8_t tsm_raw[];
+  __shared__ double2 red[G3THREADS / 32][4];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + PT_STAGES * TMA_STAGE_BYTES);
+  uint64_t* empty = full + PT_STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PT_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], G3THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == G3THREADS / 32) {  // producer warp: one lane streams every stage of every tile of this CTA
+    if (lane == 0) {
+      Producer prod;
+      prod.items = items;
+      prod.maps = maps;
+      prod.tiles = tiles;
+      prod.ntiles = ntiles;
+      prod.t = blockIdx.x;
+      prod.g = 0;
+      prod.load_tile();
+      prod.advance<TA, TB>(0xffffffffu, ring, full, empty);
+    }
+    return;
+  }
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+  const int lr = lane >> 2, lc = lane & 3;
+  int offa[2], offb[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int k = 2 * lc + s;
+    const int rowmaj = lr * 128 + ((k ^ lr) << 4);  // [row][k]: row * 128 + ((k ^ (row & 7)) * 16)
+    const int kmaj = k * 128 + ((lr ^ k) << 4);     // [k][col] 8 x 8 blocks: k * 128 + (((col & 7) ^ k) * 16)
+    offa[s] = (TA == OP_N ? rowmaj + wm * 128 : kmaj + (wm >> 3) * 1024);
+    offb[s] = (TB == OP_N ? kmaj + (wn >> 3) * 1024 : rowmaj + wn * 128);
+  }
+  uint32_t g = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const TileRef tr = tiles[t];
+    const GemmItem& it = items[tr.item];
+    const int m0 = tr.m0, n0 = tr.n0;
+    const int kt_total = ((it.k + GBK - 1) / GBK) * it.nseg;
+    double acc[4][2][3][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
+    const int mc = max(0, min(4, (it.m - m0 - wm + 7) / 8));
+    const int nc = max(0, min(2, (it.n - n0 - wn + 7) / 8));
+    switch ((mc == 0 || nc == 0) ? -1 : (mc - 1) * 2 + (nc - 1)) {
+      case 7: pt_mainloop<TA, TB, 4, 2>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
+      case 6: pt_mainloop<TA, TB, 4, 1>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
+      case 5: pt_mainloop<TA, TB, 3, 2>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
+      case 4: pt_mainloop<TA, TB, 3, 1>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
+      case 3: pt_mainloop<TA, TB, 2, 2>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
+      case 2: pt_mainloop<TA, TB, 2, 1>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
+      case 1: pt_mainloop<TA, TB, 1, 2>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
+      case 0: pt_mainloop<TA, TB, 1, 1>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
+      default: pt_mainloop<TA, TB, 0, 0>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
+    }
+    const bool trace = EPI == EPI_TRACE || (EPI == EPI_MIXED && it.nF > 0);  // uniform per tile
+    if (!trace) {
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int m = m0 + wm + mi * 8 + lr;
+            const int n = n0 + wn + ni * 8 + 2 * lc + v;
+            if (m < it.m && n < it.n) {
+              const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
+              epi_store(it, args, m, n, t1 - t2, t3 - t1 - t2);
+            }
+          }
+    } else {
+      const int nF = it.nF;
+      for (int f = 0; f < nF; ++f) {
+        const double2* F = it.F + f * it.fstride;
+        double sx = 0.0, sy = 0.0;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int p = m0 + wm + mi * 8 + lr;
+              const int q = n0 + wn + ni * 8 + 2 * lc + v;
+              if (p < it.m && q < it.n) {
+                const double2 e = F[(size_t)q * it.ldc + p];
+                const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
+                const double cr = args.alpha * (t1 - t2), ci = args.alpha * (t3 - t1 - t2);
+                sx += cr * e.x - ci * e.y;
+                sy += cr * e.y + ci * e.x;
+              }
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          sx += __shfl_xor_sync(0xffffffffu, sx, o);
+          sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        }
+        if (lane == 0) red[warp][f] = make_double2(sx, sy);
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(G3THREADS) : "memory");
+      if (threadIdx.x < nF) {
+        double2 s = make_double2(0.0, 0.0);
+        for (int w = 0; w < G3THREADS / 32; ++w) { s.x += red[w][threadIdx.x].x; s.y += red[w][threadIdx.x].y; }
+        it.tr_out[(size_t)tr.local * nF + threadIdx.x] = s;
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(G3THREADS) : "memory");  // red[] reused by the next trace tile
+    }
+  }
+}
+
+}  // namespace sqoc
