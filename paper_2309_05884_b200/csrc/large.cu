@@ -507,8 +507,8 @@ static int sm_count() {
 }
 
 template <int TA, int TB, int EPI>
-static cudaError_t launch_gemm(const GemmItem* items, const ItemMaps* maps, const TileRef* tref, int n, int tiles,
-                              GemmArgs a, cudaStream_t st) {
+static cudaError_t launch_gemm(const GemmItem* items, const ItemMaps* maps, const TileRef* tref, int* counter, int n,
+                              int tiles, GemmArgs a, cudaStream_t st) {
   static std::mutex mu;
   static uint64_t done = 0;
   cudaError_t e = once_per_device(mu, done, [] {
@@ -522,10 +522,12 @@ static cudaError_t launch_gemm(const GemmItem* items, const ItemMaps* maps, cons
     return r;
   });
   if (e != cudaSuccess) return e;
-  if (use_3m() && maps && tref && staging() == 1)
+  if (use_3m() && maps && tref && counter && staging() == 1) {
+    e = cudaMemsetAsync(counter, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
     zgemm3m_pt_kernel<TA, TB, EPI><<<std::min(tiles, sm_count()), PT_THREADS, PT_SMEM, st>>>(items, maps, tref,
-                                                                                             tiles, a);
-  else if (use_3m()) zgemm3m_kernel<TA, TB, EPI><<<tiles, G3THREADS, G_SMEM, st>>>(items, n, a);
+                                                                                             tiles, counter, a);
+  } else if (use_3m()) zgemm3m_kernel<TA, TB, EPI><<<tiles, G3THREADS, G_SMEM, st>>>(items, n, a);
   else zgemm_kernel<TA, TB, EPI><<<tiles, GTHREADS, G_SMEM, st>>>(items, n, a);
   return cudaGetLastError();
 }
@@ -717,11 +719,11 @@ static int gemm(LargeGroup& g, int op, int p, int q, int r, GemmArgs a, cudaStre
   gemm_begin(g, l, st);
   cudaError_t e;
   switch (op) {
-    case B_C: e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st); break;
-    case B_D: e = launch_gemm<OP_C, OP_N, EPI_TRACE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st); break;
-    case B_XL: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st); break;
-    case B_UC: e = launch_gemm<OP_C, OP_N, EPI_MIXED>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st); break;
-    default: e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st); break;
+    case B_C: e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
+    case B_D: e = launch_gemm<OP_C, OP_N, EPI_TRACE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
+    case B_XL: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
+    case B_UC: e = launch_gemm<OP_C, OP_N, EPI_MIXED>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
+    default: e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
   }
   gemm_end(g, st);
   if (e != cudaSuccess) {
@@ -763,6 +765,7 @@ int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, 
   LCHK(cudaMalloc(&g.trace_part, (size_t)g.trace_tiles * K * sizeof(double2)));
   LCHK(cudaMalloc(&g.tau_dev, g.nblk * sizeof(double2)));
   LCHK(cudaMalloc(&g.norm_dev, sizeof(double)));
+  LCHK(cudaMalloc(&g.pt_counter, sizeof(int)));
   std::vector<double> gn, w;
   std::vector<int> dims, gidx;
   std::vector<const double2*> gen, tgt, x0;
@@ -846,6 +849,7 @@ void large_free(LargeGroup& g) {
     cudaFree(g.dxs[i]);
   }
   cudaFree(g.norm_dev);
+  cudaFree(g.pt_counter);
   cudaFree(g.gnorm_dev);
   cudaFree(g.d_dev);
   cudaFree(g.off_dev);
@@ -1001,9 +1005,9 @@ static int hgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArgs
   }
   cudaError_t e;
   gemm_begin(g, l, st);
-  if (op == H_L) e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st);
-  else if (op == H_B) e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st);
-  else e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st);
+  if (op == H_L) e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st);
+  else if (op == H_B) e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st);
+  else e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st);
   gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
@@ -1080,8 +1084,8 @@ static int scan_gemm(LargeGroup& g, int op, int idx, int Lc, int C, cudaStream_t
   if (!l.n) return SQOC_OK;
   const GemmArgs one{1.0, 0.0, 0.0, 0.0};
   gemm_begin(g, l, st);
-  cudaError_t e = (op == H_LP1) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, one, st)
-                                : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, one, st);
+  cudaError_t e = (op == H_LP1) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, one, st)
+                                : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, one, st);
   gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
@@ -1248,8 +1252,8 @@ static int svgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArg
     return SQOC_ERR_CUDA;
   }
   gemm_begin(g, l, st);
-  cudaError_t e = (op == SV_CHI) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st)
-                                 : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, l.n, l.tiles, a, st);
+  cudaError_t e = (op == SV_CHI) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st)
+                                 : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st);
   gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
@@ -1582,8 +1586,8 @@ static int run_carry_steps(LargeGroup& g, std::vector<GemmItem>& items, const st
     const TileRef* tp = trefs ? trefs + tref_off : nullptr;
     tref_off += (size_t)tiles;
     cudaError_t e = s.ta == OP_C
-                        ? launch_gemm<OP_C, OP_N, EPI_STORE>(dev + s.first, mp, tp, (int)s.n, tiles, one, st)
-                        : launch_gemm<OP_N, OP_N, EPI_STORE>(dev + s.first, mp, tp, (int)s.n, tiles, one, st);
+                        ? launch_gemm<OP_C, OP_N, EPI_STORE>(dev + s.first, mp, tp, g.pt_counter, (int)s.n, tiles, one, st)
+                        : launch_gemm<OP_N, OP_N, EPI_STORE>(dev + s.first, mp, tp, g.pt_counter, (int)s.n, tiles, one, st);
     gemm_end(g, st);
     if (e != cudaSuccess) {
       cudaFreeAsync(dev, st);

@@ -73,6 +73,7 @@ struct LargeGroup {
   int trace_tiles = 0;
   double2* tau_dev = nullptr;     // [nblk]
   double* norm_dev = nullptr;     // scalar (max bound)
+  int* pt_counter = nullptr;      // persistent GEMM's dynamic tile counter (zeroed before each launch)
   double* gnorm_dev = nullptr;    // [nblk][K+1]
   // device copies of per-block info for elementwise kernels
   int* d_dev = nullptr;

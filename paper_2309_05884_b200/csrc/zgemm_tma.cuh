@@ -4,16 +4,15 @@
 // (T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi) on DMMA.8x8x4), sub-tile skipping at ragged
 // edges and epilogues as zgemm3m_kernel (zgemm.cuh); the operand staging and scheduling differ:
 //
-//   * one CTA per SM (grid = min(tiles, SMs)) walks a static tile list ordered by cost (largest
-//     first, dealt round-robin over the CTAs: an LPT-like balance of the 2-segment, full and edge
-//     tiles of all blocks of the launch);
-//   * one producer lane (thread 0, between its own MMA work) streams every K stage (8 complex k) of
-//     op(A) and op(B) of all the CTA's tiles into a ring of S stages by TMA (cp.async.bulk.tensor)
-//     from per-item tensor maps --
+//   * one CTA per SM (grid = min(tiles, SMs)) takes tiles from a list ordered by cost (largest
+//     first), claimed dynamically through a global counter: list scheduling that lets faster SMs
+//     (e.g. those closer to the L2 half holding the operands) absorb the tail;
+//   * a producer warp streams every K stage (8 complex k) of op(A) and op(B) of the CTA's tiles into
+//     a ring of S stages by TMA (cp.async.bulk.tensor, one lane) from per-item tensor maps --
 //     out-of-range rows, columns and k are zero-filled by the TMA unit, so ragged edges need no
-//     predication -- running up to S - 2 stages ahead across tile boundaries, so the next tile's
-//     operands land while the MMA warps run the current tile's epilogue (8 warps, 2 per SM
-//     sub-partition: up to 255 registers, room for a two-deep fragment pipeline);
+//     predication -- running up to S stages ahead across tile boundaries, so the next tile's operands
+//     land while the MMA warps run the current tile's epilogue; the tile index rides with the first
+//     stage of each tile;
 //   * a "full" mbarrier per stage (armed with the 16 KB byte count) and an "empty" mbarrier (one
 //     arrival per MMA warp): no block-wide barrier in the main loop, warps drift within the ring;
 //   * dense 128-byte rows with the 128B swizzle (16-byte chunk c of row r stored at c ^ (r & 7)).
@@ -96,45 +95,6 @@ struct TileRef {
   int item, m0, n0, local;  // work-list item, tile origin, tile index inside the item (trace partials)
 };
 
-// The producer's cursor over (tile, K stage) of this CTA's tile sequence; lives in thread 0 only.
-struct Producer {
-  const GemmItem* items;
-  const ItemMaps* maps;
-  const TileRef* tiles;
-  int ntiles;
-  int t, kt, kt_total, kt_per_seg, m0, n0;
-  const GemmItem* it;
-  const ItemMaps* mp;
-  uint32_t g;  // stages issued so far
-
-  __device__ __forceinline__ void load_tile() {
-    if (t >= ntiles) return;
-    const TileRef tr = tiles[t];
-    it = items + tr.item;
-    mp = maps + tr.item;
-    m0 = tr.m0;
-    n0 = tr.n0;
-    kt_per_seg = (it->k + GBK - 1) / GBK;
-    kt_total = kt_per_seg * it->nseg;
-    kt = 0;
-  }
-  // issue stages until `upto` stages have been issued (or the tiles run out), waiting for each slot's
-  // release by the 8 MMA warps PT_STAGES stages earlier
-  template <int TA, int TB>
-  __device__ __forceinline__ void advance(uint32_t upto, uint8_t* ring, uint64_t* full, uint64_t* empty) {
-    while (g < upto && t < ntiles) {
-      const uint32_t slot = g % PT_STAGES;
-      if (g >= PT_STAGES) mbar_wait(&empty[slot], ((g / PT_STAGES) - 1) & 1);
-      tma_issue_stage<TA, TB>(mp, *it, kt, kt_per_seg, m0, n0, ring + slot * TMA_STAGE_BYTES, &full[slot]);
-      ++g;
-      if (++kt == kt_total) {
-        t += gridDim.x;
-        load_tile();
-      }
-    }
-  }
-};
-
 // One k-step's fragments (k = 2 lc + s of a stage) with the Gauss operand sums precomputed.
 template <int MC, int NC>
 struct Frag {
@@ -204,9 +164,10 @@ template <int TA, int TB, int EPI>
 __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmItem* __restrict__ items,
                                                                    const ItemMaps* __restrict__ maps,
                                                                    const TileRef* __restrict__ tiles, int ntiles,
-                                                                   GemmArgs args) {
+                                                                   int* __restrict__ counter, GemmArgs args) {
   extern __shared__ uint8_t tsm_raw[];
   __shared__ double2 red[G3THREADS / 32][4];
+  __shared__ int stage_tile[PT_STAGES];  // tile index announced with a tile's first stage; -1 = done
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + PT_STAGES * TMA_STAGE_BYTES);
   uint64_t* empty = full + PT_STAGES;
@@ -220,17 +181,34 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
   }
   __syncthreads();
 
-  if (warp == G3THREADS / 32) {  // producer warp: one lane streams every stage of every tile of this CTA
+  if (warp == G3THREADS / 32) {
+    // ---- producer warp: one lane streams every stage of every tile this CTA takes.  Tiles are
+    // claimed dynamically (first blockIdx.x, then gridDim.x + atomicAdd) from the cost-ordered list,
+    // so faster SMs take more of the tail (largest-first list scheduling) ----
     if (lane == 0) {
-      Producer prod;
-      prod.items = items;
-      prod.maps = maps;
-      prod.tiles = tiles;
-      prod.ntiles = ntiles;
-      prod.t = blockIdx.x;
-      prod.g = 0;
-      prod.load_tile();
-      prod.advance<TA, TB>(0xffffffffu, ring, full, empty);
+      uint32_t g = 0;
+      int t = blockIdx.x;
+      while (true) {
+        if (t >= ntiles) {  // announce the end through one more (empty) stage
+          const uint32_t slot = g % PT_STAGES;
+          if (g >= PT_STAGES) mbar_wait(&empty[slot], ((g / PT_STAGES) - 1) & 1);
+          stage_tile[slot] = -1;
+          mbar_arrive(&full[slot]);
+          break;
+        }
+        const TileRef tr = tiles[t];
+        const GemmItem& it = items[tr.item];
+        const ItemMaps* mp = maps + tr.item;
+        const int kt_per_seg = (it.k + GBK - 1) / GBK;
+        const int kt_total = kt_per_seg * it.nseg;
+        for (int kt = 0; kt < kt_total; ++kt, ++g) {
+          const uint32_t slot = g % PT_STAGES;
+          if (g >= PT_STAGES) mbar_wait(&empty[slot], ((g / PT_STAGES) - 1) & 1);
+          if (kt == 0) stage_tile[slot] = t;
+          tma_issue_stage<TA, TB>(mp, it, kt, kt_per_seg, tr.m0, tr.n0, ring + slot * TMA_STAGE_BYTES, &full[slot]);
+        }
+        t = gridDim.x + atomicAdd(counter, 1);
+      }
     }
     return;
   }
@@ -246,7 +224,10 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
     offb[s] = (TB == OP_N ? kmaj + (wn >> 3) * 1024 : rowmaj + wn * 128);
   }
   uint32_t g = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  while (true) {
+    mbar_wait(&full[g % PT_STAGES], (g / PT_STAGES) & 1);
+    const int t = *reinterpret_cast<volatile int*>(&stage_tile[g % PT_STAGES]);
+    if (t < 0) break;
     const TileRef tr = tiles[t];
     const GemmItem& it = items[tr.item];
     const int m0 = tr.m0, n0 = tr.n0;

@@ -5,6 +5,8 @@
 //   v1  + LDS.128 fragment loads per k-step (6 per 24 DMMA)
 //   v2  + the 3M operand sums (6 DADD per k-step)
 //   v3  + a __syncthreads every 2 k-steps (the cp.async kernel's per-stage barrier)
+//   v4  the v2 DADDs, but their results feed a side accumulator instead of the DMMAs (pipe sharing
+//       without the LDS -> DADD -> DMMA dependency)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/dmma_loop_probe tools/dmma_loop_probe.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -34,6 +36,7 @@ __global__ void __launch_bounds__(256, MINB) loop_kernel(double* out, int iters)
 #pragma unroll
       for (int c = 0; c < 3; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
   double ar[4], ai[4], as[4], br[2], bi[2], bs[2];
+  double side = 0.0;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) { ar[mi] = sA[lane + mi].x; ai[mi] = sA[lane + mi].y; as[mi] = ar[mi] + ai[mi]; }
 #pragma unroll
@@ -47,13 +50,15 @@ __global__ void __launch_bounds__(256, MINB) loop_kernel(double* out, int iters)
         for (int mi = 0; mi < 4; ++mi) {
           const double2 a = sA[(base + lane + mi * 37) & 1023];
           ar[mi] = a.x; ai[mi] = a.y;
-          as[mi] = V >= 2 ? a.x + a.y : a.x;
+          as[mi] = (V >= 2 && V != 4) ? a.x + a.y : a.x;
+          if (V == 4) side += a.x + a.y;
         }
 #pragma unroll
         for (int ni = 0; ni < 2; ++ni) {
           const double2 b = sB[(base + lane + ni * 41) & 1023];
           br[ni] = b.x; bi[ni] = b.y;
-          bs[ni] = V >= 2 ? b.x + b.y : b.y;
+          bs[ni] = (V >= 2 && V != 4) ? b.x + b.y : b.y;
+          if (V == 4) side += b.x + b.y;
         }
       }
 #pragma unroll
@@ -65,7 +70,7 @@ __global__ void __launch_bounds__(256, MINB) loop_kernel(double* out, int iters)
           dmma(acc[mi][ni][2][0], acc[mi][ni][2][1], as[mi], bs[ni]);
         }
     }
-    if (V >= 3) __syncthreads();
+    if (V == 3) __syncthreads();
   }
   double s = 0;
 #pragma unroll
@@ -74,7 +79,7 @@ __global__ void __launch_bounds__(256, MINB) loop_kernel(double* out, int iters)
     for (int b = 0; b < 2; ++b)
 #pragma unroll
       for (int c = 0; c < 3; ++c) s += acc[a][b][c][0] + acc[a][b][c][1];
-  if (s == 12345.678) out[0] = s;
+  if (s + side == 12345.678) out[0] = s;
 }
 
 template <int V, int MINB>
@@ -101,7 +106,7 @@ int main() {
   CK(cudaMalloc(&d, 8));
   int sms;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  run<0, 2>(sms, d); run<1, 2>(sms, d); run<2, 2>(sms, d); run<3, 2>(sms, d);
-  run<0, 1>(sms, d); run<1, 1>(sms, d); run<2, 1>(sms, d); run<3, 1>(sms, d);
+  run<0, 2>(sms, d); run<1, 2>(sms, d); run<2, 2>(sms, d); run<3, 2>(sms, d); run<4, 2>(sms, d);
+  run<0, 1>(sms, d); run<1, 1>(sms, d); run<2, 1>(sms, d); run<3, 1>(sms, d); run<4, 1>(sms, d);
   return 0;
 }
