@@ -327,6 +327,25 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
         }
         ls.gen_norm[k] = best;
       }
+      // union pattern of a_0..a_K (exact nonzeros; no threshold) and the values on it
+      ls.sp_rp.assign(d + 1, 0);
+      for (int i = 0; i < d; ++i) {
+        for (int c = 0; c < d; ++c) {
+          bool nz = false;
+          for (int k = 0; k <= n_controls && !nz; ++k) {
+            const double2 z = g[(size_t)k * d * d + (size_t)i * d + c];
+            nz = z.x != 0.0 || z.y != 0.0;
+          }
+          if (nz) ls.sp_ci.push_back(c);
+        }
+        ls.sp_rp[i + 1] = (int)ls.sp_ci.size();
+      }
+      const size_t nnz = ls.sp_ci.size();
+      ls.sp_gv.resize((size_t)(n_controls + 1) * nnz);
+      for (int k = 0; k <= n_controls; ++k)
+        for (int i = 0; i < d; ++i)
+          for (int e = ls.sp_rp[i]; e < ls.sp_rp[i + 1]; ++e)
+            ls.sp_gv[(size_t)k * nnz + e] = g[(size_t)k * d * d + (size_t)i * d + ls.sp_ci[e]];
       large_specs.push_back(ls);
     }
   }

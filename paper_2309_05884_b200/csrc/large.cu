@@ -602,7 +602,7 @@ static ListRef upload_list(std::vector<GemmItem>& v, std::vector<void*>& mem) {
 
 // Sequential schedule ops.  Gate objective: B_UC = [M = U^dag Ad | trace Tr(U^dag dT E_k)] in one
 // launch, B_CU: Ad = M U.  State objective: B_C, B_D, B_XL (vector X / Lam).
-enum Op { F_STEP, F_S, F_X, B_C, B_STEP, B_S, B_D, B_XL, B_UC, B_CU };
+enum Op { F_STEP, F_S, F_X, B_C, B_STEP, B_S, B_D, B_XL, B_UC, B_CU, B_STEP1D, B_M };
 
 static GemmItem mk(const double2* A0, const double2* B0, const double2* A1, const double2* B1, double2* C,
                    const double2* E0, const double2* E1, int m, int n, int k, int nseg, int lda, int ldb, int ldc,
@@ -703,6 +703,14 @@ static ListRef get_list(LargeGroup& g, int op, int p, int q, int r) {
       case B_CU:  // gate: Ad = M U
         v.push_back(mk(g.X[0] + orr, Tp, 0, 0, Ad, 0, 0, d, d, d, 1, d, d, d, 0));
         break;
+      case B_M:  // gate, sparse trace: M (in X[0]) = U^dag Ad only (the trace runs in sp_trace_kernel)
+        v.push_back(mk(Tp, Ad, 0, 0, g.X[0] + orr, 0, 0, d, d, d, 1, d, d, d, 0));
+        break;
+      case B_STEP1D: {  // sparse step 1's dense derivative term: dslot(out) = slot(L) dslot(R)
+        const PolyStep& st1 = scheme_of(q).step[1];
+        v.push_back(mk(slot(st1.L), dslot(st1.R), 0, 0, dslot(st1.out[0].slot), 0, 0, d, d, d, 1, d, d, d, 0));
+        break;
+      }
     }
   }
   ListRef ref = upload_list(v, g.list_mem);
@@ -723,6 +731,7 @@ static int gemm(LargeGroup& g, int op, int p, int q, int r, GemmArgs a, cudaStre
     case B_D: e = launch_gemm<OP_C, OP_N, EPI_TRACE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
     case B_XL: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
     case B_UC: e = launch_gemm<OP_C, OP_N, EPI_MIXED>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
+    case B_M: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
     default: e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
   }
   gemm_end(g, st);
@@ -731,6 +740,249 @@ static int gemm(LargeGroup& g, int op, int p, int q, int r, GemmArgs a, cudaStre
     return SQOC_ERR_CUDA;
   }
   g.launches++;
+  return SQOC_OK;
+}
+
+// ------------------------------------------------------------------ sparse-generator products
+// Scheme steps 0 (A2 = A A) and 1 (A3 = A2 A, + P) of both schemes have A as a factor: with the
+// sparse A_j they run in spmm_cols_kernel (S D) / spmm_rows_kernel (D S) (sparse.cuh), same epilogues
+// as push_step.  Work lists:
+//   SP_F0  forward step 0:  A2 = S A                                      (cols)
+//   SP_F1  forward step 1:  A3, P = A2 S                                  (rows)
+//   SP_B0R backward step 0, first half of the derivative: dA2 = dA S      (rows, raw store)
+//   SP_B0C backward step 0: A2 = S A; dA2 = S dA + dA2 (+ epilogue)       (cols)
+//   SP_B1  backward step 1: A3, P = A2 S; dA3, dP = dA2 S + dA3           (rows; dA3 holds the dense
+//          GEMM term A2 dA from B_STEP1D)
+enum SpOp { SP_F0, SP_F1, SP_B0R, SP_B0C, SP_B1 };
+
+static SpListRef sp_list(LargeGroup& g, int op, int degree) {
+  auto key = std::make_tuple(op, degree, 0, 0);
+  auto found = g.splists.find(key);
+  if (found != g.splists.end()) return found->second;
+  const int k = (op == SP_F1 || op == SP_B1) ? 1 : 0;
+  const PolyStep& st = scheme_of(degree).step[k];
+  bool used[4] = {false, false, false, false};
+  for (int o = 0; o < st.nout; ++o)
+    for (int t = 0; t < 4; ++t) used[t] = used[t] || st.out[o].beta[t] != 0.0;
+  std::vector<SpItem> v;
+  int tiles = 0;
+  for (int b = 0; b < g.nblk; ++b) {
+    const int d = g.blocks[b].d;
+    const size_t o = g.off[b];
+    auto slot = [&](int c) -> double2* {
+      switch (c) {
+        case 0: return g.A + o;
+        case 1: return g.A2 + o;
+        case 2: return g.A3 + o;
+        case kSlotY: return g.T[0] + o;
+        default: return g.xs[c - 3] + o;
+      }
+    };
+    auto dslot = [&](int c) -> double2* {
+      switch (c) {
+        case 0: return g.Ad + o;
+        case 1: return g.dA2 + o;
+        case 2: return g.dA3 + o;
+        case kSlotY: return g.dT[0] + o;
+        default: return g.dxs[c - 3] + o;
+      }
+    };
+    auto item = [&](bool der, const double2* D, bool raw, bool add_x) {
+      SpItem it{};
+      it.blk = b;
+      it.D = D;
+      it.C = der ? dslot(st.out[0].slot) : slot(st.out[0].slot);
+      it.add_x = add_x ? 1 : 0;
+      it.X = add_x ? it.C : nullptr;
+      if (!raw) {
+        it.diag = der ? 0 : 1;
+        it.C2 = st.nout > 1 ? (der ? dslot(st.out[1].slot) : slot(st.out[1].slot)) : nullptr;
+        for (int t = 0; t < 4; ++t) it.E[t] = used[t] ? (der ? dslot(t) : slot(t)) : nullptr;
+      }
+      it.tile_start = tiles;
+      tiles += (d + g.sp_w - 1) / g.sp_w;
+      v.push_back(it);
+    };
+    switch (op) {
+      case SP_F0: item(false, slot(st.R), false, false); break;
+      case SP_F1: item(false, slot(st.L), false, false); break;
+      case SP_B0R: item(true, dslot(st.L), true, false); break;
+      case SP_B0C:
+        item(false, slot(st.R), false, false);
+        item(true, dslot(st.R), false, true);
+        break;
+      case SP_B1:
+        item(false, slot(st.L), false, false);
+        item(true, dslot(st.L), false, true);
+        break;
+    }
+  }
+  SpListRef ref;
+  if (cudaMalloc(&ref.dev, v.size() * sizeof(SpItem)) != cudaSuccess) return SpListRef{};
+  cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(SpItem), cudaMemcpyHostToDevice);
+  g.splist_mem.push_back(ref.dev);
+  ref.n = (int)v.size();
+  ref.rows = tiles;
+  g.splists.emplace(key, ref);
+  return ref;
+}
+
+constexpr int kSpMaxSmem = 200 * 1024;  // one dense row of double2 in shared memory: d <= 12800
+
+static int sp_smem_attr(LargeGroup& g) {
+  static std::mutex mu;
+  static uint64_t done = 0;
+  cudaError_t e = once_per_device(mu, done, [] {
+    const auto a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t r = cudaFuncSetAttribute(spmm_cols_kernel, a, kSpMaxSmem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(spmm_rows_kernel, a, kSpMaxSmem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(sp_trace_kernel, a, kSpMaxSmem);
+    return r;
+  });
+  if (e != cudaSuccess) {
+    g.err = std::string("sparse kernel attributes: ") + cudaGetErrorString(e);
+    return SQOC_ERR_CUDA;
+  }
+  return SQOC_OK;
+}
+
+static int sp_launch(LargeGroup& g, int op, int degree, GemmArgs a, cudaStream_t st) {
+  SpListRef l = sp_list(g, op, degree);
+  if (!l.dev) {
+    g.err = "sparse work list allocation failed";
+    return SQOC_ERR_CUDA;
+  }
+  int rc = sp_smem_attr(g);
+  if (rc) return rc;
+  const bool cols = op == SP_F0 || op == SP_B0C;
+  const size_t smem = g.sp_smem * g.sp_w;
+  if (cols) spmm_cols_kernel<<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
+  else spmm_rows_kernel<<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
+  LCHK(cudaGetLastError());
+  g.launches++;
+  return SQOC_OK;
+}
+
+// forward scheme step k (< 2) on the sparse A
+static int sp_fwd_step(LargeGroup& g, int k, int degree, GemmArgs a, cudaStream_t st) {
+  return sp_launch(g, k == 0 ? SP_F0 : SP_F1, degree, a, st);
+}
+
+// backward pair step k (< 2): value and derivative halves
+static int sp_pair_step(LargeGroup& g, int k, int degree, GemmArgs a, cudaStream_t st) {
+  int rc;
+  if (k == 0) {
+    if ((rc = sp_launch(g, SP_B0R, degree, GemmArgs{1.0, 0.0, 0.0, 0.0}, st))) return rc;
+    return sp_launch(g, SP_B0C, degree, a, st);
+  }
+  return sp_launch(g, SP_B1, degree, a, st);
+}
+
+static int sp_values(LargeGroup& g, int j, const double* u, double scale, cudaStream_t st) {
+  sp_values_kernel<<<dim3(64, g.nblk), 256, 0, st>>>(j, g.K, g.N, u, scale, g.sp_dev);
+  LCHK(cudaGetLastError());
+  g.launches++;
+  return SQOC_OK;
+}
+
+// Tr(U^dag N a_k) by rows (U = T[p], N = dT[p]) into sp_part, then the per-slice gradient entries
+static int sp_trace(LargeGroup& g, int j, int p, const LargeArgs& a, int s_idx, cudaStream_t st) {
+  int rc = sp_smem_attr(g);
+  if (rc) return rc;
+  sp_trace_kernel<<<g.sp_trace_tiles, kSpThreads, g.sp_smem * g.sp_w, st>>>(g.sp_trace_dev + (size_t)p * g.nblk, g.nblk,
+                                                                     g.sp_dev, g.K, g.sp_w);
+  LCHK(cudaGetLastError());
+  trace_reduce_kernel<<<g.nblk, 256, 0, st>>>(j, g.K, g.N, g.sp_rowoff_dev, g.sp_part, g.tau_dev, g.w_dev, g.gidx_dev,
+                                              a.gradb + (size_t)s_idx * g.K * g.N, a.gradb_block_stride);
+  LCHK(cudaGetLastError());
+  g.launches += 2;
+  return SQOC_OK;
+}
+
+// Upload the patterns (CSR from the host spec, CSC derived here) when every block is sparse enough.
+static int sp_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks) {
+  const char* env = getenv("SQOC_SPARSE");
+  if (env && env[0] == '0') return SQOC_OK;
+  for (auto& b : blocks)
+    if (b.sp_rp.size() != (size_t)b.d + 1 || (double)b.sp_ci.size() > (double)b.d * b.d / 8.0) return SQOC_OK;
+  std::vector<SpBlockDev> host(g.nblk);
+  std::vector<int> rowoff(g.nblk + 1, 0);
+  int maxd = 0;
+  const int K1 = g.K + 1;
+  for (int b = 0; b < g.nblk; ++b) {
+    const LargeBlockSpec& bs = blocks[b];
+    const int d = bs.d, nnz = (int)bs.sp_ci.size();
+    maxd = std::max(maxd, d);
+    // row and column ELL layouts of the union pattern (entry e of row / column x at e * d + x)
+    std::vector<int> rcount(d, 0), ccount(d, 0);
+    for (int i = 0; i < d; ++i) {
+      rcount[i] = bs.sp_rp[i + 1] - bs.sp_rp[i];
+      for (int e = bs.sp_rp[i]; e < bs.sp_rp[i + 1]; ++e) ccount[bs.sp_ci[e]]++;
+    }
+    const int wr = std::max(1, *std::max_element(rcount.begin(), rcount.end()));
+    const int wc = std::max(1, *std::max_element(ccount.begin(), ccount.end()));
+    std::vector<int> r_idx((size_t)wr * d, 0), c_idx((size_t)wc * d, 0);
+    std::vector<double2> r_gv((size_t)K1 * wr * d, make_double2(0.0, 0.0)), c_gv((size_t)K1 * wc * d, make_double2(0.0, 0.0));
+    std::vector<int> cfill(d, 0);
+    for (int i = 0; i < d; ++i)  // rows ascending: each column's entries in row order
+      for (int e = bs.sp_rp[i]; e < bs.sp_rp[i + 1]; ++e) {
+        const int er = e - bs.sp_rp[i], c = bs.sp_ci[e], ec = cfill[c]++;
+        r_idx[(size_t)er * d + i] = c;
+        c_idx[(size_t)ec * d + c] = i;
+        for (int k = 0; k < K1; ++k) {
+          const double2 v = bs.sp_gv[(size_t)k * nnz + e];
+          r_gv[((size_t)k * wr + er) * d + i] = v;
+          c_gv[((size_t)k * wc + ec) * d + c] = v;
+        }
+      }
+    auto up = [&](const void* src, size_t bytes) -> void* {
+      void* dst = nullptr;
+      if (cudaMalloc(&dst, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
+      g.sp_mem.push_back(dst);
+      if (bytes && src) cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+      return dst;
+    };
+    SpBlockDev& h = host[b];
+    h.d = d;
+    h.wr = wr;
+    h.wc = wc;
+    h.r_idx = static_cast<const int*>(up(r_idx.data(), r_idx.size() * sizeof(int)));
+    h.c_idx = static_cast<const int*>(up(c_idx.data(), c_idx.size() * sizeof(int)));
+    h.r_gv = static_cast<const double2*>(up(r_gv.data(), r_gv.size() * sizeof(double2)));
+    h.c_gv = static_cast<const double2*>(up(c_gv.data(), c_gv.size() * sizeof(double2)));
+    h.r_sv = static_cast<double2*>(up(nullptr, (size_t)wr * d * sizeof(double2)));
+    h.c_sv = static_cast<double2*>(up(nullptr, (size_t)wc * d * sizeof(double2)));
+    if (!h.r_idx || !h.c_idx || !h.r_gv || !h.c_gv || !h.r_sv || !h.c_sv) {
+      g.err = "sparse pattern allocation failed";
+      return SQOC_ERR_CUDA;
+    }
+    rowoff[b + 1] = rowoff[b] + d;
+  }
+  LCHK(cudaMalloc(&g.sp_dev, g.nblk * sizeof(SpBlockDev)));
+  LCHK(cudaMemcpy(g.sp_dev, host.data(), g.nblk * sizeof(SpBlockDev), cudaMemcpyHostToDevice));
+  LCHK(cudaMalloc(&g.sp_rowoff_dev, (g.nblk + 1) * sizeof(int)));
+  LCHK(cudaMemcpy(g.sp_rowoff_dev, rowoff.data(), (g.nblk + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  LCHK(cudaMalloc(&g.sp_part, (size_t)rowoff[g.nblk] * std::max(g.K, 1) * sizeof(double2)));
+  g.sp_smem = (size_t)maxd * sizeof(double2);  // one dense row or column panel of width 1
+  g.sp_w = (int)std::max<size_t>(1, std::min<size_t>(kSpMaxW, kSpMaxSmem / g.sp_smem));
+  std::vector<SpTraceItem> tr;
+  for (int p = 0; p < 2; ++p) {
+    int tiles = 0;
+    for (int b = 0; b < g.nblk; ++b) {
+      SpTraceItem it{};
+      it.blk = b;
+      it.tile_start = tiles;
+      tiles += (g.blocks[b].d + g.sp_w - 1) / g.sp_w;
+      it.U = g.T[p] + g.off[b];
+      it.N = g.dT[p] + g.off[b];
+      it.part = g.sp_part + (size_t)rowoff[b] * g.K;
+      tr.push_back(it);
+    }
+    g.sp_trace_tiles = tiles;
+  }
+  LCHK(cudaMalloc(&g.sp_trace_dev, tr.size() * sizeof(SpTraceItem)));
+  LCHK(cudaMemcpy(g.sp_trace_dev, tr.data(), tr.size() * sizeof(SpTraceItem), cudaMemcpyHostToDevice));
+  g.sp_on = g.sp_smem <= (size_t)kSpMaxSmem;
   return SQOC_OK;
 }
 
@@ -826,7 +1078,7 @@ int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, 
   }
   LCHK(cudaMalloc(&g.tile_off_dev, (g.nblk + 1) * sizeof(int)));
   LCHK(cudaMemcpy(g.tile_off_dev, g.trace_tile_off.data(), (g.nblk + 1) * sizeof(int), cudaMemcpyHostToDevice));
-  return SQOC_OK;
+  return sp_init(g, blocks);
 }
 
 int large_set_norms(LargeGroup& g, const std::vector<double>& gn) {
@@ -870,6 +1122,15 @@ void large_free(LargeGroup& g) {
   cudaFree(g.gentall_dev);
   double2* sv[] = {g.sv_U, g.sv_chunk, g.sv_psi, g.sv_chi, g.sv_V, g.sv_W, g.sv_acc, g.sv_g, g.mf_t};
   for (auto x : sv) cudaFree(x);
+  for (auto m : g.sp_mem) cudaFree(m);
+  g.sp_mem.clear();
+  for (auto m : g.splist_mem) cudaFree(m);
+  g.splist_mem.clear();
+  g.splists.clear();
+  cudaFree(g.sp_dev);
+  cudaFree(g.sp_rowoff_dev);
+  cudaFree(g.sp_part);
+  cudaFree(g.sp_trace_dev);
   cudaFree(g.chunk_vec);
   cudaFree(g.chunk_tau);
   cudaFree(g.chunk_ptrs);
@@ -1474,8 +1735,12 @@ static int seq_forward(LargeGroup& g, const double* u, const PolyScheme& sc, int
     build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
     LCHK(cudaGetLastError());
     g.launches++;
-    for (int k = 0; k < sc.nsteps; ++k)
-      if ((rc = gemm(g, F_STEP, k, sc.degree, 0, step_args(sc.step[k]), st))) return rc;
+    if (g.sp_on && (rc = sp_values(g, j, u, scale, st))) return rc;
+    for (int k = 0; k < sc.nsteps; ++k) {
+      if (g.sp_on && k < 2) rc = sp_fwd_step(g, k, sc.degree, step_args(sc.step[k]), st);
+      else rc = gemm(g, F_STEP, k, sc.degree, 0, step_args(sc.step[k]), st);
+      if (rc) return rc;
+    }
     int p = 0;
     for (int i = 0; i < sq; ++i) {
       if ((rc = gemm(g, F_S, p, 0, 0, one, st))) return rc;
@@ -1503,18 +1768,33 @@ static int seq_backward(LargeGroup& g, const LargeArgs& a, int s_idx, const doub
     LCHK(cudaGetLastError());
     g.launches++;
     if (!g.gate && (rc = gemm(g, B_C, 0, q, r, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
-    for (int k = 0; k < sc.nsteps; ++k)
-      if ((rc = gemm(g, B_STEP, k, sc.degree, 0, step_args(sc.step[k]), st))) return rc;
+    if (g.sp_on && (rc = sp_values(g, j, u, scale, st))) return rc;
+    for (int k = 0; k < sc.nsteps; ++k) {
+      if (g.sp_on && k == 0) {
+        rc = sp_pair_step(g, 0, sc.degree, step_args(sc.step[0]), st);
+      } else if (g.sp_on && k == 1) {
+        rc = gemm(g, B_STEP1D, 0, sc.degree, 0, one, st);
+        if (rc == SQOC_OK) rc = sp_pair_step(g, 1, sc.degree, step_args(sc.step[1]), st);
+      } else {
+        rc = gemm(g, B_STEP, k, sc.degree, 0, step_args(sc.step[k]), st);
+      }
+      if (rc) return rc;
+    }
     int p = 0;
     for (int i = 0; i < sq; ++i) {
       if ((rc = gemm(g, B_S, p, 0, 0, one, st))) return rc;
       p ^= 1;
     }
-    if ((rc = gemm(g, g.gate ? B_UC : B_D, p, 0, 0, one, st))) return rc;
-    trace_reduce_kernel<<<nblk, 256, 0, st>>>(j, K, N, g.tile_off_dev, g.trace_part, g.tau_dev, g.w_dev, g.gidx_dev,
-                                              a.gradb + (size_t)s_idx * K * N, a.gradb_block_stride);
-    LCHK(cudaGetLastError());
-    g.launches++;
+    if (g.gate && g.sp_on) {  // M = U^dag Ad on the tensor cores, the trace on the sparse a_k
+      if ((rc = gemm(g, B_M, p, 0, 0, one, st))) return rc;
+      if ((rc = sp_trace(g, j, p, a, s_idx, st))) return rc;
+    } else {
+      if ((rc = gemm(g, g.gate ? B_UC : B_D, p, 0, 0, one, st))) return rc;
+      trace_reduce_kernel<<<nblk, 256, 0, st>>>(j, K, N, g.tile_off_dev, g.trace_part, g.tau_dev, g.w_dev,
+                                                g.gidx_dev, a.gradb + (size_t)s_idx * K * N, a.gradb_block_stride);
+      LCHK(cudaGetLastError());
+      g.launches++;
+    }
     if (g.gate) {  // C_{j-1} = U^dag C_j U
       if (j > 0 && (rc = gemm(g, B_CU, p, 0, 0, one, st))) return rc;
     } else {

@@ -26,6 +26,7 @@
 #include <tuple>
 #include <vector>
 
+#include "sparse.cuh"
 #include "zgemm_tma.cuh"
 
 namespace sqoc {
@@ -47,6 +48,14 @@ struct LargeBlockSpec {
   const double2* target;  // V or psi_f
   double weight;
   double gen_norm[5];     // inf-norm bounds of a_0..a_K
+  // union pattern of a_0..a_K (host CSR) and the generator values on it, [(K+1)][nnz]
+  std::vector<int> sp_rp, sp_ci;
+  std::vector<double2> sp_gv;
+};
+
+struct SpListRef {
+  SpItem* dev = nullptr;
+  int n = 0, rows = 0;
 };
 
 struct ListRef {
@@ -94,6 +103,20 @@ struct LargeGroup {
   double gemm_macs = 0.0;  // complex MACs issued by the last evaluation's GEMMs
   int gemm_launches = 0;
   int* tile_off_dev = nullptr;    // [nblk + 1] trace tile offsets
+  // ---- sparse generators (sparse.cuh): the scheme's products with A as a factor and the gradient
+  // trace run as sparse x dense kernels in the slice-sequential schedule when every block's pattern is
+  // sparse enough (sp_on; SQOC_SPARSE=0 disables) ----
+  bool sp_on = false;
+  SpBlockDev* sp_dev = nullptr;            // [nblk]
+  std::vector<void*> sp_mem;
+  double2* sp_part = nullptr;              // [sum d][K] trace partials by row
+  int* sp_rowoff_dev = nullptr;            // [nblk + 1] row offsets (trace_reduce_kernel's tile offsets)
+  size_t sp_smem = 0;                      // bytes of one dense row (max d double2)
+  int sp_w = 1;                            // rows / columns per sparse-kernel CTA
+  int sp_trace_tiles = 0;
+  std::map<std::tuple<int, int, int, int>, SpListRef> splists;
+  std::vector<void*> splist_mem;
+  SpTraceItem* sp_trace_dev = nullptr;     // per p parity: [2][nblk]
   // ---- history schedule: every slice resident, slice-batched GEMMs (chosen when memory allows) ----
   int h_deg = -1, h_s = -1, h_C = 0;
   double2* h_chain = nullptr;       // [C][N][total]: scheme slots 0..8 (A .. Y), S_1..S_s

@@ -304,3 +304,21 @@ def test_cfg3_blocks_short_grid_against_oracle():
     Fo, go, _ = O.objective(s, u)
     assert abs(F - Fo) <= F_TOL
     assert rel(g, go) <= G_TOL
+
+
+def test_sparse_generator_products_equal_dense(monkeypatch):
+    """Scheme steps 0-1 and the gradient trace on the sparse generators (sparse.cuh) give the dense
+    path's result: gate (cfg 3 GPU-built D_14 blocks) and state (cfg 4's 4096 space), sequential."""
+    cases = ((systems.config(3, n_slices=3, builder="gpu"), "sequential"),
+             (systems.config(4, n_slices=2, full=True), "sequential"))
+    for s, sched in cases:
+        u = s.controls(9)
+        out = {}
+        for flag in ("0", "1"):
+            monkeypatch.setenv("SQOC_SPARSE", flag)
+            eng = GrapeEngine(s, max_batch=1)
+            eng.set_schedule(sched)
+            out[flag] = eng.objective(u)
+            eng.close()
+        assert abs(out["0"][0] - out["1"][0]) <= 1e-12
+        assert rel(out["0"][1], out["1"][1]) <= 1e-11
