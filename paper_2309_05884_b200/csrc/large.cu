@@ -602,7 +602,7 @@ static ListRef upload_list(std::vector<GemmItem>& v, std::vector<void*>& mem) {
 
 // Sequential schedule ops.  Gate objective: B_UC = [M = U^dag Ad | trace Tr(U^dag dT E_k)] in one
 // launch, B_CU: Ad = M U.  State objective: B_C, B_D, B_XL (vector X / Lam).
-enum Op { F_STEP, F_S, F_X, B_C, B_STEP, B_S, B_D, B_XL, B_UC, B_CU, B_STEP1D, B_M };
+enum Op { F_STEP, F_S, F_X, B_C, B_STEP, B_S, B_D, B_XL, B_UC, B_CU, B_STEP1D, B_M, B_STEPD, B_SD };
 
 static GemmItem mk(const double2* A0, const double2* B0, const double2* A1, const double2* B1, double2* C,
                    const double2* E0, const double2* E1, int m, int n, int k, int nseg, int lda, int ldb, int ldc,
@@ -684,6 +684,7 @@ static ListRef get_list(LargeGroup& g, int op, int p, int q, int r) {
     switch (op) {
       case F_STEP: push_step(v, scheme_of(q), p, d, slot, dslot, true, false); break;
       case B_STEP: push_step(v, scheme_of(q), p, d, slot, dslot, true, true); break;
+      case B_STEPD: push_step(v, scheme_of(q), p, d, slot, dslot, false, true); break;  // value from uh
       case F_S: v.push_back(mk(Tp, Tp, 0, 0, Tn, 0, 0, d, d, d, 1, d, d, d, 0)); break;
       case F_X: v.push_back(mk(Tp, Xq, 0, 0, Xn, 0, 0, d, R, d, 1, d, R, R, 0)); break;
       case B_C: v.push_back(mk(Xq, Lr, 0, 0, Ad, 0, 0, d, d, R, 1, R, R, d, 0)); break;
@@ -691,6 +692,7 @@ static ListRef get_list(LargeGroup& g, int op, int p, int q, int r) {
         v.push_back(mk(Tp, Tp, 0, 0, Tn, 0, 0, d, d, d, 1, d, d, d, 0));
         v.push_back(mk(Tp, dTp, dTp, Tp, dTn, 0, 0, d, d, d, 2, d, d, d, 0));
         break;
+      case B_SD: v.push_back(mk(Tp, dTp, dTp, Tp, dTn, 0, 0, d, d, d, 2, d, d, d, 0)); break;  // value from uh
       case B_D: v.push_back(trace_item()); break;
       case B_XL:
         v.push_back(mk(Tp, Xq, 0, 0, Xn, 0, 0, d, R, d, 1, d, R, R, 0));
@@ -751,15 +753,20 @@ static int gemm(LargeGroup& g, int op, int p, int q, int r, GemmArgs a, cudaStre
 //   SP_F1  forward step 1:  A3, P = A2 S                                  (rows)
 //   SP_B0R backward step 0, first half of the derivative: dA2 = dA S      (rows, raw store)
 //   SP_B0C backward step 0: A2 = S A; dA2 = S dA + dA2 (+ epilogue)       (cols)
-//   SP_B1  backward step 1: A3, P = A2 S; dA3, dP = dA2 S + dA3           (rows; dA3 holds the dense
-//          GEMM term A2 dA from B_STEP1D)
-enum SpOp { SP_F0, SP_F1, SP_B0R, SP_B0C, SP_B1 };
+//   SP_B1  backward step 1: A3, P = A2 S; dA3, dP = dA2 S + dA3           (rows; dA3 holds the term
+//          A2 dA: the dense B_STEP1D GEMM, or S (S dA) from SP_B1D)
+// All-sparse derivative chain (r02): A2 dA = A (A dA), so with T = S dA kept in a free derivative slot
+// (dslot 3, written only by step 2) the dense term becomes one more sparse product:
+//   SP_B0T backward step 0: A2 = S A (+ epilogue); T = S dA (raw)           (cols)
+//   SP_B0S backward step 0: dA2 = dA S + T (raw)                            (rows)
+//   SP_B1D backward step 1: dA3 = S T (raw)                                 (cols)
+enum SpOp { SP_F0, SP_F1, SP_B0R, SP_B0C, SP_B1, SP_B0T, SP_B0S, SP_B1D };
 
 static SpListRef sp_list(LargeGroup& g, int op, int degree) {
   auto key = std::make_tuple(op, degree, 0, 0);
   auto found = g.splists.find(key);
   if (found != g.splists.end()) return found->second;
-  const int k = (op == SP_F1 || op == SP_B1) ? 1 : 0;
+  const int k = (op == SP_F1 || op == SP_B1 || op == SP_B1D) ? 1 : 0;
   const PolyStep& st = scheme_of(degree).step[k];
   bool used[4] = {false, false, false, false};
   for (int o = 0; o < st.nout; ++o)
@@ -787,13 +794,14 @@ static SpListRef sp_list(LargeGroup& g, int op, int degree) {
         default: return g.dxs[c - 3] + o;
       }
     };
-    auto item = [&](bool der, const double2* D, bool raw, bool add_x) {
+    auto item = [&](bool der, const double2* D, bool raw, bool add_x, double2* C = nullptr,
+                    const double2* X = nullptr) {
       SpItem it{};
       it.blk = b;
       it.D = D;
-      it.C = der ? dslot(st.out[0].slot) : slot(st.out[0].slot);
+      it.C = C ? C : der ? dslot(st.out[0].slot) : slot(st.out[0].slot);
       it.add_x = add_x ? 1 : 0;
-      it.X = add_x ? it.C : nullptr;
+      it.X = add_x ? (X ? X : it.C) : nullptr;
       if (!raw) {
         it.diag = der ? 0 : 1;
         it.C2 = st.nout > 1 ? (der ? dslot(st.out[1].slot) : slot(st.out[1].slot)) : nullptr;
@@ -815,6 +823,12 @@ static SpListRef sp_list(LargeGroup& g, int op, int degree) {
         item(false, slot(st.L), false, false);
         item(true, dslot(st.L), false, true);
         break;
+      case SP_B0T:
+        item(false, slot(st.R), false, false);
+        item(true, dslot(st.R), true, false, dslot(3));
+        break;
+      case SP_B0S: item(true, dslot(st.L), true, true, nullptr, dslot(3)); break;
+      case SP_B1D: item(true, dslot(3), true, false, dslot(2)); break;
     }
   }
   SpListRef ref;
@@ -854,7 +868,7 @@ static int sp_launch(LargeGroup& g, int op, int degree, GemmArgs a, cudaStream_t
   }
   int rc = sp_smem_attr(g);
   if (rc) return rc;
-  const bool cols = op == SP_F0 || op == SP_B0C;
+  const bool cols = op == SP_F0 || op == SP_B0C || op == SP_B0T || op == SP_B1D;
   const size_t smem = g.sp_smem * g.sp_w;
   if (cols) spmm_cols_kernel<<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
   else spmm_rows_kernel<<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
@@ -869,12 +883,23 @@ static int sp_fwd_step(LargeGroup& g, int k, int degree, GemmArgs a, cudaStream_
 }
 
 // backward pair step k (< 2): value and derivative halves
+static bool sp_chain() {  // all-sparse derivative chain (SQOC_SPCHAIN=0: the dense A2 dA GEMM instead)
+  const char* e = getenv("SQOC_SPCHAIN");
+  return !(e && e[0] == '0');
+}
+
 static int sp_pair_step(LargeGroup& g, int k, int degree, GemmArgs a, cudaStream_t st) {
   int rc;
+  const GemmArgs raw{1.0, 0.0, 0.0, 0.0};
   if (k == 0) {
-    if ((rc = sp_launch(g, SP_B0R, degree, GemmArgs{1.0, 0.0, 0.0, 0.0}, st))) return rc;
+    if (sp_chain()) {  // step 0's epilogue is a plain store (both schemes), so raw items may share it
+      if ((rc = sp_launch(g, SP_B0T, degree, a, st))) return rc;
+      return sp_launch(g, SP_B0S, degree, raw, st);
+    }
+    if ((rc = sp_launch(g, SP_B0R, degree, raw, st))) return rc;
     return sp_launch(g, SP_B0C, degree, a, st);
   }
+  if (sp_chain() && (rc = sp_launch(g, SP_B1D, degree, raw, st))) return rc;
   return sp_launch(g, SP_B1, degree, a, st);
 }
 
@@ -1120,6 +1145,8 @@ void large_free(LargeGroup& g) {
   for (auto m : g.gentall_mem) cudaFree(m);
   g.gentall_mem.clear();
   cudaFree(g.gentall_dev);
+  cudaFree(g.uh);
+  g.uh = nullptr;
   double2* sv[] = {g.sv_U, g.sv_chunk, g.sv_psi, g.sv_chi, g.sv_V, g.sv_W, g.sv_acc, g.sv_g, g.mf_t};
   for (auto x : sv) cudaFree(x);
   for (auto m : g.sp_mem) cudaFree(m);
@@ -1722,9 +1749,28 @@ static int large_eval_matrix_free(LargeGroup& g, const LargeArgs& a, int s_idx, 
 
 
 // ------------------------------------------------------------------ slice-sequential schedule
+// Propagator history for the sequential sweeps: allocated on first use when N sum d^2 complex values fit
+// in 90% of the free device memory (cfg 3 on one B200: 500 x 285 MB = 142.5 GB of ~170 GB free).  The
+// backward sweep then reads U_j instead of forming it (one GEMM-unit per slice fewer).
+static bool uh_ensure(LargeGroup& g) {
+  const char* env = getenv("SQOC_UHIST");
+  if ((env && env[0] == '0') || g.N <= 0) return false;
+  if (g.uh) return true;
+  const size_t bytes = (size_t)g.N * g.total * sizeof(double2);
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+  if (bytes > (size_t)(0.9 * (double)free_b)) return false;
+  if (cudaMalloc(&g.uh, bytes) != cudaSuccess) {
+    cudaGetLastError();  // clear the failed allocation; run without the history
+    g.uh = nullptr;
+    return false;
+  }
+  return true;
+}
+
 // forward sweep from the boundary X_0 (I / psi_0 / a chunk's X_start); returns the parity q of X_N
 static int seq_forward(LargeGroup& g, const double* u, const PolyScheme& sc, int sq, dim3 ew_grid, cudaStream_t st,
-                       int* q_out) {
+                       int* q_out, bool keep_u = false) {
   const int K = g.K, N = g.N;
   const double scale = std::ldexp(1.0, -sq);
   int rc;
@@ -1746,16 +1792,20 @@ static int seq_forward(LargeGroup& g, const double* u, const PolyScheme& sc, int
       if ((rc = gemm(g, F_S, p, 0, 0, one, st))) return rc;
       p ^= 1;
     }
+    if (keep_u)
+      LCHK(cudaMemcpyAsync(g.uh + (size_t)j * g.total, g.T[p], g.total * sizeof(double2), cudaMemcpyDeviceToDevice,
+                           st));
     if ((rc = gemm(g, F_X, p, q, 0, one, st))) return rc;
     q ^= 1;
   }
+  g.uh_valid = keep_u;
   *q_out = q;
   return SQOC_OK;
 }
 
 // backward sweep from X_N (X[q]) and Lam_N (L[0]); tau must already be set
 static int seq_backward(LargeGroup& g, const LargeArgs& a, int s_idx, const double* u, const PolyScheme& sc, int sq,
-                        int q, dim3 ew_grid, cudaStream_t st) {
+                        int q, dim3 ew_grid, cudaStream_t st, bool have_u = false) {
   const int K = g.K, N = g.N, nblk = g.nblk;
   const double scale = std::ldexp(1.0, -sq);
   GemmArgs one{1.0, 0.0, 0.0, 0.0};
@@ -1773,8 +1823,10 @@ static int seq_backward(LargeGroup& g, const LargeArgs& a, int s_idx, const doub
       if (g.sp_on && k == 0) {
         rc = sp_pair_step(g, 0, sc.degree, step_args(sc.step[0]), st);
       } else if (g.sp_on && k == 1) {
-        rc = gemm(g, B_STEP1D, 0, sc.degree, 0, one, st);
+        rc = sp_chain() ? SQOC_OK : gemm(g, B_STEP1D, 0, sc.degree, 0, one, st);
         if (rc == SQOC_OK) rc = sp_pair_step(g, 1, sc.degree, step_args(sc.step[1]), st);
+      } else if (have_u && sq == 0 && k == sc.nsteps - 1) {  // U_j = Y from the forward's history
+        rc = gemm(g, B_STEPD, k, sc.degree, 0, step_args(sc.step[k]), st);
       } else {
         rc = gemm(g, B_STEP, k, sc.degree, 0, step_args(sc.step[k]), st);
       }
@@ -1782,9 +1834,12 @@ static int seq_backward(LargeGroup& g, const LargeArgs& a, int s_idx, const doub
     }
     int p = 0;
     for (int i = 0; i < sq; ++i) {
-      if ((rc = gemm(g, B_S, p, 0, 0, one, st))) return rc;
+      if ((rc = gemm(g, have_u && i == sq - 1 ? B_SD : B_S, p, 0, 0, one, st))) return rc;
       p ^= 1;
     }
+    if (have_u)  // U_j into the slot the value product would have written (Y = T[0] at s = 0, else T[p])
+      LCHK(cudaMemcpyAsync(g.T[p], g.uh + (size_t)j * g.total, g.total * sizeof(double2), cudaMemcpyDeviceToDevice,
+                           st));
     if (g.gate && g.sp_on) {  // M = U^dag Ad on the tensor cores, the trace on the sparse a_k
       if ((rc = gemm(g, B_M, p, 0, 0, one, st))) return rc;
       if ((rc = sp_trace(g, j, p, a, s_idx, st))) return rc;
@@ -1970,7 +2025,7 @@ static int chunk_eval(LargeGroup& g, const LargeArgs& a, int s_idx, const double
     if (g.gate) {  // forward sweep from X = I; X_N is the chunk product
       g.mode = 0;
       int q = 0;
-      if ((rc = seq_forward(g, u, sc, sq, ew_grid, st, &q))) return rc;
+      if ((rc = seq_forward(g, u, sc, sq, ew_grid, st, &q, uh_ensure(g)))) return rc;
       LCHK(cudaMemcpyAsync(g.chunk_out, g.X[q], g.total * sizeof(double2), cudaMemcpyDeviceToDevice, st));
     } else {  // every U_j kept (the sweeps of phase 2 reuse them); product by one GEMM per slice
       g.mode = 2;
@@ -2018,7 +2073,7 @@ static int chunk_eval(LargeGroup& g, const LargeArgs& a, int s_idx, const double
   if (g.gate) {
     g.mode = 0;
     rc = bc_tau(g, nullptr, a, s_idx, st);  // tau_dev and tau_out from the carries
-    if (rc == SQOC_OK) rc = seq_backward(g, a, s_idx, u, sc, sq, 0, ew_grid, st);
+    if (rc == SQOC_OK) rc = seq_backward(g, a, s_idx, u, sc, sq, 0, ew_grid, st, g.uh && g.uh_valid);
   } else {
     g.mode = 2;
     g.bc_x_dev = g.chunk_ptrs;
@@ -2069,6 +2124,11 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
       if ((rc = chunk_eval(g, a, s, u, sc, sq, bound, ew_grid, st))) return rc;
       continue;
     }
+    if (g.uh && g.force_mode != -1 && g.force_mode != 0) {  // another schedule forced: release the history
+      cudaFree(g.uh);
+      g.uh = nullptr;
+      g.uh_valid = false;
+    }
     if (!g.gate && N > 0 && g.force_mode == 3) {  // matrix-free state schedule (opt-in)
       if ((rc = sv_alloc(g, false))) return rc;
       g.mode = 3;
@@ -2109,9 +2169,10 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
       g.mode = 0;
     }
     int q = 0;
-    if ((rc = seq_forward(g, u, sc, sq, ew_grid, st, &q))) return rc;
+    const bool keep = uh_ensure(g);
+    if ((rc = seq_forward(g, u, sc, sq, ew_grid, st, &q, keep))) return rc;
     if ((rc = bc_tau(g, g.X[q], a, s, st))) return rc;
-    if ((rc = seq_backward(g, a, s, u, sc, sq, q, ew_grid, st))) return rc;
+    if ((rc = seq_backward(g, a, s, u, sc, sq, q, ew_grid, st, keep))) return rc;
   }
   return SQOC_OK;
 }

@@ -167,6 +167,11 @@ struct LargeGroup {
   const double2** bc_x_dev = nullptr;
   const double2** bc_l_dev = nullptr;
   const double2* bc_tau = nullptr;
+  // ---- propagator history of the slice-sequential gate schedule: U_j of every slice, written by the
+  // forward sweep, so the backward sweep skips the value half of the product that forms U_j (one
+  // d^3 GEMM-unit per slice); kept only when N sum d^2 fits the free memory (SQOC_UHIST=0 disables) ----
+  double2* uh = nullptr;            // [N][total]
+  bool uh_valid = false;            // uh holds the propagators of the last forward sweep (same u)
   int mode = -1;                    // last schedule used: 0 sequential, 1 history, 2 state-vector, 3 matrix-free
   int force_mode = -1;              // -1 auto, 0 sequential, 1 history, 2 state-vector, 3 matrix-free
   int launches = 0;

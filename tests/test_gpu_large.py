@@ -322,3 +322,27 @@ def test_sparse_generator_products_equal_dense(monkeypatch):
             eng.close()
         assert abs(out["0"][0] - out["1"][0]) <= 1e-12
         assert rel(out["0"][1], out["1"][1]) <= 1e-11
+
+
+@pytest.mark.gpu
+def test_propagator_history_and_sparse_chain_equal_plain_sequential(monkeypatch):
+    """r02 sequential-schedule savings give the plain schedule's result: the U_j history (backward reads
+    U_j instead of forming it, SQOC_UHIST) and the all-sparse derivative chain (A2 dA = S (S dA),
+    SQOC_SPCHAIN), gate cfg 3 blocks with 0 and 2 squarings, plus the chunked (sharded) path."""
+    s = systems.config(3, n_slices=3, builder="gpu")
+    for scale in (1.0, 6.0):  # 6x controls force squarings
+        u = s.controls(5) * scale
+        out = {}
+        for uh, ch in (("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")):
+            monkeypatch.setenv("SQOC_UHIST", uh)
+            monkeypatch.setenv("SQOC_SPCHAIN", ch)
+            eng = GrapeEngine(s, max_batch=1)
+            eng.set_schedule("sequential")
+            out[uh + ch] = eng.objective(u)
+            plan = eng.last_plan
+            eng.close()
+        for k in ("10", "01", "11"):
+            assert abs(out[k][0] - out["00"][0]) <= 1e-12, (scale, k)
+            assert rel(out[k][1], out["00"][1]) <= 1e-11, (scale, k)
+        if scale > 1.0:
+            assert plan["squarings"] > 0
