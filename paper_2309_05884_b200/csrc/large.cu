@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "../../include/symqoc_b200.h"
 #include "devonce.h"
@@ -454,6 +455,24 @@ static bool make_map(CUtensorMap* out, const double2* base, int rows, int cols, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// k-major view [k][cols] (row stride ld complex) as a 3-D map: 16 doubles (8 columns) x rows x
+// floor(cols / 8) column blocks, box 16 x 8 x 8, 128B swizzle (see ItemMaps)
+static bool make_map3(CUtensorMap* out, const double2* base, int rows, int cols, int ld) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || !base || cols < 64) return false;  // cols < 64: no tile has eight full column blocks
+  static const bool off = [] { const char* e = getenv("SQOC_TMA3D"); return e && e[0] == '0'; }();
+  if (off) return false;  // A/B knob: 2-D boxes only
+  cuuint64_t dims[3] = {16, (cuuint64_t)rows, (cuuint64_t)(cols / 8)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * sizeof(double2), 128};
+  cuuint32_t box[3] = {16, 8, 8};
+  cuuint32_t es[3] = {1, 1, 1};
+  const bool ok = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(base), dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  if (!ok) memset(out, 0, sizeof(*out));
+  return ok;
+}
+
 // Tensor maps of every item in both staging orientations (host); false if the driver cannot encode.
 static bool build_maps(const std::vector<GemmItem>& v, std::vector<ItemMaps>& maps) {
   maps.assign(v.size(), ItemMaps{});
@@ -462,11 +481,20 @@ static bool build_maps(const std::vector<GemmItem>& v, std::vector<ItemMaps>& ma
     for (int seg = 0; seg < it.nseg; ++seg) {
       const double2* A = seg ? it.A1 : it.A0;
       const double2* B = seg ? it.B1 : it.B0;
-      CUtensorMap* m = maps[i].m + 4 * seg;
+      CUtensorMap* m = maps[i].m + 6 * seg;
       if (!make_map(m + 0, A, it.m, it.k, it.lda, GBM) || !make_map(m + 1, A, it.k, it.m, it.lda, 8) ||
           !make_map(m + 2, B, it.k, it.n, it.ldb, 8) || !make_map(m + 3, B, it.n, it.k, it.ldb, GBN))
         return false;
+      // optional single-box views of the k-major orientations (the 2-D boxes remain the fallback)
+      if (make_map3(m + 4, A, it.k, it.m, it.lda)) maps[i].has3d |= 1u << (2 * seg);
+      if (make_map3(m + 5, B, it.k, it.n, it.ldb)) maps[i].has3d |= 1u << (2 * seg + 1);
     }
+  }
+  static bool said = false;
+  if (!said && getenv("SQOC_DEBUG") && !v.empty()) {
+    said = true;
+    fprintf(stderr, "[sqoc] 3-D tensor maps of the first GEMM list: has3d = 0x%x (m = %d, n = %d)\n", maps[0].has3d,
+            v[0].m, v[0].n);
   }
   return true;
 }
@@ -482,10 +510,11 @@ static void build_tiles(const std::vector<GemmItem>& v, std::vector<TileRef>& ou
     const int tm = (it.m + GBM - 1) / GBM, tn = (it.n + GBN - 1) / GBN;
     const double kt = (double)((it.k + GBK - 1) / GBK) * it.nseg;
     for (int a = 0; a < tm; ++a)
-      for (int b = 0; b < tn; ++b) {
+      for (int b = (it.herm ? a : 0); b < tn; ++b) {  // Hermitian products: the mirror tiles are not computed
         const int rows = std::min(GBM, it.m - a * GBM), cols = std::min(GBN, it.n - b * GBN);
-        const int mc = std::min(4, (std::min(rows, 32) + 7) / 8), nc = std::min(2, (std::min(cols, 16) + 7) / 8);
-        all.push_back({kt * (mc * nc + 1), TileRef{(int)i, a * GBM, b * GBN, a * tn + b}});
+        int th, tw, wc;
+        pt_layout((rows + 7) / 8, (cols + 7) / 8, th, tw, wc);
+        all.push_back({kt * (th * tw + 1), TileRef{(int)i, a * GBM, b * GBN, a * tn + b}});
       }
   }
   std::stable_sort(all.begin(), all.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
@@ -508,7 +537,7 @@ static int sm_count() {
 
 template <int TA, int TB, int EPI>
 static cudaError_t launch_gemm(const GemmItem* items, const ItemMaps* maps, const TileRef* tref, int* counter, int n,
-                              int tiles, GemmArgs a, cudaStream_t st) {
+                              int tiles, GemmArgs a, cudaStream_t st, int pt_tiles = -1) {
   static std::mutex mu;
   static uint64_t done = 0;
   cudaError_t e = once_per_device(mu, done, [] {
@@ -525,8 +554,9 @@ static cudaError_t launch_gemm(const GemmItem* items, const ItemMaps* maps, cons
   if (use_3m() && maps && tref && counter && staging() == 1) {
     e = cudaMemsetAsync(counter, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
-    zgemm3m_pt_kernel<TA, TB, EPI><<<std::min(tiles, sm_count()), PT_THREADS, PT_SMEM, st>>>(items, maps, tref,
-                                                                                             tiles, counter, a);
+    const int nt = pt_tiles >= 0 ? pt_tiles : tiles;  // the persistent list may skip mirror tiles
+    zgemm3m_pt_kernel<TA, TB, EPI><<<std::min(nt, sm_count()), PT_THREADS, PT_SMEM, st>>>(items, maps, tref, nt,
+                                                                                          counter, a);
   } else if (use_3m()) zgemm3m_kernel<TA, TB, EPI><<<tiles, G3THREADS, G_SMEM, st>>>(items, n, a);
   else zgemm_kernel<TA, TB, EPI><<<tiles, GTHREADS, G_SMEM, st>>>(items, n, a);
   return cudaGetLastError();
@@ -569,12 +599,8 @@ static ListRef upload_list(std::vector<GemmItem>& v, std::vector<void*>& mem) {
   for (auto& x : v) {
     x.tile_start = t;
     t += tiles_of(x.m, x.n);
-    ref.macs += (double)x.m * x.n * x.k * x.nseg;
   }
   if (v.empty()) return ref;
-  if (cudaMalloc(&ref.dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return ListRef{};
-  cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
-  mem.push_back(ref.dev);
   std::vector<ItemMaps> maps;
   std::vector<TileRef> tref;
   build_tiles(v, tref);
@@ -582,18 +608,33 @@ static ListRef upload_list(std::vector<GemmItem>& v, std::vector<void*>& mem) {
   // CTAs per SM hide each other's epilogues (r02 same-box A/B: cfg 2 41.1 vs 48.6 ms)
   double kmean = 0.0;
   for (auto& x : v) kmean += (double)x.k * x.nseg / v.size();
-  if (kmean >= kPersistentMinK && build_maps(v, maps) &&
-      cudaMalloc(&ref.maps, maps.size() * sizeof(ItemMaps)) == cudaSuccess &&
+  const bool persistent = kmean >= kPersistentMinK && use_3m() && staging() == 1 && build_maps(v, maps);
+  if (!persistent)  // the per-tile kernels map every tile of every item: no mirror-tile skipping
+    for (auto& x : v) x.herm = 0;
+  for (auto& x : v) {  // executed complex MACs (a Hermitian item runs its upper tile triangle only)
+    const int tm = (x.m + GBM - 1) / GBM;
+    const double frac = x.herm ? (double)(tm + 1) / (2.0 * tm) : 1.0;
+    ref.macs += (double)x.m * x.n * x.k * x.nseg * frac;
+  }
+  if (cudaMalloc(&ref.dev, v.size() * sizeof(GemmItem)) != cudaSuccess) return ListRef{};
+  cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
+  mem.push_back(ref.dev);
+  if (persistent && cudaMalloc(&ref.maps, maps.size() * sizeof(ItemMaps)) == cudaSuccess &&
       cudaMalloc(&ref.tref, tref.size() * sizeof(TileRef)) == cudaSuccess) {
     cudaMemcpy(ref.maps, maps.data(), maps.size() * sizeof(ItemMaps), cudaMemcpyHostToDevice);
     cudaMemcpy(ref.tref, tref.data(), tref.size() * sizeof(TileRef), cudaMemcpyHostToDevice);
     mem.push_back(ref.maps);
     mem.push_back(ref.tref);
+    ref.pt_tiles = (int)tref.size();
   } else {
     (void)cudaGetLastError();
     cudaFree(ref.maps);
     ref.maps = nullptr;  // cp.async kernel for this list
     ref.tref = nullptr;
+    if (persistent) {  // allocation failure after the mirror tiles were dropped: recompute everything
+      for (auto& x : v) x.herm = 0;
+      cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
+    }
   }
   ref.n = (int)v.size();
   ref.tiles = t;
@@ -612,6 +653,11 @@ static GemmItem mk(const double2* A0, const double2* B0, const double2* A1, cons
   it.m = m; it.n = n; it.k = k; it.nseg = nseg; it.lda = lda; it.ldb = ldb; it.ldc = ldc; it.diag = diag;
   it.tiles_n = (n + GBN - 1) / GBN;
   return it;
+}
+
+static bool herm_enabled() {  // SQOC_HERM=0: compute the mirror tiles of Hermitian products too (A/B)
+  const char* e = getenv("SQOC_HERM");
+  return !(e && e[0] == '0');
 }
 
 // Work-list item(s) of scheme step k for one d x d block.  slot(c) / dslot(c) give the block's
@@ -633,6 +679,8 @@ static void push_step(std::vector<GemmItem>& v, const PolyScheme& sc, int k, int
   if (fwd) {
     GemmItem it = mk(slot(st.L), slot(st.R), 0, 0, slot(st.out[0].slot), 0, 0, d, d, d, 1, d, d, d, 1);
     epi(it, slot);
+    // A and A3 are anti-Hermitian (A = -i dt H), so A A and A3 A3 are Hermitian: half the tiles
+    it.herm = (st.L == st.R && (st.L == 0 || st.L == 2) && herm_enabled()) ? 1 : 0;
     v.push_back(it);
   }
   if (deriv) {
@@ -729,12 +777,12 @@ static int gemm(LargeGroup& g, int op, int p, int q, int r, GemmArgs a, cudaStre
   gemm_begin(g, l, st);
   cudaError_t e;
   switch (op) {
-    case B_C: e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
-    case B_D: e = launch_gemm<OP_C, OP_N, EPI_TRACE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
-    case B_XL: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
-    case B_UC: e = launch_gemm<OP_C, OP_N, EPI_MIXED>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
-    case B_M: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
-    default: e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st); break;
+    case B_C: e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles); break;
+    case B_D: e = launch_gemm<OP_C, OP_N, EPI_TRACE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles); break;
+    case B_XL: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles); break;
+    case B_UC: e = launch_gemm<OP_C, OP_N, EPI_MIXED>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles); break;
+    case B_M: e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles); break;
+    default: e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles); break;
   }
   gemm_end(g, st);
   if (e != cudaSuccess) {
@@ -938,26 +986,42 @@ static int sp_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks) {
     const LargeBlockSpec& bs = blocks[b];
     const int d = bs.d, nnz = (int)bs.sp_ci.size();
     maxd = std::max(maxd, d);
-    // row and column ELL layouts of the union pattern (entry e of row / column x at e * d + x)
+    // row and column ELL layouts of the union pattern, rows / columns sorted by entry count (longest
+    // first; entry e of the row at sorted position t at e * d + t) with per-32-chunk loop bounds
     std::vector<int> rcount(d, 0), ccount(d, 0);
     for (int i = 0; i < d; ++i) {
       rcount[i] = bs.sp_rp[i + 1] - bs.sp_rp[i];
       for (int e = bs.sp_rp[i]; e < bs.sp_rp[i + 1]; ++e) ccount[bs.sp_ci[e]]++;
     }
-    const int wr = std::max(1, *std::max_element(rcount.begin(), rcount.end()));
-    const int wc = std::max(1, *std::max_element(ccount.begin(), ccount.end()));
+    auto up4 = [](int x) { return (std::max(1, x) + 3) & ~3; };  // the kernels read entry groups of 4
+    const int wr = up4(*std::max_element(rcount.begin(), rcount.end()));
+    const int wc = up4(*std::max_element(ccount.begin(), ccount.end()));
+    auto sorted_by = [&](const std::vector<int>& cnt, std::vector<int>& perm, std::vector<int>& pos,
+                         std::vector<int>& chunk) {
+      perm.resize(d);
+      for (int i = 0; i < d; ++i) perm[i] = i;
+      std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return cnt[x] > cnt[y]; });
+      pos.resize(d);
+      for (int t = 0; t < d; ++t) pos[perm[t]] = t;
+      chunk.assign((d + 31) / 32, 0);
+      for (int t = 0; t < d; ++t) chunk[t / 32] = std::max(chunk[t / 32], cnt[perm[t]]);
+    };
+    std::vector<int> r_perm, r_pos, r_cnt, c_perm, c_pos, c_cnt;
+    sorted_by(rcount, r_perm, r_pos, r_cnt);
+    sorted_by(ccount, c_perm, c_pos, c_cnt);
     std::vector<int> r_idx((size_t)wr * d, 0), c_idx((size_t)wc * d, 0);
     std::vector<double2> r_gv((size_t)K1 * wr * d, make_double2(0.0, 0.0)), c_gv((size_t)K1 * wc * d, make_double2(0.0, 0.0));
     std::vector<int> cfill(d, 0);
     for (int i = 0; i < d; ++i)  // rows ascending: each column's entries in row order
       for (int e = bs.sp_rp[i]; e < bs.sp_rp[i + 1]; ++e) {
         const int er = e - bs.sp_rp[i], c = bs.sp_ci[e], ec = cfill[c]++;
-        r_idx[(size_t)er * d + i] = c;
-        c_idx[(size_t)ec * d + c] = i;
+        const size_t ri = (size_t)er * d + r_pos[i], cj = (size_t)ec * d + c_pos[c];
+        r_idx[ri] = c;
+        c_idx[cj] = i;
         for (int k = 0; k < K1; ++k) {
           const double2 v = bs.sp_gv[(size_t)k * nnz + e];
-          r_gv[((size_t)k * wr + er) * d + i] = v;
-          c_gv[((size_t)k * wc + ec) * d + c] = v;
+          r_gv[(size_t)k * wr * d + ri] = v;
+          c_gv[(size_t)k * wc * d + cj] = v;
         }
       }
     auto up = [&](const void* src, size_t bytes) -> void* {
@@ -971,13 +1035,18 @@ static int sp_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks) {
     h.d = d;
     h.wr = wr;
     h.wc = wc;
+    h.r_perm = static_cast<const int*>(up(r_perm.data(), r_perm.size() * sizeof(int)));
+    h.c_perm = static_cast<const int*>(up(c_perm.data(), c_perm.size() * sizeof(int)));
+    h.r_cnt = static_cast<const int*>(up(r_cnt.data(), r_cnt.size() * sizeof(int)));
+    h.c_cnt = static_cast<const int*>(up(c_cnt.data(), c_cnt.size() * sizeof(int)));
     h.r_idx = static_cast<const int*>(up(r_idx.data(), r_idx.size() * sizeof(int)));
     h.c_idx = static_cast<const int*>(up(c_idx.data(), c_idx.size() * sizeof(int)));
     h.r_gv = static_cast<const double2*>(up(r_gv.data(), r_gv.size() * sizeof(double2)));
     h.c_gv = static_cast<const double2*>(up(c_gv.data(), c_gv.size() * sizeof(double2)));
     h.r_sv = static_cast<double2*>(up(nullptr, (size_t)wr * d * sizeof(double2)));
     h.c_sv = static_cast<double2*>(up(nullptr, (size_t)wc * d * sizeof(double2)));
-    if (!h.r_idx || !h.c_idx || !h.r_gv || !h.c_gv || !h.r_sv || !h.c_sv) {
+    if (!h.r_perm || !h.c_perm || !h.r_cnt || !h.c_cnt || !h.r_idx || !h.c_idx || !h.r_gv || !h.c_gv || !h.r_sv ||
+        !h.c_sv) {
       g.err = "sparse pattern allocation failed";
       return SQOC_ERR_CUDA;
     }
@@ -1293,9 +1362,9 @@ static int hgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArgs
   }
   cudaError_t e;
   gemm_begin(g, l, st);
-  if (op == H_L) e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st);
-  else if (op == H_B) e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st);
-  else e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st);
+  if (op == H_L) e = launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles);
+  else if (op == H_B) e = launch_gemm<OP_N, OP_C, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles);
+  else e = launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles);
   gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
@@ -1372,8 +1441,8 @@ static int scan_gemm(LargeGroup& g, int op, int idx, int Lc, int C, cudaStream_t
   if (!l.n) return SQOC_OK;
   const GemmArgs one{1.0, 0.0, 0.0, 0.0};
   gemm_begin(g, l, st);
-  cudaError_t e = (op == H_LP1) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, one, st)
-                                : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, one, st);
+  cudaError_t e = (op == H_LP1) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, one, st, l.pt_tiles)
+                                : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, one, st, l.pt_tiles);
   gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);
@@ -1540,8 +1609,8 @@ static int svgemm(LargeGroup& g, int op, int idx, int p, int i0, int i1, GemmArg
     return SQOC_ERR_CUDA;
   }
   gemm_begin(g, l, st);
-  cudaError_t e = (op == SV_CHI) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st)
-                                 : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st);
+  cudaError_t e = (op == SV_CHI) ? launch_gemm<OP_C, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles)
+                                 : launch_gemm<OP_N, OP_N, EPI_STORE>(l.dev, l.maps, l.tref, g.pt_counter, l.n, l.tiles, a, st, l.pt_tiles);
   gemm_end(g, st);
   if (e != cudaSuccess) {
     g.err = std::string("zgemm launch: ") + cudaGetErrorString(e);

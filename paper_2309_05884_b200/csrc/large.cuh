@@ -63,6 +63,7 @@ struct ListRef {
   ItemMaps* maps = nullptr;  // TMA tensor maps per item (null: cp.async staging)
   TileRef* tref = nullptr;   // persistent kernel's tile list (cost-ordered)
   int n = 0, tiles = 0;
+  int pt_tiles = -1;  // tiles in tref (fewer than `tiles` when Hermitian items skip their mirror tiles)
   double macs = 0.0;  // complex multiply-adds of the list (sum m n k nseg), for the executed-FLOP count
 };
 

@@ -30,11 +30,18 @@ namespace sqoc {
 constexpr int kSpMaxW = 8;       // columns / rows per CTA (fewer when a panel would not fit)
 constexpr int kSpThreads = 512;  // 16 warps: one CTA per SM (panel smem), latency hidden by warps
 
-// Union pattern of a block's generators in two padded (ELL) layouts, entry e of row / column x at
-// [e * d + x] so that a warp's threads (consecutive x) read consecutive addresses; padding entries
-// carry index 0 and value 0.
+// Union pattern of a block's generators in two padded (ELL) layouts.  Rows (columns) are sorted by
+// their entry count, longest first: entry e of the row at sorted position t sits at [e * d + t], so
+// a warp's threads (consecutive t) read consecutive addresses and the 32 rows of a warp chunk have
+// nearly equal counts -- a chunk loops to its own maximum r_cnt[t / 32] instead of the block's
+// (d = 1179: 27.7 entries on average against 41).  Padding entries carry index 0 and value 0.
+// Chunks are claimed by the warps of a CTA through a shared counter, longest first.
 struct SpBlockDev {
-  int d, wr, wc;          // dimension, entries per row (max), entries per column (max)
+  int d, wr, wc;          // dimension, entries per row / column (max, rounded up to a multiple of 4)
+  const int* r_perm;      // [d] row at sorted position t
+  const int* c_perm;      // [d] column at sorted position t
+  const int* r_cnt;       // [ceil(d / 32)] entries of the longest row of each 32-chunk
+  const int* c_cnt;
   const int* r_idx;       // [wr][d] column of row entry e
   const int* c_idx;       // [wc][d] row of column entry e
   const double2* r_gv;    // [(K+1)][wr][d] unscaled a_0..a_K, row layout
@@ -81,6 +88,14 @@ __device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
   acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
 }
 
+// next 32-chunk of sorted rows / columns for this warp (-1: none left)
+__device__ __forceinline__ int sp_claim(int* next, int nchunks, int lane) {
+  int c = 0;
+  if (lane == 0) c = atomicAdd(next, 1);
+  c = __shfl_sync(0xffffffffu, c, 0);
+  return c < nchunks ? c : -1;
+}
+
 __device__ __forceinline__ int sp_find(const SpItem* items, int nitems, int tile) {
   int lo = 0, hi = nitems - 1;
   while (lo < hi) {
@@ -116,33 +131,77 @@ static __global__ void __launch_bounds__(kSpThreads) spmm_cols_kernel(const SpIt
                                                                const SpBlockDev* __restrict__ blocks, int W,
                                                                GemmArgs args) {
   extern __shared__ double2 panel[];  // [d][W]
+  __shared__ int next;
   const int idx = sp_find(items, nitems, blockIdx.x);
   const SpItem& it = items[idx];
   const SpBlockDev& bd = blocks[it.blk];
   const int d = bd.d;
   const int c0 = (blockIdx.x - it.tile_start) * W;
   const int w_here = min(W, d - c0);
-  for (int t = threadIdx.x; t < d * W; t += blockDim.x) {
-    const int r = t / W, w = t - r * W;
-    panel[t] = w < w_here ? it.D[(size_t)r * d + c0 + w] : make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) next = 0;
+  for (int t0 = threadIdx.x; t0 < d * W; t0 += 4 * blockDim.x) {  // 4 independent loads in flight per thread
+    double2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = t0 + q * blockDim.x;
+      const int r = t / W, w = t - r * W;
+      v[q] = (t < d * W && w < w_here) ? it.D[(size_t)r * d + c0 + w] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = t0 + q * blockDim.x;
+      if (t < d * W) panel[t] = v[q];
+    }
   }
   __syncthreads();
   const GemmItem g = sp_epi(it, d);
+  const int lane = threadIdx.x & 31;
   int sl[kSpMaxW];  // rotated slot of step w
 #pragma unroll
-  for (int w = 0; w < kSpMaxW; ++w) sl[w] = (w + (int)threadIdx.x) % W;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+  for (int w = 0; w < kSpMaxW; ++w) sl[w] = (w + lane) % W;
+  const int nchunks = (d + 31) >> 5;
+  for (int ch = sp_claim(&next, nchunks, lane); ch >= 0; ch = sp_claim(&next, nchunks, lane)) {
+    const int t = min(ch * 32 + lane, d - 1);  // the last chunk's spare lanes repeat row d - 1 (not stored)
+    const bool live = ch * 32 + lane < d;
+    const int i = bd.r_perm[t];
+    const int cnt = bd.r_cnt[ch];
     double2 acc[kSpMaxW];
 #pragma unroll
     for (int w = 0; w < kSpMaxW; ++w) acc[w] = make_double2(0.0, 0.0);
-#pragma unroll 4
-    for (int e = 0; e < bd.wr; ++e) {
-      const double2 s = bd.r_sv[(size_t)e * d + i];
-      const double2* pr = panel + bd.r_idx[(size_t)e * d + i] * W;
+    // groups of 4 entries, the next group's values and indices loaded (L2) while this one multiplies;
+    // the ELL height is padded to a multiple of 4 with zero entries, so a group never reads past it
+    const double2* sv = bd.r_sv + t;
+    const int* si = bd.r_idx + t;
+    double2 cs[4];
+    int ci[4];
 #pragma unroll
-      for (int w = 0; w < kSpMaxW; ++w)
-        if (w < W) cmac(acc[w], s, pr[sl[w]]);
+    for (int q = 0; q < 4; ++q) {
+      cs[q] = sv[(size_t)q * d];
+      ci[q] = si[(size_t)q * d];
     }
+    for (int e = 0; e < cnt; e += 4) {
+      double2 ns[4];
+      int ni[4];
+      const bool more = e + 4 < cnt;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ns[q] = more ? sv[(size_t)(e + 4 + q) * d] : make_double2(0.0, 0.0);
+        ni[q] = more ? si[(size_t)(e + 4 + q) * d] : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2* pr = panel + ci[q] * W;
+#pragma unroll
+        for (int w = 0; w < kSpMaxW; ++w)
+          if (w < W) cmac(acc[w], cs[q], pr[sl[w]]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cs[q] = ns[q];
+        ci[q] = ni[q];
+      }
+    }
+    if (!live) continue;
 #pragma unroll
     for (int w = 0; w < kSpMaxW; ++w) {
       if (w >= W) break;
@@ -163,33 +222,76 @@ static __global__ void __launch_bounds__(kSpThreads) spmm_rows_kernel(const SpIt
                                                                const SpBlockDev* __restrict__ blocks, int W,
                                                                GemmArgs args) {
   extern __shared__ double2 rowsT[];  // [d][W]: rowsT[r][w] = R[i0 + w][r]
+  __shared__ int next;
   const int idx = sp_find(items, nitems, blockIdx.x);
   const SpItem& it = items[idx];
   const SpBlockDev& bd = blocks[it.blk];
   const int d = bd.d;
   const int i0 = (blockIdx.x - it.tile_start) * W;
   const int w_here = min(W, d - i0);
-  for (int t = threadIdx.x; t < d * W; t += blockDim.x) {
-    const int w = t / d, r = t - w * d;  // coalesced global reads along r
-    rowsT[r * W + w] = w < w_here ? it.D[(size_t)(i0 + w) * d + r] : make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) next = 0;
+  for (int t0 = threadIdx.x; t0 < d * W; t0 += 4 * blockDim.x) {  // 4 independent loads in flight per thread
+    double2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = t0 + q * blockDim.x;
+      const int w = t / d, r = t - w * d;  // coalesced global reads along r
+      v[q] = (t < d * W && w < w_here) ? it.D[(size_t)(i0 + w) * d + r] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = t0 + q * blockDim.x;
+      const int w = t / d, r = t - w * d;
+      if (t < d * W) rowsT[r * W + w] = v[q];
+    }
   }
   __syncthreads();
   const GemmItem g = sp_epi(it, d);
+  const int lane = threadIdx.x & 31;
   int sl[kSpMaxW];
 #pragma unroll
-  for (int w = 0; w < kSpMaxW; ++w) sl[w] = (w + (int)threadIdx.x) % W;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+  for (int w = 0; w < kSpMaxW; ++w) sl[w] = (w + lane) % W;
+  const int nchunks = (d + 31) >> 5;
+  for (int ch = sp_claim(&next, nchunks, lane); ch >= 0; ch = sp_claim(&next, nchunks, lane)) {
+    const int t = min(ch * 32 + lane, d - 1);
+    const bool live = ch * 32 + lane < d;
+    const int c = bd.c_perm[t];
+    const int cnt = bd.c_cnt[ch];
     double2 acc[kSpMaxW];
 #pragma unroll
     for (int w = 0; w < kSpMaxW; ++w) acc[w] = make_double2(0.0, 0.0);
-#pragma unroll 4
-    for (int e = 0; e < bd.wc; ++e) {
-      const double2 s = bd.c_sv[(size_t)e * d + c];
-      const double2* rr = rowsT + bd.c_idx[(size_t)e * d + c] * W;
+    const double2* sv = bd.c_sv + t;  // entry groups of 4 with the next group prefetched (see the cols kernel)
+    const int* si = bd.c_idx + t;
+    double2 cs[4];
+    int ci[4];
 #pragma unroll
-      for (int w = 0; w < kSpMaxW; ++w)
-        if (w < W) cmac(acc[w], rr[sl[w]], s);
+    for (int q = 0; q < 4; ++q) {
+      cs[q] = sv[(size_t)q * d];
+      ci[q] = si[(size_t)q * d];
     }
+    for (int e = 0; e < cnt; e += 4) {
+      double2 ns[4];
+      int ni[4];
+      const bool more = e + 4 < cnt;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ns[q] = more ? sv[(size_t)(e + 4 + q) * d] : make_double2(0.0, 0.0);
+        ni[q] = more ? si[(size_t)(e + 4 + q) * d] : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2* rr = rowsT + ci[q] * W;
+#pragma unroll
+        for (int w = 0; w < kSpMaxW; ++w)
+          if (w < W) cmac(acc[w], rr[sl[w]], cs[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cs[q] = ns[q];
+        ci[q] = ni[q];
+      }
+    }
+    if (!live) continue;
 #pragma unroll
     for (int w = 0; w < kSpMaxW; ++w) {
       if (w >= W) break;
@@ -231,34 +333,55 @@ static __global__ void __launch_bounds__(kSpThreads) sp_trace_kernel(const SpTra
   const int d = bd.d;
   const int l0 = (blockIdx.x - it.tile_start) * W;
   const int w_here = min(W, d - l0);
-  for (int t = threadIdx.x; t < d * W; t += blockDim.x) {
-    const int w = t / d, p = t - w * d;
-    const double2 v = w < w_here ? it.U[(size_t)(l0 + w) * d + p] : make_double2(0.0, 0.0);
-    uT[p * W + w] = make_double2(v.x, -v.y);
+  for (int t0 = threadIdx.x; t0 < d * W; t0 += 4 * blockDim.x) {  // 4 independent loads in flight per thread
+    double2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = t0 + q * blockDim.x;
+      const int w = t / d, p = t - w * d;
+      v[q] = (t < d * W && w < w_here) ? it.U[(size_t)(l0 + w) * d + p] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = t0 + q * blockDim.x;
+      const int w = t / d, p = t - w * d;
+      if (t < d * W) uT[p * W + w] = make_double2(v[q].x, -v[q].y);
+    }
   }
   __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int sl[kSpMaxW];
 #pragma unroll
-  for (int w = 0; w < kSpMaxW; ++w) sl[w] = (w + (int)threadIdx.x) % W;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int w = 0; w < kSpMaxW; ++w) sl[w] = (w + lane) % W;
   const size_t nr = (size_t)bd.wr * d;
+  const int nchunks = (d + 31) >> 5;
   for (int k = 0; k < K; ++k) {
     const double2* gv = bd.r_gv + (size_t)(k + 1) * nr;
     double2 acc[kSpMaxW];
 #pragma unroll
     for (int w = 0; w < kSpMaxW; ++w) acc[w] = make_double2(0.0, 0.0);
-    for (int q = threadIdx.x; q < d; q += blockDim.x) {
+    // static chunk -> warp map: the reduction order below must not depend on which warp claimed what,
+    // so that repeated evaluations are bit-identical
+    const int nw = (int)(blockDim.x >> 5);
+    for (int ps = 0; ps * nw < nchunks; ++ps) {  // serpentine over the count-sorted chunks: balanced warps
+      const int ch = ps * nw + ((ps & 1) ? nw - 1 - warp : warp);
+      if (ch >= nchunks) continue;
+      const int tq = min(ch * 32 + lane, d - 1);
+      const bool live = ch * 32 + lane < d;
+      const int q = bd.r_perm[tq];
+      const int cnt = bd.r_cnt[ch];
       double2 t[kSpMaxW];
 #pragma unroll
       for (int w = 0; w < kSpMaxW; ++w) t[w] = make_double2(0.0, 0.0);
 #pragma unroll 4
-      for (int e = 0; e < bd.wr; ++e) {
-        const double2 a = gv[(size_t)e * d + q];
-        const double2* ur = uT + bd.r_idx[(size_t)e * d + q] * W;
+      for (int e = 0; e < cnt; ++e) {
+        const double2 a = gv[(size_t)e * d + tq];
+        const double2* ur = uT + bd.r_idx[(size_t)e * d + tq] * W;
 #pragma unroll
         for (int w = 0; w < kSpMaxW; ++w)
           if (w < W) cmac(t[w], a, ur[sl[w]]);
       }
+      if (!live) continue;
 #pragma unroll
       for (int w = 0; w < kSpMaxW; ++w) {
         if (w >= W) break;

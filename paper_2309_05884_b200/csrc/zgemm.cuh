@@ -40,6 +40,8 @@ struct GemmItem {
   int diag;           // gamma applies to this item
   int tile_start, tiles_n;
   int nF;
+  int herm;           // the product is Hermitian (X X with X = -X^dag): the persistent kernel computes the tiles on
+                      // and above the diagonal and stores the conjugate mirror of the ones above it
 };
 
 // C  = alpha  acc + sum_t beta_t  E_t + gamma  [diag] I

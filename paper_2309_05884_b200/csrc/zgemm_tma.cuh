@@ -33,10 +33,14 @@ constexpr int TMA_STAGE_BYTES = 2 * GBM * 8 * 16;  // A + B tiles: 64 x 8 comple
 constexpr size_t PT_SMEM = (size_t)PT_STAGES * TMA_STAGE_BYTES + 2 * PT_STAGES * 8 + 1024;  // ring + barriers + align
 
 // per work-list item and K segment: tensor maps of A and B in both staging orientations
-// (m[4 seg + 0] A as [m][k], + 1 A as [k][m] (op = conj-transpose), + 2 B as [k][n], + 3 B as [n][k]);
-// unused ones zero
+// (m[6 seg + 0] A as [m][k], + 1 A as [k][m] (op = conj-transpose), + 2 B as [k][n], + 3 B as [n][k],
+//  + 4 / + 5: the k-major views of A / B again as 3-D maps (8 columns, k, column block) whose one
+//  16 x 8 x 8 box lands as the same eight swizzled 8 x 8 blocks that eight 2-D boxes write -- one TMA
+//  instruction instead of eight for tiles whose 64 columns are all inside the full column blocks;
+//  the column-block extent is floor(cols / 8), so no box reads past a row's end); unused ones zero
 struct alignas(64) ItemMaps {
-  CUtensorMap m[8];
+  CUtensorMap m[12];
+  unsigned has3d;  // bit 2 seg + 0 / + 1: the 3-D map of A / B of segment seg was encoded
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -61,6 +65,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_s(uint32_t b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
@@ -69,27 +87,53 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Issue the TMA copies of K stage kt (segment and k0 from kt) into ring slot `st`.
 template <int TA, int TB>
 __device__ __forceinline__ void tma_issue_stage(const ItemMaps* mp, const GemmItem& it, int kt, int kt_per_seg,
-                                                int m0, int n0, uint8_t* slot, uint64_t* full) {
+                                                int m0, int n0, bool a3d, bool b3d, uint8_t* slot, uint64_t* full) {
   const int seg = kt / kt_per_seg;
   const int k0 = (kt - seg * kt_per_seg) * GBK;
-  const CUtensorMap* ma = &mp->m[4 * seg + (TA == OP_N ? 0 : 1)];
-  const CUtensorMap* mb = &mp->m[4 * seg + (TB == OP_N ? 2 : 3)];
+  const CUtensorMap* ma = &mp->m[6 * seg + (TA == OP_N ? 0 : 1)];
+  const CUtensorMap* mb = &mp->m[6 * seg + (TB == OP_N ? 2 : 3)];
   uint8_t* sA = slot;
   uint8_t* sB = slot + GBM * 8 * 16;
   mbar_arrive_expect(full, TMA_STAGE_BYTES);
   if (TA == OP_N) tma_load_2d(sA, ma, 2 * k0, m0, full);  // [m][k]: one 64-row box
+  else if (a3d && (mp->has3d >> (2 * seg) & 1u)) tma_load_3d(sA, &mp->m[6 * seg + 4], 0, k0, m0 >> 3, full);  // [k][m]: 8 blocks, one box
   else
 #pragma unroll
     for (int b = 0; b < GBM / 8; ++b) tma_load_2d(sA + b * 1024, ma, 2 * (m0 + 8 * b), k0, full);  // [k][m] blocks
-  if (TB == OP_N)
+  if (TB != OP_N) tma_load_2d(sB, mb, 2 * k0, n0, full);  // [n][k]: one 64-row box
+  else if (b3d && (mp->has3d >> (2 * seg + 1) & 1u)) tma_load_3d(sB, &mp->m[6 * seg + 5], 0, k0, n0 >> 3, full);  // [k][n]: 8 blocks, one box
+  else
 #pragma unroll
     for (int b = 0; b < GBN / 8; ++b) tma_load_2d(sB + b * 1024, mb, 2 * (n0 + 8 * b), k0, full);  // [k][n] blocks
-  else tma_load_2d(sB, mb, 2 * k0, n0, full);  // [n][k]: one 64-row box
 }
 
+// Warp layout of a tile with R x Cc valid 8 x 8 sub-tiles (R, Cc <= 8): the 8 MMA warps form a
+// (8 / WC) x WC grid of th x tw sub-tile warp tiles (th <= 4, tw <= 2: the accumulator array).  Full
+// tiles use 2 x 4 warps of 4 x 2; a ragged edge tile picks the grid with the smallest per-warp work
+// th * tw that still covers it (d = 1179: the 27-wide edge tiles run 4 x 2 warps of 2 x 2, half the
+// DMMAs per warp of the full layout, which would leave 4 of 8 warps idle).
+__host__ __device__ inline void pt_layout(int R, int Cc, int& th, int& tw, int& WC) {
+  th = 4; tw = 2; WC = 4;
+  int best = 8;
+  for (int wc = 1; wc <= 8; wc *= 2) {
+    const int wr = 8 / wc;
+    const int h = (R + wr - 1) / wr, w = (Cc + wc - 1) / wc;
+    if (h <= 4 && w <= 2 && h * w < best) {
+      best = h * w; th = h; tw = w; WC = wc;
+    }
+  }
+}
 
 struct TileRef {
   int item, m0, n0, local;  // work-list item, tile origin, tile index inside the item (trace partials)
@@ -102,21 +146,29 @@ struct Frag {
   double br[NC > 0 ? NC : 1], bi[NC > 0 ? NC : 1], bs[NC > 0 ? NC : 1];
 };
 
+// 16-byte fragment load by 32-bit shared address (LDS.128; a generic pointer derived from the aligned
+// dynamic-smem base compiles to generic LD.E.128 with 64-bit address arithmetic)
+__device__ __forceinline__ double2 lds_c128(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 template <int TA, int TB, int MC, int NC>
-__device__ __forceinline__ void frag_load(Frag<MC, NC>& f, const uint8_t* stage, int oa, int ob) {
+__device__ __forceinline__ void frag_load(Frag<MC, NC>& f, uint32_t stage, int oa, int ob) {
   constexpr int A_MI = (TA == OP_N) ? 8 * 128 : 1024;  // byte stride between the warp's 8-row sub-tiles
   constexpr int B_NI = (TB == OP_N) ? 1024 : 8 * 128;
-  const uint8_t* sA = stage;
-  const uint8_t* sB = stage + GBM * 8 * 16;
+  const uint32_t sA = stage + oa;
+  const uint32_t sB = stage + GBM * 8 * 16 + ob;
 #pragma unroll
   for (int mi = 0; mi < MC; ++mi) {
-    double2 a = *reinterpret_cast<const double2*>(sA + oa + mi * A_MI);
+    double2 a = lds_c128(sA + mi * A_MI);
     if (TA == OP_C) a.y = -a.y;
     f.ar[mi] = a.x; f.ai[mi] = a.y; f.as[mi] = a.x + a.y;
   }
 #pragma unroll
   for (int ni = 0; ni < NC; ++ni) {
-    double2 b = *reinterpret_cast<const double2*>(sB + ob + ni * B_NI);
+    double2 b = lds_c128(sB + ni * B_NI);
     if (TB == OP_C) b.y = -b.y;
     f.br[ni] = b.x; f.bi[ni] = b.y; f.bs[ni] = b.x + b.y;
   }
@@ -139,12 +191,11 @@ __device__ __forceinline__ void frag_mma(double (&acc)[4][2][3][2], const Frag<M
 // slice): this plain loop 102.1 / 83.0; a two-deep register pipeline of the fragments 106.2 / 87.0
 // (the 168-register cap of 9 warps spills); the producer fused into thread 0 (256 threads) 142 / 112.
 template <int TA, int TB, int MC, int NC>
-__device__ __forceinline__ void pt_mainloop(double (&acc)[4][2][3][2], const uint8_t* ring, uint64_t* full,
-                                            uint64_t* empty, uint32_t& g, int kt_total, const int (&offa)[2],
+__device__ __forceinline__ void pt_mainloop(double (&acc)[4][2][3][2], uint32_t ring, uint32_t full, uint32_t empty,
+                                            uint32_t& slot, uint32_t& phase, int kt_total, const int (&offa)[2],
                                             const int (&offb)[2], int lane) {
-  for (int kt = 0; kt < kt_total; ++kt, ++g) {
-    const uint32_t slot = g % PT_STAGES;
-    mbar_wait(&full[slot], (g / PT_STAGES) & 1);
+  for (int kt = 0; kt < kt_total; ++kt) {
+    mbar_wait_s(full + 8 * slot, phase);
     if constexpr (MC > 0 && NC > 0) {
       Frag<MC, NC> f;
 #pragma unroll
@@ -154,7 +205,8 @@ __device__ __forceinline__ void pt_mainloop(double (&acc)[4][2][3][2], const uin
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (lane == 0) mbar_arrive_s(empty + 8 * slot);
+    if (++slot == PT_STAGES) { slot = 0; phase ^= 1; }
   }
 }
 
@@ -201,32 +253,32 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
         const ItemMaps* mp = maps + tr.item;
         const int kt_per_seg = (it.k + GBK - 1) / GBK;
         const int kt_total = kt_per_seg * it.nseg;
+        const bool a3d = tr.m0 + GBM <= (it.m & ~7), b3d = tr.n0 + GBN <= (it.n & ~7);  // all 8 blocks full
         for (int kt = 0; kt < kt_total; ++kt, ++g) {
           const uint32_t slot = g % PT_STAGES;
           if (g >= PT_STAGES) mbar_wait(&empty[slot], ((g / PT_STAGES) - 1) & 1);
           if (kt == 0) stage_tile[slot] = t;
-          tma_issue_stage<TA, TB>(mp, it, kt, kt_per_seg, tr.m0, tr.n0, ring + slot * TMA_STAGE_BYTES, &full[slot]);
+          tma_issue_stage<TA, TB>(mp, it, kt, kt_per_seg, tr.m0, tr.n0, a3d, b3d, ring + slot * TMA_STAGE_BYTES,
+                                  &full[slot]);
         }
         t = gridDim.x + atomicAdd(counter, 1);
       }
     }
     return;
   }
-  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
   const int lr = lane >> 2, lc = lane & 3;
-  int offa[2], offb[2];
+  int rowmaj[2], kmaj[2];  // fragment byte offsets of this lane inside an 8-row / 8-column group, k-steps 0 and 1
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const int k = 2 * lc + s;
-    const int rowmaj = lr * 128 + ((k ^ lr) << 4);  // [row][k]: row * 128 + ((k ^ (row & 7)) * 16)
-    const int kmaj = k * 128 + ((lr ^ k) << 4);     // [k][col] 8 x 8 blocks: k * 128 + (((col & 7) ^ k) * 16)
-    offa[s] = (TA == OP_N ? rowmaj + wm * 128 : kmaj + (wm >> 3) * 1024);
-    offb[s] = (TB == OP_N ? kmaj + (wn >> 3) * 1024 : rowmaj + wn * 128);
+    rowmaj[s] = lr * 128 + ((k ^ lr) << 4);  // [row][k]: row * 128 + ((k ^ (row & 7)) * 16)
+    kmaj[s] = k * 128 + ((lr ^ k) << 4);     // [k][col] 8 x 8 blocks: k * 128 + (((col & 7) ^ k) * 16)
   }
-  uint32_t g = 0;
+  const uint32_t ring_s = smem_u32(ring), full_s = smem_u32(full), empty_s = smem_u32(empty);
+  uint32_t slot = 0, phase = 0;
   while (true) {
-    mbar_wait(&full[g % PT_STAGES], (g / PT_STAGES) & 1);
-    const int t = *reinterpret_cast<volatile int*>(&stage_tile[g % PT_STAGES]);
+    mbar_wait_s(full_s + 8 * slot, phase);
+    const int t = *reinterpret_cast<volatile int*>(&stage_tile[slot]);
     if (t < 0) break;
     const TileRef tr = tiles[t];
     const GemmItem& it = items[tr.item];
@@ -239,18 +291,29 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
       for (int b = 0; b < 2; ++b)
 #pragma unroll
         for (int c = 0; c < 3; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
-    const int mc = max(0, min(4, (it.m - m0 - wm + 7) / 8));
-    const int nc = max(0, min(2, (it.n - n0 - wn + 7) / 8));
+    int th, tw, WC;
+    const int R = min(8, (it.m - m0 + 7) / 8), Cc = min(8, (it.n - n0 + 7) / 8);
+    pt_layout(R, Cc, th, tw, WC);
+    const int wri = warp / WC, wci = warp - wri * WC;
+    const int wm = wri * th * 8, wn = wci * tw * 8;
+    const int mc = max(0, min(th, R - wri * th));
+    const int nc = max(0, min(tw, Cc - wci * tw));
+    int offa[2], offb[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      offa[s] = (TA == OP_N ? rowmaj[s] + wm * 128 : kmaj[s] + (wm >> 3) * 1024);
+      offb[s] = (TB == OP_N ? kmaj[s] + (wn >> 3) * 1024 : rowmaj[s] + wn * 128);
+    }
     switch ((mc == 0 || nc == 0) ? -1 : (mc - 1) * 2 + (nc - 1)) {
-      case 7: pt_mainloop<TA, TB, 4, 2>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
-      case 6: pt_mainloop<TA, TB, 4, 1>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
-      case 5: pt_mainloop<TA, TB, 3, 2>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
-      case 4: pt_mainloop<TA, TB, 3, 1>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
-      case 3: pt_mainloop<TA, TB, 2, 2>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
-      case 2: pt_mainloop<TA, TB, 2, 1>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
-      case 1: pt_mainloop<TA, TB, 1, 2>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
-      case 0: pt_mainloop<TA, TB, 1, 1>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
-      default: pt_mainloop<TA, TB, 0, 0>(acc, ring, full, empty, g, kt_total, offa, offb, lane); break;
+      case 7: pt_mainloop<TA, TB, 4, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
+      case 6: pt_mainloop<TA, TB, 4, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
+      case 5: pt_mainloop<TA, TB, 3, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
+      case 4: pt_mainloop<TA, TB, 3, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
+      case 3: pt_mainloop<TA, TB, 2, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
+      case 2: pt_mainloop<TA, TB, 2, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
+      case 1: pt_mainloop<TA, TB, 1, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
+      case 0: pt_mainloop<TA, TB, 1, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
+      default: pt_mainloop<TA, TB, 0, 0>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
     }
     const bool trace = EPI == EPI_TRACE || (EPI == EPI_MIXED && it.nF > 0);  // uniform per tile
     if (!trace) {
@@ -262,11 +325,26 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
           for (int v = 0; v < 2; ++v) {
             const int m = m0 + wm + mi * 8 + lr;
             const int n = n0 + wn + ni * 8 + 2 * lc + v;
-            if (m < it.m && n < it.n) {
+            if (mi < mc && ni < nc && m < it.m && n < it.n) {
               const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
               epi_store(it, args, m, n, t1 - t2, t3 - t1 - t2);
             }
           }
+      if (it.herm && n0 > m0) {  // Hermitian product, tile above the diagonal: (n, m) = conj (m, n)
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int m = m0 + wm + mi * 8 + lr;
+              const int n = n0 + wn + ni * 8 + 2 * lc + v;
+              if (mi < mc && ni < nc && m < it.m && n < it.n) {
+                const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
+                epi_store(it, args, n, m, t1 - t2, t1 + t2 - t3);
+              }
+            }
+      }
     } else {
       const int nF = it.nF;
       for (int f = 0; f < nF; ++f) {
@@ -280,7 +358,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
             for (int v = 0; v < 2; ++v) {
               const int p = m0 + wm + mi * 8 + lr;
               const int q = n0 + wn + ni * 8 + 2 * lc + v;
-              if (p < it.m && q < it.n) {
+              if (mi < mc && ni < nc && p < it.m && q < it.n) {
                 const double2 e = F[(size_t)q * it.ldc + p];
                 const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
                 const double cr = args.alpha * (t1 - t2), ci = args.alpha * (t3 - t1 - t2);
