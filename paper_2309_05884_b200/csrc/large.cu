@@ -808,7 +808,7 @@ static int gemm(LargeGroup& g, int op, int p, int q, int r, GemmArgs a, cudaStre
 //   SP_B0T backward step 0: A2 = S A (+ epilogue); T = S dA (raw)           (cols)
 //   SP_B0S backward step 0: dA2 = dA S + T (raw)                            (rows)
 //   SP_B1D backward step 1: dA3 = S T (raw)                                 (cols)
-enum SpOp { SP_F0, SP_F1, SP_B0R, SP_B0C, SP_B1, SP_B0T, SP_B0S, SP_B1D };
+enum SpOp { SP_F0, SP_F1, SP_B0R, SP_B0C, SP_B1, SP_B0T, SP_B0S, SP_B1D, SP_B0T1 };
 
 static SpListRef sp_list(LargeGroup& g, int op, int degree) {
   auto key = std::make_tuple(op, degree, 0, 0);
@@ -875,6 +875,7 @@ static SpListRef sp_list(LargeGroup& g, int op, int degree) {
         item(false, slot(st.R), false, false);
         item(true, dslot(st.R), true, false, dslot(3));
         break;
+      case SP_B0T1: item(true, dslot(st.R), true, false, dslot(3)); break;  // T = S dA only (A2 by spgemm_a2)
       case SP_B0S: item(true, dslot(st.L), true, true, nullptr, dslot(3)); break;
       case SP_B1D: item(true, dslot(3), true, false, dslot(2)); break;
     }
@@ -916,7 +917,7 @@ static int sp_launch(LargeGroup& g, int op, int degree, GemmArgs a, cudaStream_t
   }
   int rc = sp_smem_attr(g);
   if (rc) return rc;
-  const bool cols = op == SP_F0 || op == SP_B0C || op == SP_B0T || op == SP_B1D;
+  const bool cols = op == SP_F0 || op == SP_B0C || op == SP_B0T || op == SP_B1D || op == SP_B0T1;
   const size_t smem = g.sp_smem * g.sp_w;
   if (cols) spmm_cols_kernel<<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
   else spmm_rows_kernel<<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
@@ -926,7 +927,16 @@ static int sp_launch(LargeGroup& g, int op, int degree, GemmArgs a, cudaStream_t
 }
 
 // forward scheme step k (< 2) on the sparse A
+// A2 = A A on the squared pattern (step 0 of both schemes is a plain store of the product)
+static int sp_a2(LargeGroup& g, cudaStream_t st) {
+  spgemm_a2_kernel<<<dim3(128, g.nblk), 256, 0, st>>>(g.sp_dev, g.off_dev, g.A2);
+  LCHK(cudaGetLastError());
+  g.launches++;
+  return SQOC_OK;
+}
+
 static int sp_fwd_step(LargeGroup& g, int k, int degree, GemmArgs a, cudaStream_t st) {
+  if (k == 0 && g.sp_a2) return sp_a2(g, st);
   return sp_launch(g, k == 0 ? SP_F0 : SP_F1, degree, a, st);
 }
 
@@ -941,7 +951,10 @@ static int sp_pair_step(LargeGroup& g, int k, int degree, GemmArgs a, cudaStream
   const GemmArgs raw{1.0, 0.0, 0.0, 0.0};
   if (k == 0) {
     if (sp_chain()) {  // step 0's epilogue is a plain store (both schemes), so raw items may share it
-      if ((rc = sp_launch(g, SP_B0T, degree, a, st))) return rc;
+      if (g.sp_a2) {  // value A2 on its own pattern; only T = S dA remains an S x dense product
+        if ((rc = sp_a2(g, st))) return rc;
+        if ((rc = sp_launch(g, SP_B0T1, degree, raw, st))) return rc;
+      } else if ((rc = sp_launch(g, SP_B0T, degree, a, st))) return rc;
       return sp_launch(g, SP_B0S, degree, raw, st);
     }
     if ((rc = sp_launch(g, SP_B0R, degree, raw, st))) return rc;
@@ -980,6 +993,7 @@ static int sp_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks) {
     if (b.sp_rp.size() != (size_t)b.d + 1 || (double)b.sp_ci.size() > (double)b.d * b.d / 8.0) return SQOC_OK;
   std::vector<SpBlockDev> host(g.nblk);
   std::vector<int> rowoff(g.nblk + 1, 0);
+  bool a2_all = true;  // every block's A2 = A A pattern is small enough for the sparse x sparse kernel
   int maxd = 0;
   const int K1 = g.K + 1;
   for (int b = 0; b < g.nblk; ++b) {
@@ -1045,6 +1059,43 @@ static int sp_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks) {
     h.c_gv = static_cast<const double2*>(up(c_gv.data(), c_gv.size() * sizeof(double2)));
     h.r_sv = static_cast<double2*>(up(nullptr, (size_t)wr * d * sizeof(double2)));
     h.c_sv = static_cast<double2*>(up(nullptr, (size_t)wc * d * sizeof(double2)));
+    {  // symbolic A2 = A A: per nonzero (i, k) of the squared pattern the (A_ij, A_jk) pairs, j ascending
+      auto sv_off = [&](int i, int e) { return (e - bs.sp_rp[i]) * d + r_pos[i]; };  // CSR entry e of row i in r_sv
+      double est = 0.0;  // pair count; dense-ish patterns keep the S x dense product
+      for (int i = 0; i < d; ++i)
+        for (int e = bs.sp_rp[i]; e < bs.sp_rp[i + 1]; ++e) est += rcount[bs.sp_ci[e]];
+      a2_all = a2_all && est <= 4.0 * (double)d * d;
+      std::vector<int> a2_ptr(1, 0), a2_out;
+      std::vector<int2> a2_pairs;
+      std::vector<std::vector<int2>> acc(d);
+      std::vector<int> touched;
+      for (int i = 0; i < d && a2_all; ++i) {
+        touched.clear();
+        for (int e = bs.sp_rp[i]; e < bs.sp_rp[i + 1]; ++e) {
+          const int j = bs.sp_ci[e];
+          for (int f = bs.sp_rp[j]; f < bs.sp_rp[j + 1]; ++f) {
+            const int k = bs.sp_ci[f];
+            if (acc[k].empty()) touched.push_back(k);
+            acc[k].push_back(make_int2(sv_off(i, e), sv_off(j, f)));
+          }
+        }
+        std::sort(touched.begin(), touched.end());
+        for (int k : touched) {
+          a2_out.push_back(i * d + k);
+          a2_pairs.insert(a2_pairs.end(), acc[k].begin(), acc[k].end());
+          a2_ptr.push_back((int)a2_pairs.size());
+          acc[k].clear();
+        }
+      }
+      h.a2_nnz = (int)a2_out.size();
+      h.a2_ptr = static_cast<const int*>(up(a2_ptr.data(), a2_ptr.size() * sizeof(int)));
+      h.a2_out = static_cast<const int*>(up(a2_out.data(), a2_out.size() * sizeof(int)));
+      h.a2_pairs = static_cast<const int2*>(up(a2_pairs.data(), a2_pairs.size() * sizeof(int2)));
+      if (!h.a2_ptr || !h.a2_out || !h.a2_pairs) {
+        g.err = "sparse A2 pattern allocation failed";
+        return SQOC_ERR_CUDA;
+      }
+    }
     if (!h.r_perm || !h.c_perm || !h.r_cnt || !h.c_cnt || !h.r_idx || !h.c_idx || !h.r_gv || !h.c_gv || !h.r_sv ||
         !h.c_sv) {
       g.err = "sparse pattern allocation failed";
@@ -1077,6 +1128,8 @@ static int sp_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks) {
   LCHK(cudaMalloc(&g.sp_trace_dev, tr.size() * sizeof(SpTraceItem)));
   LCHK(cudaMemcpy(g.sp_trace_dev, tr.data(), tr.size() * sizeof(SpTraceItem), cudaMemcpyHostToDevice));
   g.sp_on = g.sp_smem <= (size_t)kSpMaxSmem;
+  const char* a2env = getenv("SQOC_SPGEMM");
+  g.sp_a2 = g.sp_on && a2_all && !(a2env && a2env[0] == '0');
   return SQOC_OK;
 }
 
@@ -1102,6 +1155,7 @@ int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, 
   const size_t bytes = g.total * sizeof(double2);
   double2** sq[] = {&g.A, &g.Ad, &g.A2, &g.dA2, &g.A3, &g.dA3, &g.T[0], &g.T[1], &g.dT[0], &g.dT[1]};
   for (auto pp : sq) LCHK(cudaMalloc(pp, bytes));
+  LCHK(cudaMemset(g.A2, 0, bytes));  // spgemm_a2_kernel writes the pattern of A A only: the rest stays zero
   for (int i = 0; i < 5; ++i) {
     LCHK(cudaMalloc(&g.xs[i], bytes));
     LCHK(cudaMalloc(&g.dxs[i], bytes));

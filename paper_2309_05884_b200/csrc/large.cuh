@@ -108,6 +108,7 @@ struct LargeGroup {
   // trace run as sparse x dense kernels in the slice-sequential schedule when every block's pattern is
   // sparse enough (sp_on; SQOC_SPARSE=0 disables) ----
   bool sp_on = false;
+  bool sp_a2 = false;                      // A2 = A A by spgemm_a2_kernel (SQOC_SPGEMM=0 disables)
   SpBlockDev* sp_dev = nullptr;            // [nblk]
   std::vector<void*> sp_mem;
   double2* sp_part = nullptr;              // [sum d][K] trace partials by row
