@@ -897,9 +897,12 @@ static int sp_smem_attr(LargeGroup& g) {
   static uint64_t done = 0;
   cudaError_t e = once_per_device(mu, done, [] {
     const auto a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    cudaError_t r = cudaFuncSetAttribute(spmm_cols_kernel, a, kSpMaxSmem);
-    if (r == cudaSuccess) r = cudaFuncSetAttribute(spmm_rows_kernel, a, kSpMaxSmem);
-    if (r == cudaSuccess) r = cudaFuncSetAttribute(sp_trace_kernel, a, kSpMaxSmem);
+    cudaError_t r = cudaFuncSetAttribute(spmm_cols_kernel<0>, a, kSpMaxSmem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(spmm_rows_kernel<0>, a, kSpMaxSmem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(sp_trace_kernel<0>, a, kSpMaxSmem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(spmm_cols_kernel<kSpMaxW>, a, kSpMaxSmem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(spmm_rows_kernel<kSpMaxW>, a, kSpMaxSmem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(sp_trace_kernel<kSpMaxW>, a, kSpMaxSmem);
     return r;
   });
   if (e != cudaSuccess) {
@@ -919,8 +922,11 @@ static int sp_launch(LargeGroup& g, int op, int degree, GemmArgs a, cudaStream_t
   if (rc) return rc;
   const bool cols = op == SP_F0 || op == SP_B0C || op == SP_B0T || op == SP_B1D || op == SP_B0T1;
   const size_t smem = g.sp_smem * g.sp_w;
-  if (cols) spmm_cols_kernel<<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
-  else spmm_rows_kernel<<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
+  const bool full_w = g.sp_w == kSpMaxW;  // compile-time panel width
+  if (cols && full_w) spmm_cols_kernel<kSpMaxW><<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
+  else if (cols) spmm_cols_kernel<0><<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
+  else if (full_w) spmm_rows_kernel<kSpMaxW><<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
+  else spmm_rows_kernel<0><<<l.rows, kSpThreads, smem, st>>>(l.dev, l.n, g.sp_dev, g.sp_w, a);
   LCHK(cudaGetLastError());
   g.launches++;
   return SQOC_OK;
@@ -975,8 +981,12 @@ static int sp_values(LargeGroup& g, int j, const double* u, double scale, cudaSt
 static int sp_trace(LargeGroup& g, int j, int p, const LargeArgs& a, int s_idx, cudaStream_t st) {
   int rc = sp_smem_attr(g);
   if (rc) return rc;
-  sp_trace_kernel<<<g.sp_trace_tiles, kSpThreads, g.sp_smem * g.sp_w, st>>>(g.sp_trace_dev + (size_t)p * g.nblk, g.nblk,
-                                                                     g.sp_dev, g.K, g.sp_w);
+  if (g.sp_w == kSpMaxW)
+    sp_trace_kernel<kSpMaxW><<<g.sp_trace_tiles, kSpThreads, g.sp_smem * g.sp_w, st>>>(
+        g.sp_trace_dev + (size_t)p * g.nblk, g.nblk, g.sp_dev, g.K, g.sp_w);
+  else
+    sp_trace_kernel<0><<<g.sp_trace_tiles, kSpThreads, g.sp_smem * g.sp_w, st>>>(g.sp_trace_dev + (size_t)p * g.nblk,
+                                                                         g.nblk, g.sp_dev, g.K, g.sp_w);
   LCHK(cudaGetLastError());
   trace_reduce_kernel<<<g.nblk, 256, 0, st>>>(j, g.K, g.N, g.sp_rowoff_dev, g.sp_part, g.tau_dev, g.w_dev, g.gidx_dev,
                                               a.gradb + (size_t)s_idx * g.K * g.N, a.gradb_block_stride);

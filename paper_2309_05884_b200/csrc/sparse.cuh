@@ -152,9 +152,13 @@ __device__ __forceinline__ GemmItem sp_epi(const SpItem& it, int d) {
 // output column / row (w + t) % W, a static register index.
 
 // C[:, c0:c0+W] = S L[:, c0:c0+W] (+ X), epilogue.  Dynamic smem: d x W double2 (the L panel).
+// WT > 0: the panel width as a compile-time constant (the usual 8: no width guards, shifts for the
+// panel index arithmetic); WT = 0: the run-time width Wrt (panels narrowed to fit shared memory).
+template <int WT>
 static __global__ void __launch_bounds__(kSpThreads) spmm_cols_kernel(const SpItem* __restrict__ items, int nitems,
-                                                               const SpBlockDev* __restrict__ blocks, int W,
+                                                               const SpBlockDev* __restrict__ blocks, int Wrt,
                                                                GemmArgs args) {
+  const int W = WT ? WT : Wrt;
   extern __shared__ double2 panel[];  // [d][W]
   __shared__ int next;
   const int idx = sp_find(items, nitems, blockIdx.x);
@@ -243,9 +247,11 @@ static __global__ void __launch_bounds__(kSpThreads) spmm_cols_kernel(const SpIt
 }
 
 // C[i0:i0+W, :] = R[i0:i0+W, :] S (+ X), epilogue.  Dynamic smem: d x W double2 (R rows, transposed).
+template <int WT>
 static __global__ void __launch_bounds__(kSpThreads) spmm_rows_kernel(const SpItem* __restrict__ items, int nitems,
-                                                               const SpBlockDev* __restrict__ blocks, int W,
+                                                               const SpBlockDev* __restrict__ blocks, int Wrt,
                                                                GemmArgs args) {
+  const int W = WT ? WT : Wrt;
   extern __shared__ double2 rowsT[];  // [d][W]: rowsT[r][w] = R[i0 + w][r]
   __shared__ int next;
   const int idx = sp_find(items, nitems, blockIdx.x);
@@ -343,8 +349,10 @@ struct SpTraceItem {
   double2* part;  // [d][K] of this block
 };
 
+template <int WT>
 static __global__ void __launch_bounds__(kSpThreads) sp_trace_kernel(const SpTraceItem* __restrict__ items, int nitems,
-                                                              const SpBlockDev* __restrict__ blocks, int K, int W) {
+                                                              const SpBlockDev* __restrict__ blocks, int K, int Wrt) {
+  const int W = WT ? WT : Wrt;
   extern __shared__ double2 uT[];  // [d][W]: uT[p][w] = conj(U[l0 + w][p])
   __shared__ double2 red[kSpMaxW][kSpThreads / 32];
   int lo = 0, hi = nitems - 1;

@@ -28,9 +28,26 @@
 
 namespace sqoc {
 
-constexpr int PT_STAGES = 12;
-constexpr int TMA_STAGE_BYTES = 2 * GBM * 8 * 16;  // A + B tiles: 64 x 8 complex each
-constexpr size_t PT_SMEM = (size_t)PT_STAGES * TMA_STAGE_BYTES + 2 * PT_STAGES * 8 + 1024;  // ring + barriers + align
+// Operand-sum planes (build with -DSQOC_PT_SUMS=1; default off): two helper warps form the Gauss operand
+// sums Re + Im of every landed stage once per CTA (512 per operand) and store them beside the tiles, so
+// the MMA warps issue no DADDs (each of the 8 warps forms the sums of its own fragments otherwise:
+// 3072 DADD lanes per stage; the bare loop loses 8% to them, profiles/r02_dmma_loop_probe.txt v1 vs
+// v2).  Measured and rejected (r02, cfg 3, GEMM ms per 6 slices, same day): 329.0 with the DADDs,
+// 371.1 with the planes (434.0 before the helper's 16 loads were batched) -- the 9-stage ring, the
+// extra full -> ready hop and 12 more LDS.64 per MMA warp and stage cost more than the DADDs did.
+#ifndef SQOC_PT_SUMS
+#define SQOC_PT_SUMS 0
+#endif
+constexpr bool kPtSums = SQOC_PT_SUMS != 0;
+#ifndef SQOC_PT_STAGES
+#define SQOC_PT_STAGES (SQOC_PT_SUMS ? 9 : 12)
+#endif
+constexpr int PT_STAGES = SQOC_PT_STAGES;
+constexpr int TMA_STAGE_BYTES = 2 * GBM * 8 * 16;  // A + B tiles: 64 x 8 complex each (the TMA byte count)
+constexpr int PT_SUM_BYTES = GBM * 8 * 8;           // one operand's sums: 64 x 8 doubles
+constexpr int PT_SLOT_BYTES = TMA_STAGE_BYTES + (kPtSums ? 2 * PT_SUM_BYTES : 0);  // ring slot stride
+constexpr int PT_HELPERS = kPtSums ? 2 : 0;         // helper warps (A sums, B sums)
+constexpr size_t PT_SMEM = (size_t)PT_STAGES * PT_SLOT_BYTES + 3 * PT_STAGES * 8 + 1024;  // ring + barriers + align
 
 // per work-list item and K segment: tensor maps of A and B in both staging orientations
 // (m[6 seg + 0] A as [m][k], + 1 A as [k][m] (op = conj-transpose), + 2 B as [k][n], + 3 B as [n][k],
@@ -154,8 +171,22 @@ __device__ __forceinline__ double2 lds_c128(uint32_t addr) {
   return v;
 }
 
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_c128(uint32_t addr, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(x), "d"(y) : "memory");
+}
+
+// Sum plane of one operand: [index 0..63][k 0..7] doubles, 64-byte rows, index = the tile row (column
+// for k-major operands); k is stored at k ^ ((index >> 1) & 1) so that the 16 lanes of an LDS.64 phase
+// (4 rows x 4 k) hit 16 different 8-byte bank pairs.
+__device__ __forceinline__ int sum_off(int idx, int k) { return idx * 64 + ((k ^ ((idx >> 1) & 1)) << 3); }
+
 template <int TA, int TB, int MC, int NC>
-__device__ __forceinline__ void frag_load(Frag<MC, NC>& f, uint32_t stage, int oa, int ob) {
+__device__ __forceinline__ void frag_load(Frag<MC, NC>& f, uint32_t stage, int oa, int ob, int osa, int osb) {
   constexpr int A_MI = (TA == OP_N) ? 8 * 128 : 1024;  // byte stride between the warp's 8-row sub-tiles
   constexpr int B_NI = (TB == OP_N) ? 1024 : 8 * 128;
   const uint32_t sA = stage + oa;
@@ -164,18 +195,79 @@ __device__ __forceinline__ void frag_load(Frag<MC, NC>& f, uint32_t stage, int o
   for (int mi = 0; mi < MC; ++mi) {
     double2 a = lds_c128(sA + mi * A_MI);
     if (TA == OP_C) a.y = -a.y;
-    f.ar[mi] = a.x; f.ai[mi] = a.y; f.as[mi] = a.x + a.y;
+    f.ar[mi] = a.x; f.ai[mi] = a.y;
+    if constexpr (kPtSums) f.as[mi] = lds_f64(stage + TMA_STAGE_BYTES + osa + mi * 512);
+    else f.as[mi] = a.x + a.y;
   }
 #pragma unroll
   for (int ni = 0; ni < NC; ++ni) {
     double2 b = lds_c128(sB + ni * B_NI);
     if (TB == OP_C) b.y = -b.y;
-    f.br[ni] = b.x; f.bi[ni] = b.y; f.bs[ni] = b.x + b.y;
+    f.br[ni] = b.x; f.bi[ni] = b.y;
+    if constexpr (kPtSums) f.bs[ni] = lds_f64(stage + TMA_STAGE_BYTES + PT_SUM_BYTES + osb + ni * 512);
+    else f.bs[ni] = b.x + b.y;
   }
 }
 
+// Helper warp: the 512 sums Re +- Im (conjugated operands: Re - Im) of one operand tile of a landed
+// stage.  Lane handles tile indices lane and lane + 32.  At step q index idx works on the k pair
+// pi((idx >> 1) & 3) ^ q with pi = (0, 2, 3, 1): both pi(a) and pi(a) ^ a are permutations of 0..3, so
+// the 8 lanes of a phase read 8 different swizzled 16-byte chunks (chunk = k ^ (idx & 7)) and store
+// to 8 different bank groups (group = 4 (idx & 1) + pair).  kmajor: the tile is eight
+// [k][8 columns] blocks, else [index][k] rows.
+template <bool KMAJOR, bool CONJ>
+__device__ __forceinline__ void sum_tile(uint32_t src, uint32_t dst, int lane) {
+  double2 v[2][4][2];  // all 16 loads in flight before the first sum (one shared-memory latency per stage)
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int idx = lane + 32 * j;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = ((0x78 >> (2 * ((idx >> 1) & 3))) & 3) ^ q;  // k pair (2p, 2p + 1)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = 2 * p + h;
+        const uint32_t a = KMAJOR ? src + (idx >> 3) * 1024 + k * 128 + ((((idx & 7) ^ k)) << 4)
+                                  : src + idx * 128 + (((k ^ (idx & 7))) << 4);
+        v[j][q][h] = lds_c128(a);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int idx = lane + 32 * j;
+    const int b = (idx >> 1) & 1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = ((0x78 >> (2 * ((idx >> 1) & 3))) & 3) ^ q;
+      const double s0 = CONJ ? v[j][q][0].x - v[j][q][0].y : v[j][q][0].x + v[j][q][0].y;
+      const double s1 = CONJ ? v[j][q][1].x - v[j][q][1].y : v[j][q][1].x + v[j][q][1].y;
+      sts_c128(dst + idx * 64 + p * 16, b ? s1 : s0, b ? s0 : s1);
+    }
+  }
+}
+
+// SQOC_MMA_ORDER 1: the two Gauss products that need no operand sums first, for every sub-tile, then
+// the third ones -- the DADDs that form the sums complete behind 2 MC NC DMMAs instead of stalling
+// the first sub-tile's third product (the asm statements keep their program order).
+#ifndef SQOC_MMA_ORDER
+#define SQOC_MMA_ORDER 0
+#endif
 template <int MC, int NC>
 __device__ __forceinline__ void frag_mma(double (&acc)[4][2][3][2], const Frag<MC, NC>& f) {
+#if SQOC_MMA_ORDER
+#pragma unroll
+  for (int mi = 0; mi < MC; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NC; ++ni) {
+      dmma(acc[mi][ni][0][0], acc[mi][ni][0][1], f.ar[mi], f.br[ni]);
+      dmma(acc[mi][ni][1][0], acc[mi][ni][1][1], f.ai[mi], f.bi[ni]);
+    }
+#pragma unroll
+  for (int mi = 0; mi < MC; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NC; ++ni) dmma(acc[mi][ni][2][0], acc[mi][ni][2][1], f.as[mi], f.bs[ni]);
+#else
 #pragma unroll
   for (int mi = 0; mi < MC; ++mi)
 #pragma unroll
@@ -184,6 +276,7 @@ __device__ __forceinline__ void frag_mma(double (&acc)[4][2][3][2], const Frag<M
       dmma(acc[mi][ni][1][0], acc[mi][ni][1][1], f.ai[mi], f.bi[ni]);
       dmma(acc[mi][ni][2][0], acc[mi][ni][2][1], f.as[mi], f.bs[ni]);
     }
+#endif
 }
 
 // kt_total K stages of one tile for a warp whose valid output is MC x NC DMMA sub-tiles; every warp
@@ -193,14 +286,14 @@ __device__ __forceinline__ void frag_mma(double (&acc)[4][2][3][2], const Frag<M
 template <int TA, int TB, int MC, int NC>
 __device__ __forceinline__ void pt_mainloop(double (&acc)[4][2][3][2], uint32_t ring, uint32_t full, uint32_t empty,
                                             uint32_t& slot, uint32_t& phase, int kt_total, const int (&offa)[2],
-                                            const int (&offb)[2], int lane) {
+                                            const int (&offb)[2], const int (&osa)[2], const int (&osb)[2], int lane) {
   for (int kt = 0; kt < kt_total; ++kt) {
-    mbar_wait_s(full + 8 * slot, phase);
+    mbar_wait_s(full + 8 * slot, phase);  // `full` is the helpers' ready barrier when the sum planes are on
     if constexpr (MC > 0 && NC > 0) {
       Frag<MC, NC> f;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        frag_load<TA, TB>(f, ring + slot * TMA_STAGE_BYTES, offa[s], offb[s]);
+        frag_load<TA, TB>(f, ring + slot * PT_SLOT_BYTES, offa[s], offb[s], osa[s], osb[s]);
         frag_mma(acc, f);
       }
     }
@@ -210,7 +303,7 @@ __device__ __forceinline__ void pt_mainloop(double (&acc)[4][2][3][2], uint32_t 
   }
 }
 
-constexpr int PT_THREADS = G3THREADS + 32;  // 8 MMA warps + 1 producer warp
+constexpr int PT_THREADS = G3THREADS + 32 + 32 * PT_HELPERS;  // 8 MMA warps + 1 producer warp + helper warps
 
 template <int TA, int TB, int EPI>
 __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmItem* __restrict__ items,
@@ -221,13 +314,15 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
   __shared__ double2 red[G3THREADS / 32][4];
   __shared__ int stage_tile[PT_STAGES];  // tile index announced with a tile's first stage; -1 = done
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + PT_STAGES * TMA_STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + PT_STAGES * PT_SLOT_BYTES);
   uint64_t* empty = full + PT_STAGES;
+  uint64_t* ready = empty + PT_STAGES;  // sum planes written (one arrival per helper warp)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < PT_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], G3THREADS / 32);
+      mbar_init(&ready[s], PT_HELPERS > 0 ? PT_HELPERS : 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -258,10 +353,36 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
           const uint32_t slot = g % PT_STAGES;
           if (g >= PT_STAGES) mbar_wait(&empty[slot], ((g / PT_STAGES) - 1) & 1);
           if (kt == 0) stage_tile[slot] = t;
-          tma_issue_stage<TA, TB>(mp, it, kt, kt_per_seg, tr.m0, tr.n0, a3d, b3d, ring + slot * TMA_STAGE_BYTES,
+          tma_issue_stage<TA, TB>(mp, it, kt, kt_per_seg, tr.m0, tr.n0, a3d, b3d, ring + slot * PT_SLOT_BYTES,
                                   &full[slot]);
         }
         t = gridDim.x + atomicAdd(counter, 1);
+      }
+    }
+    return;
+  }
+  if (warp > G3THREADS / 32) {
+    // ---- helper warps (sum planes): warp 9 the A tile, warp 10 the B tile of every landed stage ----
+    const bool isB = warp == G3THREADS / 32 + 2;
+    const uint32_t ring_h = smem_u32(ring), full_h = smem_u32(full), ready_h = smem_u32(ready);
+    uint32_t slot = 0, phase = 0;
+    while (true) {
+      mbar_wait_s(full_h + 8 * slot, phase);
+      const int t = *reinterpret_cast<volatile int*>(&stage_tile[slot]);
+      if (t < 0) {  // pass the end marker on to the MMA warps
+        if (lane == 0) mbar_arrive_s(ready_h + 8 * slot);
+        break;
+      }
+      const GemmItem& it = items[tiles[t].item];
+      const int kt_total = ((it.k + GBK - 1) / GBK) * it.nseg;
+      for (int kt = 0; kt < kt_total; ++kt) {
+        if (kt) mbar_wait_s(full_h + 8 * slot, phase);
+        const uint32_t st = ring_h + slot * PT_SLOT_BYTES;
+        if (!isB) sum_tile<TA != OP_N, TA == OP_C>(st, st + TMA_STAGE_BYTES, lane);
+        else sum_tile<TB == OP_N, TB == OP_C>(st + GBM * 8 * 16, st + TMA_STAGE_BYTES + PT_SUM_BYTES, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_s(ready_h + 8 * slot);
+        if (++slot == PT_STAGES) { slot = 0; phase ^= 1; }
       }
     }
     return;
@@ -274,7 +395,10 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
     rowmaj[s] = lr * 128 + ((k ^ lr) << 4);  // [row][k]: row * 128 + ((k ^ (row & 7)) * 16)
     kmaj[s] = k * 128 + ((lr ^ k) << 4);     // [k][col] 8 x 8 blocks: k * 128 + (((col & 7) ^ k) * 16)
   }
-  const uint32_t ring_s = smem_u32(ring), full_s = smem_u32(full), empty_s = smem_u32(empty);
+  const uint32_t ring_s = smem_u32(ring), full_s = smem_u32(kPtSums ? ready : full), empty_s = smem_u32(empty);
+  int sumo[2];  // sum-plane byte offsets of this lane inside an 8-index group (k-steps 0 and 1)
+#pragma unroll
+  for (int s = 0; s < 2; ++s) sumo[s] = sum_off(lr, 2 * lc + s);
   uint32_t slot = 0, phase = 0;
   while (true) {
     mbar_wait_s(full_s + 8 * slot, phase);
@@ -298,22 +422,24 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
     const int wm = wri * th * 8, wn = wci * tw * 8;
     const int mc = max(0, min(th, R - wri * th));
     const int nc = max(0, min(tw, Cc - wci * tw));
-    int offa[2], offb[2];
+    int offa[2], offb[2], osa[2], osb[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       offa[s] = (TA == OP_N ? rowmaj[s] + wm * 128 : kmaj[s] + (wm >> 3) * 1024);
       offb[s] = (TB == OP_N ? kmaj[s] + (wn >> 3) * 1024 : rowmaj[s] + wn * 128);
+      osa[s] = sumo[s] + wm * 64;
+      osb[s] = sumo[s] + wn * 64;
     }
     switch ((mc == 0 || nc == 0) ? -1 : (mc - 1) * 2 + (nc - 1)) {
-      case 7: pt_mainloop<TA, TB, 4, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
-      case 6: pt_mainloop<TA, TB, 4, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
-      case 5: pt_mainloop<TA, TB, 3, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
-      case 4: pt_mainloop<TA, TB, 3, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
-      case 3: pt_mainloop<TA, TB, 2, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
-      case 2: pt_mainloop<TA, TB, 2, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
-      case 1: pt_mainloop<TA, TB, 1, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
-      case 0: pt_mainloop<TA, TB, 1, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
-      default: pt_mainloop<TA, TB, 0, 0>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, lane); break;
+      case 7: pt_mainloop<TA, TB, 4, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, osa, osb, lane); break;
+      case 6: pt_mainloop<TA, TB, 4, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, osa, osb, lane); break;
+      case 5: pt_mainloop<TA, TB, 3, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, osa, osb, lane); break;
+      case 4: pt_mainloop<TA, TB, 3, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, osa, osb, lane); break;
+      case 3: pt_mainloop<TA, TB, 2, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, osa, osb, lane); break;
+      case 2: pt_mainloop<TA, TB, 2, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, osa, osb, lane); break;
+      case 1: pt_mainloop<TA, TB, 1, 2>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, osa, osb, lane); break;
+      case 0: pt_mainloop<TA, TB, 1, 1>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, osa, osb, lane); break;
+      default: pt_mainloop<TA, TB, 0, 0>(acc, ring_s, full_s, empty_s, slot, phase, kt_total, offa, offb, osa, osb, lane); break;
     }
     const bool trace = EPI == EPI_TRACE || (EPI == EPI_MIXED && it.nF > 0);  // uniform per tile
     if (!trace) {

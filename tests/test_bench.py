@@ -95,3 +95,15 @@ def test_gate_compare_raises_on_mismatch():
         bench._compare(0.5, np.ones(3), 0.5 + 1e-9, np.ones(3), "F off", rep)
     with pytest.raises(bench.CorrectnessGateError):
         bench._compare(0.5, np.ones(3), 0.5, np.ones(3) * (1 + 1e-6), "grad off", rep)
+
+
+def test_gemm_kernel_name_follows_the_staging_rule():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    # large.cu upload_list: lists with mean K x segments >= 256 run the persistent TMA kernel
+    assert bench.gemm_kernel_name(3, [687, 495, 1179]) == "zgemm3m_pt_kernel"
+    assert bench.gemm_kernel_name(3, [30, 105, 13]) == "zgemm3m_kernel"  # tiny blocks (<= 16) never reach a GEMM
+    assert bench.gemm_kernel_name(3, [4096]) == "zgemm3m_pt_kernel"
+    assert bench.gemm_kernel_name(4, [4096]) == "zgemm_kernel"
+    assert "/" in bench.gemm_kernel_name(3, [105, 1179])

@@ -60,22 +60,35 @@ def main():
     for grid in args.grids.split(","):
         G, C = (int(x) for x in grid.split("x"))
         world = G * C
-        ranks = [parallel.ShardedObjective(s, None, lambda x: GrapeEngine(x, max_batch=1), G, rank=r, world=world)
-                 for r in range(world)]
-        for r in ranks:
-            r.eng.set_timing(True)
+        # one rank's engine at a time (each keeps its chunk's propagator history: 8 ranks of cfg 3 do not
+        # fit one GPU together): pass 1 times every rank's chunk forward and keeps the packed products,
+        # pass 2 rebuilds each rank's forward state (untimed) and times its chunk backward
+        def make(r):
+            o = parallel.ShardedObjective(s, None, lambda x: GrapeEngine(x, max_batch=1), G, rank=r, world=world)
+            o.eng.set_timing(True)
+            return o
+
         fwd, packed = [], []
-        for r in ranks:
-            p, ms = timed(lambda: r.stage_forward(u_t))
-            packed.append(p)
+        for r in range(world):
+            o = make(r)
+            p, ms = timed(lambda: o.stage_forward(u_t))
+            packed.append(p.clone())
             fwd.append(ms)
+            o.eng.close()
+            del o
+            torch.cuda.empty_cache()
         bwd, carry, rows = [], [], []
-        for r in ranks:
-            gathered = torch.stack(packed[r.g * C:(r.g + 1) * C]) if C > 1 else None
-            row, ms = timed(lambda: r.stage_backward(u_t, gathered))
-            rows.append(row)
+        for r in range(world):
+            o = make(r)
+            o.stage_forward(u_t)
+            gathered = torch.stack(packed[o.g * C:(o.g + 1) * C]) if C > 1 else None
+            row, ms = timed(lambda: o.stage_backward(u_t, gathered))
+            rows.append(row.clone())
             bwd.append(ms)
-            carry.append(r.eng.carry_stats())
+            carry.append(o.eng.carry_stats())
+            o.eng.close()
+            del o
+            torch.cuda.empty_cache()
         tot = parallel.ShardedObjective.reduce_rows(torch.stack(rows))
         per = [f + b for f, b in zip(fwd, bwd)]
         crit = max(per)
@@ -87,9 +100,7 @@ def main():
             rec["projected_efficiency_compute_only"] = out["single_ms"] / (world * crit)
         out["grids"].append(rec)
         print(json.dumps(rec), flush=True)
-        for r in ranks:
-            r.eng.close()
-        del ranks, packed, rows
+        del packed, rows
         torch.cuda.empty_cache()
     print(json.dumps(out))
 
