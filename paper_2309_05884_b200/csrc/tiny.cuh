@@ -68,7 +68,10 @@ __host__ __device__ constexpr int tiny_pad(int d, bool mma) {
 }
 // Three problems per warp (3 x 3 lane grid each, d = 3, 5, 6, 9): lane -> 9 sub + 3 tr + tc
 // (255 = idle), so that every 8-lane shared-memory phase is conflict-free for the own-entry,
-// operand, seed and generator accesses (searched by tools/lane_maps.py with the pads above).
+// operand, seed and generator accesses (searched by tools/lane_maps.py with the pads above).  The
+// search covers those four access patterns only: ncu on the d = 9 sector still counts 12.6% of the
+// shared-load wavefronts as bank conflicts (r01 v12 capture), from the patterns it does
+// not cover (transposed reads of the adjoint products, history staging).
 __host__ __device__ constexpr int tiny_map_id(int d) { return d == 3 ? 0 : d == 5 ? 1 : d == 6 ? 2 : 3; }
 __constant__ unsigned char c_lane_map[4][32] = {
     {0, 9, 10, 15, 19, 255, 255, 255, 11, 12, 13, 14, 16, 17, 26, 255, 18, 20, 21, 22, 23, 24, 25, 255, 1, 2, 3, 4, 5, 6, 7, 8},
