@@ -184,6 +184,7 @@ static __global__ void __launch_bounds__(kSpThreads) spmm_cols_kernel(const SpIt
   }
   __syncthreads();
   const GemmItem g = sp_epi(it, d);
+  const double2* addX = it.add_x ? it.X : nullptr;  // in a register: the stores below may alias the item
   const int lane = threadIdx.x & 31;
   int sl[kSpMaxW];  // rotated slot of step w
 #pragma unroll
@@ -236,8 +237,8 @@ static __global__ void __launch_bounds__(kSpThreads) spmm_cols_kernel(const SpIt
       if (w >= W) break;
       const int cw = sl[w];
       if (cw >= w_here) continue;
-      if (it.add_x) {
-        const double2 x = it.X[(size_t)i * d + c0 + cw];
+      if (addX) {
+        const double2 x = addX[(size_t)i * d + c0 + cw];
         acc[w].x += x.x;
         acc[w].y += x.y;
       }
@@ -278,6 +279,7 @@ static __global__ void __launch_bounds__(kSpThreads) spmm_rows_kernel(const SpIt
   }
   __syncthreads();
   const GemmItem g = sp_epi(it, d);
+  const double2* addX = it.add_x ? it.X : nullptr;  // in a register: the stores below may alias the item
   const int lane = threadIdx.x & 31;
   int sl[kSpMaxW];
 #pragma unroll
@@ -328,8 +330,8 @@ static __global__ void __launch_bounds__(kSpThreads) spmm_rows_kernel(const SpIt
       if (w >= W) break;
       const int rw = sl[w];
       if (rw >= w_here) continue;
-      if (it.add_x) {
-        const double2 x = it.X[(size_t)(i0 + rw) * d + c];
+      if (addX) {
+        const double2 x = addX[(size_t)(i0 + rw) * d + c];
         acc[w].x += x.x;
         acc[w].y += x.y;
       }

@@ -313,6 +313,8 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
   extern __shared__ uint8_t tsm_raw[];
   __shared__ double2 red[G3THREADS / 32][4];
   __shared__ int stage_tile[PT_STAGES];  // tile index announced with a tile's first stage; -1 = done
+  __shared__ int stage_info[PT_STAGES][8];  // with it: item, m0, n0, K stages, item m, item n, local (no global loads
+                                            // between a tile's announcement and its first DMMA)
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + PT_STAGES * PT_SLOT_BYTES);
   uint64_t* empty = full + PT_STAGES;
@@ -352,7 +354,12 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
         for (int kt = 0; kt < kt_total; ++kt, ++g) {
           const uint32_t slot = g % PT_STAGES;
           if (g >= PT_STAGES) mbar_wait(&empty[slot], ((g / PT_STAGES) - 1) & 1);
-          if (kt == 0) stage_tile[slot] = t;
+          if (kt == 0) {
+            stage_tile[slot] = t;
+            stage_info[slot][0] = tr.item; stage_info[slot][1] = tr.m0; stage_info[slot][2] = tr.n0;
+            stage_info[slot][3] = kt_total; stage_info[slot][4] = it.m; stage_info[slot][5] = it.n;
+            stage_info[slot][6] = tr.local;
+          }
           tma_issue_stage<TA, TB>(mp, it, kt, kt_per_seg, tr.m0, tr.n0, a3d, b3d, ring + slot * PT_SLOT_BYTES,
                                   &full[slot]);
         }
@@ -404,10 +411,22 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
     mbar_wait_s(full_s + 8 * slot, phase);
     const int t = *reinterpret_cast<volatile int*>(&stage_tile[slot]);
     if (t < 0) break;
+#ifndef SQOC_TILE_INFO
+#define SQOC_TILE_INFO 1
+#endif
+#if SQOC_TILE_INFO
+    volatile const int* info = stage_info[slot];
+    const GemmItem& it = items[info[0]];
+    const int m0 = info[1], n0 = info[2];
+    const int kt_total = info[3];
+    const int it_m = info[4], it_n = info[5], tile_local = info[6];
+#else
     const TileRef tr = tiles[t];
     const GemmItem& it = items[tr.item];
     const int m0 = tr.m0, n0 = tr.n0;
     const int kt_total = ((it.k + GBK - 1) / GBK) * it.nseg;
+    const int it_m = it.m, it_n = it.n, tile_local = tr.local;
+#endif
     double acc[4][2][3][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -416,7 +435,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
 #pragma unroll
         for (int c = 0; c < 3; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
     int th, tw, WC;
-    const int R = min(8, (it.m - m0 + 7) / 8), Cc = min(8, (it.n - n0 + 7) / 8);
+    const int R = min(8, (it_m - m0 + 7) / 8), Cc = min(8, (it_n - n0 + 7) / 8);
     pt_layout(R, Cc, th, tw, WC);
     const int wri = warp / WC, wci = warp - wri * WC;
     const int wm = wri * th * 8, wn = wci * tw * 8;
@@ -443,6 +462,20 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
     }
     const bool trace = EPI == EPI_TRACE || (EPI == EPI_MIXED && it.nF > 0);  // uniform per tile
     if (!trace) {
+      // the epilogue's item fields in registers: through the reference every store to C forces the
+      // pointers to be loaded again (they may alias), 16 dependent global loads per thread and tile
+#ifndef SQOC_EP_COPY
+#define SQOC_EP_COPY 1
+#endif
+#if SQOC_EP_COPY
+      GemmItem ep{};
+      ep.C = it.C; ep.C2 = it.C2; ep.E0 = it.E0; ep.E1 = it.E1; ep.E2 = it.E2; ep.E3 = it.E3;
+      ep.ldc = it.ldc; ep.diag = it.diag;
+#else
+      const GemmItem& ep = it;
+#endif
+      const int im = it_m, in = it_n;
+      const bool mirror = it.herm && n0 > m0;
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -451,12 +484,12 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
           for (int v = 0; v < 2; ++v) {
             const int m = m0 + wm + mi * 8 + lr;
             const int n = n0 + wn + ni * 8 + 2 * lc + v;
-            if (mi < mc && ni < nc && m < it.m && n < it.n) {
+            if (mi < mc && ni < nc && m < im && n < in) {
               const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
-              epi_store(it, args, m, n, t1 - t2, t3 - t1 - t2);
+              epi_store(ep, args, m, n, t1 - t2, t3 - t1 - t2);
             }
           }
-      if (it.herm && n0 > m0) {  // Hermitian product, tile above the diagonal: (n, m) = conj (m, n)
+      if (mirror) {  // Hermitian product, tile above the diagonal: (n, m) = conj (m, n)
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -465,9 +498,9 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
             for (int v = 0; v < 2; ++v) {
               const int m = m0 + wm + mi * 8 + lr;
               const int n = n0 + wn + ni * 8 + 2 * lc + v;
-              if (mi < mc && ni < nc && m < it.m && n < it.n) {
+              if (mi < mc && ni < nc && m < im && n < in) {
                 const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
-                epi_store(it, args, n, m, t1 - t2, t1 + t2 - t3);
+                epi_store(ep, args, n, m, t1 - t2, t1 + t2 - t3);
               }
             }
       }
@@ -484,7 +517,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
             for (int v = 0; v < 2; ++v) {
               const int p = m0 + wm + mi * 8 + lr;
               const int q = n0 + wn + ni * 8 + 2 * lc + v;
-              if (mi < mc && ni < nc && p < it.m && q < it.n) {
+              if (mi < mc && ni < nc && p < it_m && q < it_n) {
                 const double2 e = F[(size_t)q * it.ldc + p];
                 const double t1 = acc[mi][ni][0][v], t2 = acc[mi][ni][1][v], t3 = acc[mi][ni][2][v];
                 const double cr = args.alpha * (t1 - t2), ci = args.alpha * (t3 - t1 - t2);
@@ -503,7 +536,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
       if (threadIdx.x < nF) {
         double2 s = make_double2(0.0, 0.0);
         for (int w = 0; w < G3THREADS / 32; ++w) { s.x += red[w][threadIdx.x].x; s.y += red[w][threadIdx.x].y; }
-        it.tr_out[(size_t)tr.local * nF + threadIdx.x] = s;
+        it.tr_out[(size_t)tile_local * nF + threadIdx.x] = s;
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(G3THREADS) : "memory");  // red[] reused by the next trace tile
     }
