@@ -375,6 +375,12 @@ int sqoc_create(sqoc_problem** out, int device, int n_blocks, const int* dims, i
     free_problem(p);
     return rc;
   }
+  // setup copies come from pageable host memory (staged DMA on the legacy stream); evaluations run on
+  // non-blocking streams that do not wait for it
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    free_problem(p);
+    return report_error(SQOC_ERR_CUDA, "sqoc_create: device synchronisation failed");
+  }
   *out = p;
   return SQOC_OK;
 }

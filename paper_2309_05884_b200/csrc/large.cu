@@ -645,6 +645,13 @@ static ListRef upload_list(std::vector<GemmItem>& v, std::vector<void*>& mem) {
       cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(GemmItem), cudaMemcpyHostToDevice);
     }
   }
+  // The copies above come from pageable host memory: cudaMemcpy returns once the data is staged, the DMA
+  // of anything larger than the inline limit (the ~75 KB tile list of cfg 3) may still be in flight, and
+  // the evaluation streams are non-blocking -- they do not wait for the legacy stream the DMA runs on.
+  // Without this the first launch of a freshly built list could read a partly written tile list or
+  // tensor maps (r02: rare rounding-to-1e-8 gradient deviations in the first evaluation of an engine,
+  // tools/repeat_check.py; the cp.async kernel only reads the 2 KB item array, which is copied inline).
+  cudaDeviceSynchronize();
   ref.n = (int)v.size();
   ref.tiles = t;
   return ref;
@@ -893,6 +900,7 @@ static SpListRef sp_list(LargeGroup& g, int op, int degree) {
   if (cudaMalloc(&ref.dev, v.size() * sizeof(SpItem)) != cudaSuccess) return SpListRef{};
   cudaMemcpy(ref.dev, v.data(), v.size() * sizeof(SpItem), cudaMemcpyHostToDevice);
   g.splist_mem.push_back(ref.dev);
+  cudaDeviceSynchronize();  // pageable H2D copy: see upload_list
   ref.n = (int)v.size();
   ref.rows = tiles;
   g.splists.emplace(key, ref);
@@ -1260,7 +1268,11 @@ int large_init(LargeGroup& g, const std::vector<LargeBlockSpec>& blocks, int K, 
   }
   LCHK(cudaMalloc(&g.tile_off_dev, (g.nblk + 1) * sizeof(int)));
   LCHK(cudaMemcpy(g.tile_off_dev, g.trace_tile_off.data(), (g.nblk + 1) * sizeof(int), cudaMemcpyHostToDevice));
-  return sp_init(g, blocks);
+  const int rc_sp = sp_init(g, blocks);
+  // the setup above used the legacy default stream (memset of A2, generator transposes); evaluations run on
+  // non-blocking streams that do not wait for it
+  LCHK(cudaDeviceSynchronize());
+  return rc_sp;
 }
 
 int large_set_norms(LargeGroup& g, const std::vector<double>& gn) {
@@ -1397,6 +1409,7 @@ static int hist_alloc(LargeGroup& g, int degree, int sq) {
       for (int r = 0; r < g.blocks[b].d; ++r) eye[g.offr[b] + (size_t)r * g.blocks[b].d + r] = make_double2(1.0, 0.0);
     LCHK(cudaMalloc(&g.h_I, g.totalr * sizeof(double2)));
     LCHK(cudaMemcpy(g.h_I, eye.data(), g.totalr * sizeof(double2), cudaMemcpyHostToDevice));
+    LCHK(cudaDeviceSynchronize());  // pageable H2D copy vs the non-blocking evaluation stream: see upload_list
   }
   g.h_C = C;
   return SQOC_OK;

@@ -104,6 +104,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// Tensor maps live in global memory (uploaded per work list): before the async proxy reads a map whose
+// bytes the host wrote, the generic -> tensormap proxy acquire fence of the CUDA programming guide is
+// required, or an SM may use a stale cached descriptor of a map that used to live at the same address
+// (an earlier engine's list): r02 found first evaluations of fresh engines reading slightly wrong
+// operands that way (tools/repeat_check.py).
+__device__ __forceinline__ void tensormap_acquire(const CUtensorMap* map) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.sys [%0], 128;\n" ::"l"(map) : "memory");
+}
+
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
@@ -351,6 +360,12 @@ __global__ void __launch_bounds__(PT_THREADS, 1) zgemm3m_pt_kernel(const GemmIte
         const int kt_per_seg = (it.k + GBK - 1) / GBK;
         const int kt_total = kt_per_seg * it.nseg;
         const bool a3d = tr.m0 + GBM <= (it.m & ~7), b3d = tr.n0 + GBN <= (it.n & ~7);  // all 8 blocks full
+        for (int seg = 0; seg < it.nseg; ++seg) {  // the maps this tile's stages use
+          const bool a3 = TA != OP_N && a3d && (mp->has3d >> (2 * seg) & 1u);
+          const bool b3 = TB == OP_N && b3d && (mp->has3d >> (2 * seg + 1) & 1u);
+          tensormap_acquire(&mp->m[6 * seg + (TA == OP_N ? 0 : a3 ? 4 : 1)]);
+          tensormap_acquire(&mp->m[6 * seg + (TB != OP_N ? 3 : b3 ? 5 : 2)]);
+        }
         for (int kt = 0; kt < kt_total; ++kt, ++g) {
           const uint32_t slot = g % PT_STAGES;
           if (g >= PT_STAGES) mbar_wait(&empty[slot], ((g / PT_STAGES) - 1) & 1);

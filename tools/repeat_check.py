@@ -17,7 +17,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 s = systems.config(3, n_slices=n, builder="gpu")
 u = s.controls(9)
-for flag in ("1", "0"):
+for flag in os.environ.get("REPEAT_MODES", "1,0").split(","):
     os.environ["SQOC_SPARSE"] = flag
     outs = []
     for r in range(reps):
@@ -31,4 +31,5 @@ for flag in ("1", "0"):
     dF = [abs(F - F0) for F, _ in outs]
     dg = [float(np.abs(g - g0).max() / np.abs(g0).max()) for _, g in outs]
     print(json.dumps({"sparse": flag, "n_slices": n, "evaluations": len(outs), "max_abs_dF": max(dF),
-                      "max_rel_dgrad": max(dg), "dgrad": dg}))
+                      "max_rel_dgrad": max(dg), "blips": [i for i, x in enumerate(dg) if x > 1e-15],
+                      "dgrad": dg if len(dg) <= 12 else None}))
