@@ -790,6 +790,7 @@ static int gemm(LargeGroup& g, int op, int p, int q, int r, GemmArgs a, cudaStre
     g.err = "work list allocation failed";
     return SQOC_ERR_CUDA;
   }
+  if (g.dry) return SQOC_OK;
   gemm_begin(g, l, st);
   cudaError_t e;
   switch (op) {
@@ -937,6 +938,7 @@ static int sp_launch(LargeGroup& g, int op, int degree, GemmArgs a, cudaStream_t
   }
   int rc = sp_smem_attr(g);
   if (rc) return rc;
+  if (g.dry) return SQOC_OK;
   const bool cols = op == SP_F0 || op == SP_B0C || op == SP_B0T || op == SP_B1D || op == SP_B0T1;
   const size_t smem = g.sp_smem * g.sp_w;
   const bool full_w = g.sp_w == kSpMaxW;  // compile-time panel width
@@ -952,6 +954,7 @@ static int sp_launch(LargeGroup& g, int op, int degree, GemmArgs a, cudaStream_t
 // forward scheme step k (< 2) on the sparse A
 // A2 = A A on the squared pattern (step 0 of both schemes is a plain store of the product)
 static int sp_a2(LargeGroup& g, cudaStream_t st) {
+  if (g.dry) return SQOC_OK;
   spgemm_a2_kernel<<<dim3(128, g.nblk), 256, 0, st>>>(g.sp_dev, g.off_dev, g.A2);
   LCHK(cudaGetLastError());
   g.launches++;
@@ -988,6 +991,7 @@ static int sp_pair_step(LargeGroup& g, int k, int degree, GemmArgs a, cudaStream
 }
 
 static int sp_values(LargeGroup& g, int j, const double* u, double scale, cudaStream_t st) {
+  if (g.dry) return SQOC_OK;
   sp_values_kernel<<<dim3(64, g.nblk), 256, 0, st>>>(j, g.K, g.N, u, scale, g.sp_dev);
   LCHK(cudaGetLastError());
   g.launches++;
@@ -998,6 +1002,7 @@ static int sp_values(LargeGroup& g, int j, const double* u, double scale, cudaSt
 static int sp_trace(LargeGroup& g, int j, int p, const LargeArgs& a, int s_idx, cudaStream_t st) {
   int rc = sp_smem_attr(g);
   if (rc) return rc;
+  if (g.dry) return SQOC_OK;
   if (g.sp_w == kSpMaxW)
     sp_trace_kernel<kSpMaxW><<<g.sp_trace_tiles, kSpThreads, g.sp_smem * g.sp_w, st>>>(
         g.sp_trace_dev + (size_t)p * g.nblk, g.nblk, g.sp_dev, g.K, g.sp_w);
@@ -1944,13 +1949,15 @@ static int seq_forward(LargeGroup& g, const double* u, const PolyScheme& sc, int
   const int K = g.K, N = g.N;
   const double scale = std::ldexp(1.0, -sq);
   int rc;
-  if ((rc = bc_init(g, g.X[0], g.L[0], ew_grid, st))) return rc;
+  if (!g.dry && (rc = bc_init(g, g.X[0], g.L[0], ew_grid, st))) return rc;
   int q = 0;
   GemmArgs one{1.0, 0.0, 0.0, 0.0};
   for (int j = 0; j < N; ++j) {
-    build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
-    LCHK(cudaGetLastError());
-    g.launches++;
+    if (!g.dry) {
+      build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
+      LCHK(cudaGetLastError());
+      g.launches++;
+    }
     if (g.sp_on && (rc = sp_values(g, j, u, scale, st))) return rc;
     for (int k = 0; k < sc.nsteps; ++k) {
       if (g.sp_on && k < 2) rc = sp_fwd_step(g, k, sc.degree, step_args(sc.step[k]), st);
@@ -1962,13 +1969,13 @@ static int seq_forward(LargeGroup& g, const double* u, const PolyScheme& sc, int
       if ((rc = gemm(g, F_S, p, 0, 0, one, st))) return rc;
       p ^= 1;
     }
-    if (keep_u)
+    if (keep_u && !g.dry)
       LCHK(cudaMemcpyAsync(g.uh + (size_t)j * g.total, g.T[p], g.total * sizeof(double2), cudaMemcpyDeviceToDevice,
                            st));
     if ((rc = gemm(g, F_X, p, q, 0, one, st))) return rc;
     q ^= 1;
   }
-  g.uh_valid = keep_u;
+  if (!g.dry) g.uh_valid = keep_u;
   *q_out = q;
   return SQOC_OK;
 }
@@ -1984,9 +1991,11 @@ static int seq_backward(LargeGroup& g, const LargeArgs& a, int s_idx, const doub
     if ((rc = gemm(g, B_C, 0, q, 0, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
   }
   for (int j = N - 1; j >= 0; --j) {
-    build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
-    LCHK(cudaGetLastError());
-    g.launches++;
+    if (!g.dry) {
+      build_a_kernel<<<ew_grid, 256, 0, st>>>(j, K, N, u, g.d_dev, g.off_dev, g.gen_dev, scale, g.A, 0);
+      LCHK(cudaGetLastError());
+      g.launches++;
+    }
     if (!g.gate && (rc = gemm(g, B_C, 0, q, r, GemmArgs{scale, 0.0, 0.0, 0.0}, st))) return rc;
     if (g.sp_on && (rc = sp_values(g, j, u, scale, st))) return rc;
     for (int k = 0; k < sc.nsteps; ++k) {
@@ -2007,7 +2016,7 @@ static int seq_backward(LargeGroup& g, const LargeArgs& a, int s_idx, const doub
       if ((rc = gemm(g, have_u && i == sq - 1 ? B_SD : B_S, p, 0, 0, one, st))) return rc;
       p ^= 1;
     }
-    if (have_u)  // U_j into the slot the value product would have written (Y = T[0] at s = 0, else T[p])
+    if (have_u && !g.dry)  // U_j into the slot the value product would have written (Y = T[0] at s = 0, else T[p])
       LCHK(cudaMemcpyAsync(g.T[p], g.uh + (size_t)j * g.total, g.total * sizeof(double2), cudaMemcpyDeviceToDevice,
                            st));
     if (g.gate && g.sp_on) {  // M = U^dag Ad on the tensor cores, the trace on the sparse a_k
@@ -2015,10 +2024,12 @@ static int seq_backward(LargeGroup& g, const LargeArgs& a, int s_idx, const doub
       if ((rc = sp_trace(g, j, p, a, s_idx, st))) return rc;
     } else {
       if ((rc = gemm(g, g.gate ? B_UC : B_D, p, 0, 0, one, st))) return rc;
-      trace_reduce_kernel<<<nblk, 256, 0, st>>>(j, K, N, g.tile_off_dev, g.trace_part, g.tau_dev, g.w_dev,
-                                                g.gidx_dev, a.gradb + (size_t)s_idx * K * N, a.gradb_block_stride);
-      LCHK(cudaGetLastError());
-      g.launches++;
+      if (!g.dry) {
+        trace_reduce_kernel<<<nblk, 256, 0, st>>>(j, K, N, g.tile_off_dev, g.trace_part, g.tau_dev, g.w_dev,
+                                                  g.gidx_dev, a.gradb + (size_t)s_idx * K * N, a.gradb_block_stride);
+        LCHK(cudaGetLastError());
+        g.launches++;
+      }
     }
     if (g.gate) {  // C_{j-1} = U^dag C_j U
       if (j > 0 && (rc = gemm(g, B_CU, p, 0, 0, one, st))) return rc;
@@ -2266,6 +2277,22 @@ int large_carry_time(LargeGroup& g, double* ms) {
 
 // ------------------------------------------------------------------ evaluation
 int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
+  // First evaluation of a group on the persistent TMA kernel: run it once and discard the result.  r02
+  // measured (tools/repeat_check.py, tools/stale_check.py): the first evaluation of a fresh engine
+  // deviates intermittently by 1e-14 .. 1e-8 relative in the gradient, every later evaluation -- same or
+  // different controls -- is bit-identical to the steady-state value (0 deviations in ~200), and the
+  // cp.async kernel never deviates.  Not explained yet (not the lazy list setup, not staged host copies,
+  // not tensor-map visibility: each was removed without effect; a timing window that only cold page
+  // tables / TLBs open is the remaining suspect), so the cold pass is spent before the result counts.
+  // SQOC_GEMM_TMA=0 selects the cp.async kernel and skips this.
+  if (!g.warmed) {
+    g.warmed = true;
+    static const bool off = [] { const char* e = getenv("SQOC_WARM"); return e && e[0] == '0'; }();
+    if (!off && use_3m() && staging() == 1) {
+      const int rc0 = large_eval(g, a, st);
+      if (rc0) return rc0;
+    }
+  }
   const int N = g.N, K = g.K, nblk = g.nblk;
   int maxd = 0;
   for (auto& b : g.blocks) maxd = std::max(maxd, b.d);
@@ -2340,6 +2367,19 @@ int large_eval(LargeGroup& g, const LargeArgs& a, cudaStream_t st) {
     }
     int q = 0;
     const bool keep = uh_ensure(g);
+    if (g.seq_ready_key != sc.degree * 100 + sq) {  // build every list of this plan before anything runs
+      const int n_save = g.N;
+      g.dry = true;
+      g.N = std::min(n_save, 2);  // two slices reach both parities of the ping-pong buffers
+      int qd = 0;
+      rc = seq_forward(g, u, sc, sq, ew_grid, st, &qd, keep);
+      for (int qq = 0; qq < 2 && rc == SQOC_OK; ++qq) rc = seq_backward(g, a, s, u, sc, sq, qq, ew_grid, st, keep);
+      g.dry = false;
+      g.N = n_save;
+      if (rc) return rc;
+      LCHK(cudaDeviceSynchronize());
+      g.seq_ready_key = sc.degree * 100 + sq;
+    }
     if ((rc = seq_forward(g, u, sc, sq, ew_grid, st, &q, keep))) return rc;
     if ((rc = bc_tau(g, g.X[q], a, s, st))) return rc;
     if ((rc = seq_backward(g, a, s, u, sc, sq, q, ew_grid, st, keep))) return rc;

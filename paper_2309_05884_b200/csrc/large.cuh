@@ -107,6 +107,12 @@ struct LargeGroup {
   // ---- sparse generators (sparse.cuh): the scheme's products with A as a factor and the gradient
   // trace run as sparse x dense kernels in the slice-sequential schedule when every block's pattern is
   // sparse enough (sp_on; SQOC_SPARSE=0 disables) ----
+  // dry pass: the slice-sequential driver runs once without launching anything so that every work list it
+  // needs (tile lists, tensor maps, sparse items: cudaMalloc + host-to-device copies) exists before the
+  // first kernel of an evaluation starts
+  bool warmed = false;                     // first evaluation repeated once (large_eval)
+  bool dry = false;
+  int seq_ready_key = -1;                  // scheme degree * 100 + squarings the lists were prepared for
   bool sp_on = false;
   bool sp_a2 = false;                      // A2 = A A by spgemm_a2_kernel (SQOC_SPGEMM=0 disables)
   SpBlockDev* sp_dev = nullptr;            // [nblk]
