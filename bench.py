@@ -553,6 +553,7 @@ def run_sharded(args):
             gsys = parallel.local_system(s, 0, 2)
             gu, fz, gz = gsys.controls(11), float(z["cfg4_full_F"]), z["cfg4_full_grad"]
         gobj = parallel.ShardedObjective(gsys, comm, factory, n_block_groups=groups)
+        gobj.objective(gu)  # the chunk entry points have no discarded first evaluation
         Fz, gzz = gobj.objective(gu)
         gobj.eng.close()
         del gobj
